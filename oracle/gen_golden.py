@@ -1,0 +1,260 @@
+"""Generate tests/golden/*.npz from the REFERENCE implementation itself.
+
+TEST INFRASTRUCTURE ONLY.  Run in the build container, where the reference
+is importable (oracle/_ref built by oracle/build_ref.sh, or the read-only
+source tree /root/reference/pkg/src).  The committed fixtures pin both the
+oracle restatement (oracle/oracle.py, oracle/mrs_oracle.c) and the device
+path, and travel to the GPU box where the reference does not exist.
+
+    python oracle/gen_golden.py            # rewrites tests/golden/
+
+Every fixture stores the seeded inputs next to the reference outputs, so
+tests never need the reference at run time.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+OUT = os.path.join(ROOT, "tests", "golden")
+
+
+def import_reference():
+    os.environ.setdefault("MRSOLVE_KERNELS", "cython")
+    for cand in (os.path.join(HERE, "_ref"), "/root/reference/pkg/src"):
+        if os.path.isdir(os.path.join(cand, "mrsolve")):
+            sys.path.insert(0, cand)
+            break
+    import mrsolve  # noqa: F401
+    return mrsolve
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
+
+
+def gen_kernels(ms, rng):
+    """Plugin KATs: csr_spmv over widths x precisions x modes x m, plus the
+    blocked vector kernels (kernels/__init__.py:27-41)."""
+    K = ms.kernels
+    from mrsolve.core import CsrBlock, IndexWidth, compress_indices
+    out = {}
+    cases = []
+    for ci, (n, ncols, dens, m) in enumerate([(37, 29, 0.3, 1), (64, 200, 0.1, 2),
+                                              (150, 150, 0.05, 4), (300, 1000, 0.01, 8),
+                                              (97, 66000, 0.0005, 1), (40, 40, 0.5, 16),
+                                              (33, 33, 0.2, 32), (20, 20, 0.0, 2)]):
+        a = rng.standard_normal((n, ncols)) * (rng.random((n, ncols)) < dens)
+        if ci == 4:  # empty rows interleaved
+            a[::3] = 0.0
+        blk = CsrBlock.from_dense(a)
+        x = rng.standard_normal((ncols, m))
+        b = rng.standard_normal((n, m))
+        y0 = rng.standard_normal((n, m))
+        out[f"spmv{ci}_x"], out[f"spmv{ci}_b"], out[f"spmv{ci}_y0"] = x, b, y0
+        for width in (IndexWidth.W8, IndexWidth.W16, IndexWidth.W32):
+            if blk.ncols > width.capacity:
+                continue
+            wb = compress_indices(blk, width)
+            for vdt in (np.float64, np.float32):
+                key = f"spmv{ci}_w{int(width)}_{np.dtype(vdt).name}"
+                out[key + "_rp"] = wb.row_ptr
+                out[key + "_ci"] = wb.col_idx
+                out[key + "_v"] = wb.values.astype(vdt)
+                for mode in range(4):
+                    y = y0.copy()
+                    K.csr_spmv(wb.row_ptr, wb.col_idx, wb.values.astype(vdt), x, y,
+                               mode, b=b if mode == 3 else None)
+                    out[f"{key}_out{mode}"] = y
+                cases.append(key)
+    out["spmv_cases"] = np.array(cases)
+    # blocked vector kernels
+    vcases = []
+    for vi, (n, m) in enumerate([(1, 1), (257, 1), (1000, 2), (333, 4), (1031, 8),
+                                 (300, 16), (129, 32), (50, 3)]):
+        x, y, u, v, w, z, s = (rng.standard_normal((n, m)) for _ in range(7))
+        a, bb, c = (rng.standard_normal(m) for _ in range(3))
+        key = f"vec{vi}"
+        for nm, arr in dict(x=x, y=y, u=u, v=v, w=w, z=z, s=s, a=a, bb=bb, c=c).items():
+            out[f"{key}_{nm}"] = arr
+        t = y.copy(); K.axpby(a, x, bb, t); out[key + "_axpby"] = t
+        t = y.copy(); K.add2_scaled(t, a, u, bb, v); out[key + "_add2"] = t
+        out[key + "_dot"] = K.dot_partial(x, y)
+        t = y.copy(); out[key + "_ud_dot"] = K.fused_update_dot(a, x, bb, t)
+        out[key + "_ud_y"] = t
+        t1, t2 = y.copy(), w.copy()  # y2 output buffer distinct from w
+        K.fused_paired_update(t1, a, u, bb, s, t2, c, x)
+        out[key + "_pu_y1"], out[key + "_pu_y2"] = t1, t2
+        t = y.copy()
+        d1, d2 = K.fused_update_dot2(t, u, c, w, z)
+        out[key + "_ud2_y"], out[key + "_ud2_d1"], out[key + "_ud2_d2"] = t, d1, d2
+        vcases.append(key)
+    out["vec_cases"] = np.array(vcases)
+    np.savez_compressed(os.path.join(OUT, "kernels.npz"), **out)
+
+
+def tree(ms, roles):
+    t = ms.ParamTree()
+    for role, entries in roles.items():
+        t.add_map(role, {k: str(v) for k, v in entries.items()})
+    t.set_defaults()
+    return t
+
+
+SOLVE_CASES = {
+    # name: (grid, m, seed, roles)  -- shrunken BASELINE.json configs 1-3
+    "c1_jacobi_pcg": ((12, 12, 12), 4, 0, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "Jacobi"}}),
+    "c2_amg_pcg": ((16, 16, 16), 4, 0, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "MultiGrid"},
+        "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+        "post_smoother": {"method": "Jacobi", "weight": "0.8"}}),
+    "c3_amg_bicgstab_mixed": ((16, 16, 16), 4, 0, {
+        "solver": {"method": "BiCGStab", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "MultiGrid", "mg_mixed_precision": "1"},
+        "pre_smoother": {"method": "Chebyshev", "polynomial_order": "2"},
+        "post_smoother": {"method": "Chebyshev", "polynomial_order": "2"}}),
+    "c2_amg_pcg_20": ((20, 18, 16), 2, 7, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-10"},
+        "preconditioner": {"method": "MultiGrid", "mg_coarse_matrix_size": "100"},
+        "pre_smoother": {"method": "Jacobi", "weight": "0.8", "max_iters": "2"},
+        "post_smoother": {"method": "Jacobi", "weight": "0.8"}}),
+    "plain_bicgstab": ((10, 10, 10), 3, 1, {
+        "solver": {"method": "BiCGStab", "rel_tolerance": "1e-9"}}),
+    "plain_cg": ((10, 10, 10), 2, 2, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-9"}}),
+    "c3_amg_bicgstab_full_cheb3": ((14, 14, 14), 2, 3, {
+        "solver": {"method": "BiCGStab", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "MultiGrid"},
+        "pre_smoother": {"method": "Chebyshev", "polynomial_order": "3"},
+        "post_smoother": {"method": "Chebyshev", "polynomial_order": "1"}}),
+}
+
+
+def gen_solves(ms):
+    from mrsolve.core import BlockVector
+    from mrsolve.io import gen_poisson3d
+    out = {}
+    for name, (grid, m, seed, roles) in SOLVE_CASES.items():
+        A, _ = gen_poisson3d(*grid)
+        n = A.nrows
+        B = np.random.default_rng(seed).uniform(-1.0, 1.0, (n, m))
+        cfg = tree(ms, roles)
+        cs = ms.prepare(cfg, A)
+        X = BlockVector.zeros(n, m)
+        st = cs.run(BlockVector.from_array(B), X)
+        out[f"{name}_B"] = B
+        out[f"{name}_X"] = X.data
+        out[f"{name}_iters"] = np.int64(st.iterations)
+        out[f"{name}_rel"] = st.final_rel_residual
+        out[f"{name}_hist"] = np.array(st.residual_history)
+        h = cs.hierarchy
+        if h is not None:
+            out[f"{name}_nlevels"] = np.int64(h.nlevels)
+            for l, lv in enumerate(h.levels):
+                Ag = lv.A.blocks[0].diag   # 1x1 topology: stored precision
+                out[f"{name}_L{l}_A_shape"] = np.array([Ag.nrows, Ag.nnz])
+                out[f"{name}_L{l}_eig"] = np.array(lv.eig_bounds if lv.eig_bounds
+                                                   else [np.nan, np.nan])
+                for tag, blk in (("A", Ag), ("P", lv.P), ("R", lv.R)):
+                    if blk is None:
+                        continue
+                    out[f"{name}_L{l}_{tag}_sha"] = np.array(
+                        [sha(blk.row_ptr), sha(blk.col_idx.astype(np.int64)),
+                         sha(blk.values)])
+                    out[f"{name}_L{l}_{tag}_dtype"] = np.array(str(blk.values.dtype))
+        print(f"{name}: n={n} m={m} iters={st.iterations} "
+              f"levels={h.nlevels if h is not None else '-'} "
+              f"maxrel={st.final_rel_residual.max():.3e}")
+    out["solve_cases"] = np.array(list(SOLVE_CASES))
+    np.savez_compressed(os.path.join(OUT, "solves.npz"), **out)
+
+
+def gen_hierarchies(ms):
+    """Full level arrays for small problems: the AMG-setup upload contract
+    (amg.py:199-308), used to pin the native setup restatement bitwise."""
+    from mrsolve.amg import AmgParams, setup
+    from mrsolve.io import gen_poisson3d
+    sys.path.insert(0, ROOT)
+    from paper_2103_07329_b200.io import gen_stencil27_aniso
+    out = {}
+    probs = {
+        "p7_12": (gen_poisson3d(12, 12, 12)[0], AmgParams(), False),
+        "p7_16_mixed": (gen_poisson3d(16, 16, 16)[0], AmgParams(), True),
+        "p7_9x7x5_c50": (gen_poisson3d(9, 7, 5)[0], AmgParams(coarse_matrix_size=50), False),
+        "p27_10": (gen_stencil27_aniso(10, seed=4), AmgParams(), False),
+        "p7_12_agg": (gen_poisson3d(12, 12, 12)[0],
+                      AmgParams(agg_num_levels=1, num_paths=2), False),
+    }
+    for name, (A, prm, mixed) in probs.items():
+        h = setup(A, prm, mixed_precision=mixed)
+        out[f"{name}_nlevels"] = np.int64(h.nlevels)
+        for l, lv in enumerate(h.levels):
+            for tag, blk in (("A", lv.A.blocks[0].diag), ("P", lv.P), ("R", lv.R)):
+                if blk is None:
+                    continue
+                out[f"{name}_L{l}_{tag}_rp"] = blk.row_ptr
+                out[f"{name}_L{l}_{tag}_ci"] = blk.col_idx
+                out[f"{name}_L{l}_{tag}_v"] = blk.values
+                out[f"{name}_L{l}_{tag}_shape"] = np.array([blk.nrows, blk.ncols])
+        out[f"{name}_A_rp"] = A.row_ptr
+        out[f"{name}_A_ci"] = A.col_idx
+        out[f"{name}_A_v"] = A.values
+        out[f"{name}_A_shape"] = np.array([A.nrows, A.ncols])
+        out[f"{name}_params"] = np.array([prm.strength_threshold, prm.agg_num_levels,
+                                          prm.num_paths, prm.coarse_matrix_size,
+                                          prm.max_levels, float(mixed)])
+        print(f"{name}: levels={h.nlevels} rows={[lv.nrows for lv in h.levels]}")
+    out["hier_cases"] = np.array(list(probs))
+    np.savez_compressed(os.path.join(OUT, "hierarchies.npz"), **out)
+
+
+def gen_generators(ms):
+    from mrsolve.io import gen_poisson3d
+    out = {}
+    for dims in ((2, 1, 1), (3, 4, 5), (8, 8, 8)):
+        A, b = gen_poisson3d(*dims)
+        key = "poisson_%dx%dx%d" % dims
+        out[key + "_rp"], out[key + "_ci"], out[key + "_v"] = A.row_ptr, A.col_idx, A.values
+        out[key + "_b"] = b.data
+    np.savez_compressed(os.path.join(OUT, "generators.npz"), **out)
+
+
+def gen_eig(ms):
+    from mrsolve.core import CsrBlock, SegmentedMatrix
+    from mrsolve.io import gen_poisson3d
+    from mrsolve.solvers import estimate_eig_bounds
+    out = {}
+    A, _ = gen_poisson3d(9, 8, 7)
+    out["p7_987"] = np.array(estimate_eig_bounds(SegmentedMatrix.from_global(A)))
+    A32 = A.with_precision(ms.PrecisionTag.REDUCED)
+    out["p7_987_f32"] = np.array(estimate_eig_bounds(SegmentedMatrix.from_global(A32)))
+    out["eye32"] = np.array(estimate_eig_bounds(
+        SegmentedMatrix.from_global(CsrBlock.from_dense(np.eye(32)))))
+    np.savez_compressed(os.path.join(OUT, "eig.npz"), **out)
+
+
+def main():
+    ms = import_reference()
+    assert ms.kernels.BACKEND == "cython", ms.kernels.BACKEND
+    os.makedirs(OUT, exist_ok=True)
+    rng = np.random.default_rng(20240817)
+    gen_kernels(ms, rng)
+    gen_generators(ms)
+    gen_eig(ms)
+    gen_solves(ms)
+    gen_hierarchies(ms)
+    for f in sorted(os.listdir(OUT)):
+        print(f, os.path.getsize(os.path.join(OUT, f)))
+
+
+if __name__ == "__main__":
+    main()
