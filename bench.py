@@ -1,0 +1,411 @@
+#!/usr/bin/env python
+"""Benchmark: AMG-PCG RHS*iterations/s on BASELINE.json config 2, plus the
+blocked-SpMM HBM roofline (config 5 sweep).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+Workload (N=1): 64^3 7-point Poisson (reference generator), m = 8 seeded
+uniform[-1,1] right-hand sides, zero initial guess, classical RS AMG V(1,1)
+with weighted Jacobi (w = 0.8) preconditioning CG, fp64, tol 1e-8.  A step
+is one whole solve with B, X resident in HBM; setup (prepare) is excluded,
+like the reference's bench (src/cli.py:111-146).  L2 is flushed (256 MB
+write) between timed steps, outside the per-step CUDA events.
+
+N > 1 (torchrun): each rank solves its own replica of the workload (weak
+scaling, "parallelism": "replicas") until the row-partitioned path lands.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref,
+mrsolve with its Cython kernels) on this host, same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "AMG-PCG RHS·iterations/sec; blocked SpMM HBM GB/s vs roofline"
+UNIT = "RHS*it/s"
+GRID, M, SEED, TOL = 64, 8, 0, 1e-8
+WORKLOAD = ("C2: 3D Poisson 7-pt 64^3 (n=262144), m=8 seeded uniform[-1,1] RHS, zero guess, "
+            "classical RS AMG V(1,1) weighted-Jacobi (w=0.8) + PCG, fp64, tol 1e-8")
+ROLES = {"solver": {"method": "CG", "rel_tolerance": str(TOL)},
+         "preconditioner": {"method": "MultiGrid"},
+         "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+         "post_smoother": {"method": "Jacobi", "weight": "0.8"}}
+REF_SNIPPET = r"""
+import json, sys, time, numpy as np
+import mrsolve
+from mrsolve.core import BlockVector
+from mrsolve.io import gen_poisson3d
+grid, m, seed, tol, steps, warmup = {grid}, {m}, {seed}, {tol}, {steps}, {warmup}
+roles = {roles}
+A, _ = gen_poisson3d(grid, grid, grid)
+B = np.random.default_rng(seed).uniform(-1.0, 1.0, (A.nrows, m))
+t = mrsolve.ParamTree()
+for role, e in roles.items():
+    t.add_map(role, e)
+t.set_defaults()
+t0 = time.perf_counter()
+cs = mrsolve.prepare(t, A)
+setup = time.perf_counter() - t0
+out = []
+for k in range(warmup + steps):
+    X = BlockVector.zeros(A.nrows, m)
+    t0 = time.perf_counter()
+    st = cs.run(BlockVector.from_array(B), X)
+    dt = time.perf_counter() - t0
+    if k >= warmup:
+        out.append((dt, st.iterations, float(st.final_rel_residual.max())))
+print("REFJSON" + json.dumps(dict(setup=setup, runs=out, backend=mrsolve.kernels.BACKEND)))
+"""
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-spmm", action="store_true", help="skip the config-5 SpMM sweep")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--quick", action="store_true", help="small SpMM sweep (m=8 only)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# clocks (nvidia-smi sampled during the timed region)
+# ---------------------------------------------------------------------------
+
+REASONS = [("gpu_idle", 0x1), ("applications_clocks_setting", 0x2), ("sw_power_cap", 0x4),
+           ("hw_slowdown", 0x8), ("sync_boost", 0x10), ("sw_thermal_slowdown", 0x20),
+           ("hw_thermal_slowdown", 0x40), ("hw_power_brake_slowdown", 0x80),
+           ("display_clock_setting", 0x100)]
+
+
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.f = None
+
+    def __enter__(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 3:
+                    try:
+                        rows.append((float(p[0]), float(p[1]), int(p[2], 16)))
+                    except ValueError:
+                        pass
+        os.unlink(self.f.name)
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = sorted(r[0] for r in rows)
+        mask = 0
+        for r in rows:
+            mask |= r[2]
+        reasons = [nm for nm, bit in REASONS if mask & bit and nm != "gpu_idle"]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+# ---------------------------------------------------------------------------
+# reference arm / cpu baseline
+# ---------------------------------------------------------------------------
+
+def run_reference_cpu(steps: int, warmup: int, timeout: float = 900.0):
+    """Run the reference (oracle/_ref: mrsolve + its Cython kernels) on this
+    host's CPU, pinned to one core (its kernels hold the GIL: one core is its
+    fastest configuration)."""
+    ref = os.path.join(ROOT, "oracle", "_ref")
+    if not os.path.isdir(os.path.join(ref, "mrsolve")):
+        return None, "oracle/_ref missing (run oracle/build_ref.sh)"
+    code = REF_SNIPPET.format(grid=GRID, m=M, seed=SEED, tol=TOL, steps=steps, warmup=warmup,
+                              roles=repr(ROLES))
+    env = dict(os.environ, PYTHONPATH=ref, MRSOLVE_KERNELS="cython", OMP_NUM_THREADS="1",
+               OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    cmd = [sys.executable, "-c", code]
+    try:
+        cmd = ["taskset", "-c", str(sorted(os.sched_getaffinity(0))[0])] + cmd
+    except Exception:
+        pass
+    r = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=timeout)
+    for line in r.stdout.splitlines():
+        if line.startswith("REFJSON"):
+            return json.loads(line[7:]), None
+    return None, (r.stderr or r.stdout)[-400:]
+
+
+def reference_arm(args, rank):
+    if rank != 0:
+        return
+    res, err = run_reference_cpu(args.steps, args.warmup)
+    ncores = os.cpu_count()
+    if res is None:
+        print(json.dumps({"impl": "reference", "unavailable": f"reference CPU run failed: {err}"}))
+        return
+    runs = res["runs"]
+    tot = sum(r[0] for r in runs)
+    its = [r[1] for r in runs]
+    val = M * sum(its) / tot
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": len(runs), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(runs),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: reference gen_poisson3d + default_rng(0).uniform(-1,1) RHS",
+        "config": {"workload": WORKLOAD, "n": GRID ** 3, "m": M, "iterations": its[0],
+                   "parallelism": "1 CPU core (reference kernels hold the GIL)",
+                   "setup_s_excluded": res["setup"]},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "reference",
+                         "sample": f"{len(runs)} full C2 solves after {args.warmup} warm-up, "
+                                   f"1 of {ncores} host cores, mrsolve backend {res['backend']}"},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------------------
+# B200 arm
+# ---------------------------------------------------------------------------
+
+def spmm_sweep(torch, K, quick: bool):
+    """Config 5: blocked SpMM GB/s against the HBM roofline (ASSIGN mode)."""
+    from paper_2103_07329_b200.io import gen_random_sdd
+    t0 = time.time()
+    A = gen_random_sdd()
+    gen_s = time.time() - t0
+    peak, _ = peak_hbm()
+    out = []
+    ms_list = [8] if quick else [1, 2, 4, 8, 16, 32]
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for vdt in ("f64", "f32"):
+        vals = A.values if vdt == "f64" else A.values.astype("float32")
+        D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols)
+        for m in ms_list:
+            x = torch.rand(A.ncols, m, dtype=torch.float64, device="cuda")
+            y = torch.empty(A.nrows, m, dtype=torch.float64, device="cuda")
+            for _ in range(3):
+                K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
+            times = []
+            for _ in range(10):
+                flush.add_(1)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
+                e1.record()
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1) * 1e-3)
+            t = sorted(times)[len(times) // 2]
+            vb = 8 if vdt == "f64" else 4
+            byts = A.nnz * (vb + 4) + (A.nrows + 1) * 4 + 2 * A.nrows * m * 8
+            out.append({"m": m, "values": vdt, "idx": "u32", "us": t * 1e6,
+                        "GBps": byts / t / 1e9, "frac": byts / t / 1e9 / peak})
+            del x, y
+        del D
+    return {"n": A.nrows, "nnz": A.nnz, "gen_s": gen_s, "points": out}
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        reference_arm(args, rank)
+        return
+    import numpy as np
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2103_07329_b200 import BlockVector, gen_poisson3d, kernels as K
+    from paper_2103_07329_b200.params import tree
+    from paper_2103_07329_b200.solvers import prepare
+
+    A, _ = gen_poisson3d(GRID, GRID, GRID)
+    n = A.nrows
+    B = np.random.default_rng(SEED).uniform(-1.0, 1.0, (n, M))
+    t0 = time.perf_counter()
+    cs = prepare(tree(ROLES), A)
+    plan = cs.plan_factory(M)
+    setup_s = time.perf_counter() - t0
+    Bd = torch.from_numpy(B).cuda()
+    Xd = torch.zeros_like(Bd)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+
+    for _ in range(max(args.warmup, 3)):
+        st = cs.run(Bd, Xd, x_is_zero=True)
+    iters = st.iterations
+    assert st.all_converged, "warm-up solve did not converge"
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    step_t = []
+    with ClockSampler(local) as clk:
+        barrier()
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.add_(1)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            st = cs.run(Bd, Xd, x_is_zero=True)
+            e1.record()
+            e1.synchronize()
+            step_t.append(e0.elapsed_time(e1) * 1e-3)
+            assert st.iterations == iters
+        barrier()
+        wall = time.perf_counter() - wall0
+    clocks = clk.summary()
+    t_dev = sum(step_t)
+    if dist is not None:
+        tt = torch.tensor([t_dev], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_dev = float(tt.item())
+    value = world * M * iters * args.steps / t_dev
+
+    # e2e through the public API with pinned host buffers
+    Bh = torch.from_numpy(B).pin_memory()
+    Xh = torch.zeros(n, M, dtype=torch.float64).pin_memory()
+    Bv = BlockVector(Bh.numpy())
+    e2e_t = []
+    for k in range(args.warmup + args.steps):
+        Xv = BlockVector.zeros(n, M)
+        Xv.data = Xh.numpy()
+        Xv.flags.zero = True
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        st2 = cs.run(Bv, Xv)
+        dt = time.perf_counter() - t0
+        if k >= args.warmup:
+            e2e_t.append(dt)
+    assert st2.iterations == iters
+    e2e_val = world * M * iters * len(e2e_t) / sum(e2e_t)
+    err = float(np.abs(Xh.numpy() - Xd.cpu().numpy()).max())
+
+    # roofline: the dominant kernel (fine-level SpMM, residual form b - A x, m=8)
+    peak, peak_src = peak_hbm()
+    D0 = K.DeviceCsr.from_block(A)
+    Rd = torch.empty_like(Bd)
+    for _ in range(5):
+        K.csr_spmv(D0, None, None, Xd, Rd, K.MODE_RSUB, Bd)
+    reps = 50
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(reps):
+        K.csr_spmv(D0, None, None, Xd, Rd, K.MODE_RSUB, Bd)
+    e1.record()
+    torch.cuda.synchronize()
+    kt = e0.elapsed_time(e1) * 1e-3 / reps
+    kbytes = A.nnz * 12 + (n + 1) * 4 + 3 * n * M * 8
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("spmm_rsub_c2_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roof = {"bound": "hbm", "achieved": kbytes / kt / 1e9, "peak": peak, "unit": "GB/s",
+            "frac": kbytes / kt / 1e9 / peak, "traffic": traffic,
+            "kernel": "spmm_kernel<8, OP_SPMV(RSUB), double, uint32> on A0 (C2 fine level)",
+            "algorithmic_bytes": kbytes, "us_per_launch": kt * 1e6, "peak_source": peak_src}
+
+    sweep = None
+    if not args.no_spmm and rank == 0:
+        sweep = spmm_sweep(torch, K, args.quick)
+
+    cpu = None
+    if not args.no_cpu and rank == 0 and world == 1:
+        res, errs = run_reference_cpu(steps=1, warmup=0, timeout=600)
+        if res is not None:
+            r = res["runs"][0]
+            cpu = {"value": M * r[1] / r[0], "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"1 full C2 solve ({r[1]} iterations, {r[0]:.2f} s) after a "
+                             f"{res['setup']:.1f} s reference setup; 1 of {os.cpu_count()} "
+                             f"host cores, mrsolve {res['backend']} kernels"}
+        else:
+            cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {errs}"}
+
+    launches = plan.kernel_launches(iters) * args.steps
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * t_dev / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic: reference 7-pt Poisson generator + default_rng(0).uniform(-1,1) RHS",
+            "config": {"workload": WORKLOAD, "n": n, "m": M, "iterations": iters,
+                       "levels": cs.hierarchy.nlevels,
+                       "kernels_per_iteration": plan.kernels_per_iteration,
+                       "parallelism": "single GPU" if world == 1 else f"{world} replicas",
+                       "l2": "flushed (256 MB write) between timed steps, outside the events",
+                       "setup_s_excluded": setup_s, "wall_s_timed_region": wall,
+                       "iteration_algorithmic_bytes": plan.iteration_bytes,
+                       "final_rel_residual_max": float(st.final_rel_residual.max())},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n * M * 8,
+                    "d2h_bytes_per_step": n * M * 8,
+                    "note": "public API run() on pinned host BlockVectors; H2D of B and D2H of "
+                            "X inside the timed region", "max_abs_diff_vs_device_run": err},
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if sweep is not None:
+            line["spmm_sweep"] = sweep
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,210 @@
+/*
+ * mrsolve_b200.h -- C ABI of the B200-native multi-RHS AMG-Krylov solve path.
+ *
+ * Plain C: pointers, sizes, int status codes; no torch or C++ types.  Built
+ * into paper_2103_07329_b200/libmrsolve_b200.so (sm_100a).
+ *
+ * Two layers, mirroring the two boundaries of the reference package
+ * (/root/reference/pkg/src/mrsolve):
+ *
+ *  1. Kernel plugin  -- replaces the `mrsolve.kernels` backend module
+ *     (src/kernels/__init__.py:27-41, compiled twin src/kernels/_ckernels.pyx).
+ *     Same operations, same arithmetic order, on DEVICE pointers, enqueued on
+ *     a caller-supplied cudaStream_t (passed as void*).  Asynchronous.
+ *
+ *  2. Solver plan    -- replaces `solvers.prepare(config, A, team).run(B, X)`
+ *     (src/solvers.py:850-959).  An opaque plan owns the uploaded AMG
+ *     hierarchy (src/amg.py:199-239), the device workspaces and the captured
+ *     CUDA graph of the whole solve; `mrs_plan_solve` runs one solve and
+ *     returns SolveStats fields (src/solvers.py:80-92).
+ *
+ *  3. Native host setup -- the reference's Ruge-Stueben setup
+ *     (src/amg.py:55-308) and eigenvalue-bound estimate (src/solvers.py:
+ *     486-517), re-implemented in C++ with bitwise-identical output, so the
+ *     uploaded hierarchy is the reference's.
+ *
+ * Conventions: vectors are (n, m) row-major float64 ("RHS-interleaved",
+ * reference core.py:94-143).  Matrix values are float32 or float64
+ * (val_bytes 4/8); column indices uint8/uint16/uint32 (idx_bytes 1/2/4).
+ * Device CSR row pointers are int32 (nnz < 2^31); host CSR row pointers are
+ * int64 like the reference's CsrBlock.
+ */
+#ifndef MRSOLVE_B200_H
+#define MRSOLVE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define MRS_OK               0
+#define MRS_ERR_ARG          1   /* bad shape / dtype / mode / alias          */
+#define MRS_ERR_CUDA         2   /* CUDA runtime error                          */
+#define MRS_ERR_UNSUPPORTED  3   /* configuration not on the device path        */
+#define MRS_ERR_ALLOC        4   /* device or host allocation failed            */
+#define MRS_ERR_BREAKDOWN    5   /* Krylov breakdown (column in stats)          */
+#define MRS_ERR_SINGULAR     6   /* zero / missing diagonal                     */
+#define MRS_ERR_DEGENERATE   7   /* AMG setup degeneracy after the retry        */
+#define MRS_ERR_STATE        8   /* call out of order (e.g. solve before finalize) */
+
+/* csr_spmv accumulation modes (reference kernels/python_ref.py:24-27) */
+#define MRS_MODE_ASSIGN 0   /* y  = A x     */
+#define MRS_MODE_ADD    1   /* y += A x     */
+#define MRS_MODE_SUB    2   /* y -= A x     */
+#define MRS_MODE_RSUB   3   /* y  = b - A x */
+
+/* Device CSR view.  All pointers are device pointers owned by the caller. */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    const int32_t* row_ptr;   /* nrows + 1 */
+    const void* col_idx;      /* nnz entries of idx_bytes */
+    const void* values;       /* nnz entries of val_bytes */
+    int32_t idx_bytes;        /* 1, 2 or 4 */
+    int32_t val_bytes;        /* 4 or 8 */
+} mrs_csr;
+
+/* Host CSR (the reference CsrBlock layout, core.py:146-254). */
+typedef struct {
+    int64_t nrows, ncols, nnz;
+    const int64_t* row_ptr;
+    const void* col_idx;
+    const void* values;
+    int32_t idx_bytes;
+    int32_t val_bytes;
+} mrs_host_csr;
+
+/* ---- 1. kernel plugin (src/kernels/__init__.py:27-41) ------------------ */
+
+/* _ckernels.pyx:30-57.  x: (A.ncols, m), y/b: (A.nrows, m).  b only for RSUB.
+ * x must not alias y.  Per-(row, column) accumulation in CSR entry order with
+ * separately rounded mul/add: bitwise equal to the reference kernel. */
+int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m,
+                 int32_t mode, const double* b, void* stream);
+
+/* Vector kernels over (n, m) blocks; per-column scalars a, b, c are DEVICE
+ * arrays of length m.  Same per-element expressions as _ckernels.pyx:82-162. */
+int mrs_axpby(int64_t n, int64_t m, const double* a, const double* x,
+              const double* b, double* y, void* stream);
+int mrs_add2_scaled(int64_t n, int64_t m, double* y, const double* a,
+                    const double* u, const double* b, const double* v, void* stream);
+int mrs_fused_paired_update(int64_t n, int64_t m, double* y1, const double* a,
+                            const double* u, const double* b, const double* s,
+                            double* y2, const double* c, const double* w, void* stream);
+/* Reductions write the full per-column result (m doubles, device) -- the
+ * reduction over row blocks is done on the device in a fixed order, so the
+ * result is deterministic (not the reference's sequential fold bitwise). */
+int mrs_dot(int64_t n, int64_t m, const double* x, const double* y, double* out,
+            void* stream);
+int mrs_fused_update_dot(int64_t n, int64_t m, const double* a, const double* x,
+                         const double* b, double* y, double* out, void* stream);
+int mrs_fused_update_dot2(int64_t n, int64_t m, double* y, const double* u,
+                          const double* c, const double* w, const double* z,
+                          double* d1, double* d2, void* stream);
+
+/* ---- 2. solver plan (src/solvers.py:850-959) ---------------------------- */
+
+#define MRS_METHOD_CG        0
+#define MRS_METHOD_BICGSTAB  1   /* classical van der Vorst, solvers.py:219-293 */
+
+#define MRS_PC_NONE     0
+#define MRS_PC_JACOBI   1        /* _SweepPrecond(jacobi), solvers.py:716-726,782-788 */
+#define MRS_PC_MG       2        /* MultiGrid V-cycle, solvers.py:615-675 */
+
+#define MRS_SMOOTH_JACOBI     0  /* blas2.jacobi_sweep, blas2.py:165-185 */
+#define MRS_SMOOTH_CHEBYSHEV  1  /* solvers.chebyshev_apply, solvers.py:520-571 */
+
+typedef struct {
+    int32_t kind;        /* MRS_SMOOTH_* */
+    int32_t sweeps;      /* Jacobi: sweeps per application (max_iters) */
+    double  weight;      /* Jacobi omega */
+    int32_t order;       /* Chebyshev polynomial order */
+} mrs_smoother;
+
+typedef struct {
+    int32_t method;      /* MRS_METHOD_* */
+    int32_t precond;     /* MRS_PC_* */
+    int64_t nrows;       /* fine rows */
+    int64_t m;           /* right-hand sides */
+    double  rel_tol;
+    int32_t max_iters;
+    double  pc_weight;   /* Jacobi preconditioner omega */
+    int32_t pc_sweeps;   /* Jacobi preconditioner sweeps */
+    int32_t mg_cycles;   /* V-cycles per preconditioner application */
+    mrs_smoother pre, post;
+    int32_t nlevels;     /* MultiGrid: hierarchy depth (>= 1) */
+    int32_t exec;        /* 0: CUDA graph with device-side while loop (default)
+                            1: eager launches, host checks convergence */
+    int32_t merged;      /* BiCGStab merged=1 (solvers.py:258-283): ||s|| always
+                            replaces rnorm in the omega breakdown test */
+} mrs_plan_desc;
+
+typedef struct mrs_plan mrs_plan;
+
+int  mrs_plan_create(const mrs_plan_desc* desc, mrs_plan** out);
+/* Upload level `l` (copied; host arrays may be freed afterwards).  For the
+ * Jacobi / no-preconditioner plans only level 0 (A) is set.  P, R NULL on the
+ * coarsest level.  lmin/lmax: Chebyshev bounds (ignored for Jacobi). */
+int  mrs_plan_set_level(mrs_plan* p, int32_t l, const mrs_host_csr* A,
+                        const mrs_host_csr* P, const mrs_host_csr* R,
+                        double lmin, double lmax);
+/* Coarsest-level dense inverse, row-major nc x nc float64 (host). */
+int  mrs_plan_set_coarse_inverse(mrs_plan* p, const double* inv, int64_t nc);
+int  mrs_plan_finalize(mrs_plan* p, void* stream);
+
+typedef struct {
+    int32_t iterations;
+    int32_t status;          /* MRS_OK or MRS_ERR_BREAKDOWN */
+    int32_t breakdown_column;
+    int32_t breakdown_site;  /* which coefficient vanished (see solver.cu) */
+    double  device_ms;       /* device time of the solve (CUDA events) */
+} mrs_stats;
+
+/* Solve A X = B.  B, X: (nrows, m) float64, device pointers unless
+ * host_buffers != 0 (then pinned/pageable host memory, copies inside).
+ * x_is_zero: X is a certified zero initial guess (reference VectorFlags.zero).
+ * final_rel (m), history ((max_iters+1) * m, may be NULL) are host outputs. */
+int  mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
+                    int32_t host_buffers, void* stream, mrs_stats* stats,
+                    double* final_rel, double* history);
+/* Algorithmic HBM bytes of one outer iteration / of the setup residual
+ * (the roofline model of SURVEY.md 8(d)). */
+double mrs_plan_iteration_bytes(const mrs_plan* p);
+int  mrs_plan_kernel_count(const mrs_plan* p);   /* kernels per outer iteration */
+int  mrs_plan_fixed_kernel_count(const mrs_plan* p); /* kernels outside the loop */
+void mrs_plan_destroy(mrs_plan* p);
+
+/* ---- 3. native host setup (src/amg.py:55-308, src/solvers.py:486-517) --- */
+
+typedef struct {
+    double  strength_threshold;   /* 0.25 */
+    int32_t agg_num_levels;       /* 0 */
+    int32_t num_paths;            /* 1 */
+    int64_t coarse_matrix_size;   /* 500 */
+    int32_t max_levels;           /* 25 */
+    double  stall_ratio;          /* 0.9 */
+    int32_t mixed_precision;      /* levels >= 1 stored float32 */
+} mrs_amg_params;
+
+typedef struct mrs_hierarchy mrs_hierarchy;
+
+int  mrs_amg_setup(const mrs_host_csr* A, const mrs_amg_params* prm, mrs_hierarchy** out);
+int  mrs_hier_nlevels(const mrs_hierarchy* h);
+/* which: 0 = A, 1 = P, 2 = R.  Returns MRS_ERR_ARG when absent.  Arrays stay
+ * owned by the hierarchy (int64 row_ptr, uint32 columns before width
+ * compression is applied by the caller, float64/float32 values). */
+int  mrs_hier_get(const mrs_hierarchy* h, int32_t level, int32_t which, mrs_host_csr* out);
+void mrs_hier_destroy(mrs_hierarchy* h);
+
+/* Power-iteration bounds of D^-1 A exactly as solvers.estimate_eig_bounds. */
+int  mrs_eig_bounds(const mrs_host_csr* A, int32_t iterations, uint64_t seed_unused,
+                    const double* start_vec, double* lmin, double* lmax);
+
+const char* mrs_status_string(int32_t status);
+int  mrs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MRSOLVE_B200_H */

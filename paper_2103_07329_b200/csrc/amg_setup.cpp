@@ -1,0 +1,378 @@
+// amg_setup.cpp -- native host restatement of the reference AMG setup and of
+// the Chebyshev eigenvalue-bound estimate.  Output is bitwise identical to
+// the reference (pinned by tests/test_setup_native.py against
+// tests/golden/hierarchies.npz), so the hierarchy uploaded to the GPU is the
+// reference's hierarchy -- produced ~100x faster than its Python loops.
+//
+//   strength_graph   src/amg.py:55-78    classical negative-coupling rule
+//   coarsen          src/amg.py:89-124   index-ordered greedy C/F split
+//   interpolate      src/amg.py:127-182  direct interpolation (numpy pairwise
+//                                        sums reproduced exactly)
+//   galerkin         src/amg.py:185-196  (R @ A) @ P with scipy's SMMP order:
+//                                        unsorted intermediate rows, exact-zero
+//                                        drop, then sort
+//   setup            src/amg.py:254-308  level loop, stall cut, retry once,
+//                                        mixed precision (levels >= 1 float32)
+//   estimate_eig_bounds  src/solvers.py:486-517
+//
+// Compiled with -ffp-contract=off and no -march flags: every multiply-add is
+// separately rounded, like the x86-64 baseline builds of numpy/scipy.
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "../../include/mrsolve_b200.h"
+
+namespace {
+
+struct Csr {
+    int64_t nrows = 0, ncols = 0;
+    std::vector<int64_t> rp;
+    std::vector<int64_t> ci;
+    std::vector<double> v;
+    int64_t nnz() const { return (int64_t)ci.size(); }
+};
+
+constexpr int8_t U = 0, C = 1, F = 2;
+
+// numpy's pairwise summation (loops_utils.h, PW_BLOCKSIZE 128) for a
+// contiguous float64 array: what `arr.sum()` computes.
+double pairwise_sum(const double* a, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; ++i) res += a[i];
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i = 8;
+        for (; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return pairwise_sum(a, n2) + pairwise_sum(a + n2, n - n2);
+}
+
+// Transpose with sorted output columns (scipy csr -> csc -> csr).
+Csr transpose(const Csr& A) {
+    Csr T;
+    T.nrows = A.ncols; T.ncols = A.nrows;
+    T.rp.assign(T.nrows + 1, 0);
+    for (int64_t k = 0; k < A.nnz(); ++k) T.rp[A.ci[k] + 1]++;
+    for (int64_t i = 0; i < T.nrows; ++i) T.rp[i + 1] += T.rp[i];
+    T.ci.resize(A.nnz()); T.v.resize(A.nnz());
+    std::vector<int64_t> pos(T.rp.begin(), T.rp.end() - 1);
+    for (int64_t i = 0; i < A.nrows; ++i)
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            int64_t p = pos[A.ci[k]]++;
+            T.ci[p] = i; T.v[p] = A.v[k];
+        }
+    return T;
+}
+
+// scipy csr_matmat (sparsetools/csr.h): per output row a linked list of
+// touched columns (head insertion), sums accumulated in traversal order,
+// exact zeros dropped, row emitted in list order (NOT sorted).
+Csr matmat(const Csr& A, const Csr& B) {
+    Csr Cm;
+    Cm.nrows = A.nrows; Cm.ncols = B.ncols;
+    Cm.rp.assign(A.nrows + 1, 0);
+    std::vector<int64_t> next(B.ncols, -1);
+    std::vector<double> sums(B.ncols, 0.0);
+    for (int64_t i = 0; i < A.nrows; ++i) {
+        int64_t head = -2, length = 0;
+        for (int64_t jj = A.rp[i]; jj < A.rp[i + 1]; ++jj) {
+            const int64_t j = A.ci[jj];
+            const double v = A.v[jj];
+            for (int64_t kk = B.rp[j]; kk < B.rp[j + 1]; ++kk) {
+                const int64_t k = B.ci[kk];
+                sums[k] += v * B.v[kk];
+                if (next[k] == -1) { next[k] = head; head = k; ++length; }
+            }
+        }
+        for (int64_t jj = 0; jj < length; ++jj) {
+            if (sums[head] != 0) { Cm.ci.push_back(head); Cm.v.push_back(sums[head]); }
+            int64_t tmp = head;
+            head = next[head];
+            next[tmp] = -1;
+            sums[tmp] = 0;
+        }
+        Cm.rp[i + 1] = Cm.nnz();
+    }
+    return Cm;
+}
+
+void sort_rows(Csr& A) {
+    std::vector<std::pair<int64_t, double>> row;
+    for (int64_t i = 0; i < A.nrows; ++i) {
+        int64_t lo = A.rp[i], hi = A.rp[i + 1];
+        row.clear();
+        for (int64_t k = lo; k < hi; ++k) row.emplace_back(A.ci[k], A.v[k]);
+        std::sort(row.begin(), row.end(),
+                  [](const auto& a, const auto& b) { return a.first < b.first; });
+        for (int64_t k = lo; k < hi; ++k) { A.ci[k] = row[k - lo].first; A.v[k] = row[k - lo].second; }
+    }
+}
+
+// strength_graph (amg.py:55-78): S[i,j] iff j != i and
+// -a_ij >= theta * max_k(-a_ik) with a positive row max.  Structure only.
+Csr strength(const Csr& A, double theta) {
+    Csr S;
+    S.nrows = A.nrows; S.ncols = A.ncols;
+    S.rp.assign(A.nrows + 1, 0);
+    for (int64_t i = 0; i < A.nrows; ++i) {
+        double rowmax = 0.0;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+            if (A.ci[k] != i) rowmax = std::max(rowmax, -A.v[k]);
+        if (rowmax > 0) {
+            const double thr = theta * rowmax;
+            for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+                if (A.ci[k] != i && -A.v[k] >= thr) { S.ci.push_back(A.ci[k]); S.v.push_back(1.0); }
+        }
+        S.rp[i + 1] = S.nnz();
+    }
+    return S;
+}
+
+// coarsen (amg.py:89-124)
+std::vector<int8_t> split(const Csr& S, bool aggressive, int num_paths) {
+    const int64_t n = S.nrows;
+    Csr ST = transpose(S);
+    std::vector<int8_t> st(n, U);
+    std::vector<int32_t> cnt(aggressive ? n : 0, 0);
+    std::vector<int64_t> touched;
+    for (int64_t i = 0; i < n; ++i) {
+        if (st[i] != U) continue;
+        st[i] = C;
+        const int64_t lo = ST.rp[i], hi = ST.rp[i + 1];
+        for (int64_t k = lo; k < hi; ++k)
+            if (st[ST.ci[k]] == U) st[ST.ci[k]] = F;
+        if (aggressive && hi > lo) {
+            touched.clear();
+            for (int64_t k = lo; k < hi; ++k) {
+                const int64_t q = ST.ci[k];
+                for (int64_t kk = ST.rp[q]; kk < ST.rp[q + 1]; ++kk) {
+                    const int64_t j = ST.ci[kk];
+                    if (cnt[j]++ == 0) touched.push_back(j);
+                }
+            }
+            for (int64_t j : touched) {
+                if (cnt[j] >= num_paths && st[j] == U && j != i) st[j] = F;
+            }
+            for (int64_t j : touched) cnt[j] = 0;
+        }
+    }
+    return st;
+}
+
+// interpolate (amg.py:127-182).  Returns false with the degenerate F rows.
+bool interp(const Csr& A, const Csr& S, const std::vector<int8_t>& st, Csr& P,
+            std::vector<int64_t>& bad) {
+    const int64_t n = A.nrows;
+    std::vector<int64_t> cmap(n, -1);
+    int64_t nc = 0;
+    for (int64_t i = 0; i < n; ++i)
+        if (st[i] == C) cmap[i] = nc++;
+    P = Csr();
+    P.nrows = n; P.ncols = nc;
+    P.rp.assign(n + 1, 0);
+    bad.clear();
+    std::vector<double> diag, off, sel;
+    std::vector<int64_t> selc;
+    std::vector<char> strong_mark(n, 0);
+    for (int64_t i = 0; i < n; ++i) {
+        if (st[i] == C) {
+            P.ci.push_back(cmap[i]); P.v.push_back(1.0);
+            P.rp[i + 1] = P.nnz();
+            continue;
+        }
+        for (int64_t k = S.rp[i]; k < S.rp[i + 1]; ++k) strong_mark[S.ci[k]] = 1;
+        diag.clear(); off.clear(); sel.clear(); selc.clear();
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+            const int64_t c = A.ci[k];
+            if (c == i) diag.push_back(A.v[k]);
+            else off.push_back(A.v[k]);
+            if (strong_mark[c] && st[c] == C) { sel.push_back(A.v[k]); selc.push_back(c); }
+        }
+        for (int64_t k = S.rp[i]; k < S.rp[i + 1]; ++k) strong_mark[S.ci[k]] = 0;
+        if (sel.empty()) {
+            bad.push_back(i);
+            P.rp[i + 1] = P.nnz();
+            continue;
+        }
+        const double a_ii = pairwise_sum(diag.data(), (int64_t)diag.size());
+        const double off_sum = pairwise_sum(off.data(), (int64_t)off.size());
+        const double strong_sum = pairwise_sum(sel.data(), (int64_t)sel.size());
+        const double ratio = off_sum / strong_sum;
+        for (size_t q = 0; q < sel.size(); ++q) {
+            P.ci.push_back(cmap[selc[q]]);
+            P.v.push_back((-(sel[q] / a_ii)) * ratio);
+        }
+        P.rp[i + 1] = P.nnz();
+    }
+    return bad.empty();
+}
+
+struct Level {
+    Csr A, P, R;
+    bool hasP = false;
+    bool reduced = false;
+    std::vector<float> Af, Pf, Rf;       // float32 copies on reduced levels
+    std::vector<uint32_t> Aci, Pci, Rci; // 32-bit column copies for export
+};
+
+}  // namespace
+
+struct mrs_hierarchy {
+    std::vector<Level> levels;
+};
+
+namespace {
+
+Csr from_host(const mrs_host_csr* h) {
+    Csr A;
+    A.nrows = h->nrows; A.ncols = h->ncols;
+    A.rp.assign(h->row_ptr, h->row_ptr + h->nrows + 1);
+    A.ci.resize(h->nnz); A.v.resize(h->nnz);
+    for (int64_t k = 0; k < h->nnz; ++k) {
+        A.ci[k] = h->idx_bytes == 4 ? ((const uint32_t*)h->col_idx)[k]
+                : h->idx_bytes == 2 ? ((const uint16_t*)h->col_idx)[k]
+                                    : ((const uint8_t*)h->col_idx)[k];
+        A.v[k] = h->val_bytes == 8 ? ((const double*)h->values)[k]
+                                   : (double)((const float*)h->values)[k];
+    }
+    return A;
+}
+
+void export_csr(const Csr& A, bool reduced, std::vector<float>& vf, std::vector<uint32_t>& ci) {
+    ci.resize(A.nnz());
+    for (int64_t k = 0; k < A.nnz(); ++k) ci[k] = (uint32_t)A.ci[k];
+    if (reduced) {
+        vf.resize(A.nnz());
+        for (int64_t k = 0; k < A.nnz(); ++k) vf[k] = (float)A.v[k];
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarchy** out) {
+    if (!Ah || !prm || !out) return MRS_ERR_ARG;
+    if (Ah->nrows != Ah->ncols) return MRS_ERR_ARG;
+    if (!(prm->strength_threshold > 0.0 && prm->strength_threshold < 1.0)) return MRS_ERR_ARG;
+    if (prm->coarse_matrix_size < 1 || prm->max_levels < 2 || prm->num_paths < 1) return MRS_ERR_ARG;
+    std::vector<Csr> chain;
+    chain.push_back(from_host(Ah));
+    sort_rows(chain.back());
+    std::vector<Csr> Ps;
+    while (chain.back().nrows > prm->coarse_matrix_size && (int)chain.size() < prm->max_levels) {
+        const Csr& M = chain.back();
+        Csr S = strength(M, prm->strength_threshold);
+        const bool agg = (int)chain.size() - 1 < prm->agg_num_levels;
+        std::vector<int8_t> st = split(S, agg, prm->num_paths);
+        Csr P;
+        std::vector<int64_t> bad;
+        if (!interp(M, S, st, P, bad)) {
+            for (int64_t r : bad) st[r] = C;
+            if (!interp(M, S, st, P, bad)) return MRS_ERR_DEGENERATE;
+        }
+        const int64_t ncoarse = P.ncols;
+        if (ncoarse == 0 || (double)ncoarse > prm->stall_ratio * (double)M.nrows) break;
+        Csr R = transpose(P);
+        Csr RA = matmat(R, M);
+        Csr Ac = matmat(RA, P);
+        sort_rows(Ac);
+        Ps.push_back(std::move(P));
+        chain.push_back(std::move(Ac));
+    }
+    mrs_hierarchy* h = new mrs_hierarchy();
+    h->levels.resize(chain.size());
+    for (size_t l = 0; l < chain.size(); ++l) {
+        Level& lv = h->levels[l];
+        lv.reduced = prm->mixed_precision && l > 0;
+        lv.A = std::move(chain[l]);
+        export_csr(lv.A, lv.reduced, lv.Af, lv.Aci);
+        if (l < Ps.size()) {
+            lv.hasP = true;
+            lv.P = std::move(Ps[l]);
+            lv.R = transpose(lv.P);
+            export_csr(lv.P, lv.reduced, lv.Pf, lv.Pci);
+            export_csr(lv.R, lv.reduced, lv.Rf, lv.Rci);
+        }
+    }
+    *out = h;
+    return MRS_OK;
+}
+
+int mrs_hier_nlevels(const mrs_hierarchy* h) { return h ? (int)h->levels.size() : 0; }
+
+int mrs_hier_get(const mrs_hierarchy* h, int32_t level, int32_t which, mrs_host_csr* out) {
+    if (!h || !out || level < 0 || level >= (int)h->levels.size()) return MRS_ERR_ARG;
+    const Level& lv = h->levels[level];
+    const Csr* M;
+    const std::vector<float>* vf;
+    const std::vector<uint32_t>* ci;
+    switch (which) {
+    case 0: M = &lv.A; vf = &lv.Af; ci = &lv.Aci; break;
+    case 1: if (!lv.hasP) return MRS_ERR_ARG; M = &lv.P; vf = &lv.Pf; ci = &lv.Pci; break;
+    case 2: if (!lv.hasP) return MRS_ERR_ARG; M = &lv.R; vf = &lv.Rf; ci = &lv.Rci; break;
+    default: return MRS_ERR_ARG;
+    }
+    out->nrows = M->nrows; out->ncols = M->ncols; out->nnz = M->nnz();
+    out->row_ptr = M->rp.data();
+    out->col_idx = ci->data();
+    out->idx_bytes = 4;
+    if (lv.reduced) { out->values = vf->data(); out->val_bytes = 4; }
+    else { out->values = M->v.data(); out->val_bytes = 8; }
+    return MRS_OK;
+}
+
+void mrs_hier_destroy(mrs_hierarchy* h) { delete h; }
+
+// estimate_eig_bounds (solvers.py:486-517): power iteration on D^-1 A with
+// the caller's start vector (numpy default_rng(12345).standard_normal(n)).
+int mrs_eig_bounds(const mrs_host_csr* Ah, int32_t iterations, uint64_t, const double* start,
+                   double* lmin, double* lmax) {
+    if (!Ah || !start || !lmin || !lmax) return MRS_ERR_ARG;
+    Csr A = from_host(Ah);
+    const int64_t n = A.nrows;
+    std::vector<double> d(n, 0.0);
+    for (int64_t i = 0; i < n; ++i) {
+        bool found = false;
+        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+            if (A.ci[k] == i) { d[i] = A.v[k]; found = true; break; }
+        if (!found || d[i] == 0.0) return MRS_ERR_SINGULAR;
+    }
+    std::vector<double> vec(start, start + n), w(n);
+    double lam = 1.0;
+    for (int it = 0; it < iterations; ++it) {
+        for (int64_t i = 0; i < n; ++i) {       // csr_spmv ASSIGN, entry order
+            double acc = 0.0;
+            for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) acc += A.v[k] * vec[A.ci[k]];
+            w[i] = acc;
+        }
+        for (int64_t i = 0; i < n; ++i) w[i] = w[i] / d[i];
+        double num = 0.0, den = 0.0, ww = 0.0;   // dot_partial: sequential folds
+        for (int64_t i = 0; i < n; ++i) num += vec[i] * w[i];
+        for (int64_t i = 0; i < n; ++i) den += vec[i] * vec[i];
+        lam = num / den;
+        for (int64_t i = 0; i < n; ++i) ww += w[i] * w[i];
+        const double wn = std::sqrt(ww);
+        if (wn == 0.0) break;
+        for (int64_t i = 0; i < n; ++i) vec[i] = w[i] / wn;
+    }
+    const double lm = 1.1 * std::fabs(lam);
+    *lmin = lm / 30.0;
+    *lmax = lm;
+    return MRS_OK;
+}
+
+}  // extern "C"

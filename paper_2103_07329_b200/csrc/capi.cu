@@ -1,0 +1,177 @@
+// capi.cu -- the kernel-plugin half of the C ABI (include/mrsolve_b200.h).
+//
+// Each entry point replaces one function of the reference plugin module
+// `mrsolve.kernels` (src/kernels/__init__.py:27-41).  Argument checks that
+// the reference performs in blas/blas2 (shape, alias, mode) are done here
+// because this is the library boundary; everything else is asynchronous on
+// the caller's stream.
+#include <cstdint>
+#include <cstring>
+
+#include "dispatch.h"
+
+using namespace mrs;
+
+namespace {
+
+// 16-byte alignment needed by the vectorised column slices.
+inline bool aligned16(const void* p) { return ((uintptr_t)p & 15u) == 0; }
+
+inline bool m_ok(int64_t m) { return m >= 1 && m <= kMaxM; }
+
+struct Scratch {
+    double* partials = nullptr;
+    unsigned int* ticket = nullptr;
+    int cap = 0;
+};
+
+// One reduction scratch per device per thread (plugin calls are stream-ordered;
+// concurrent use from several host threads needs distinct streams AND is
+// serialised here by thread_local ownership).
+thread_local Scratch t_scratch[16];
+
+int get_scratch(int64_t Km, Scratch** out) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return MRS_ERR_CUDA;
+    Scratch& s = t_scratch[dev];
+    int need = max_grid() * (int)Km;
+    if (s.cap < need) {
+        if (s.partials) cudaFree(s.partials);
+        if (!s.ticket) {
+            if (cudaMalloc(&s.ticket, sizeof(unsigned int)) != cudaSuccess) return MRS_ERR_ALLOC;
+            if (cudaMemset(s.ticket, 0, sizeof(unsigned int)) != cudaSuccess) return MRS_ERR_CUDA;
+        }
+        if (cudaMalloc(&s.partials, sizeof(double) * need) != cudaSuccess) return MRS_ERR_ALLOC;
+        s.cap = need;
+    }
+    *out = &s;
+    return MRS_OK;
+}
+
+int vec_call(int op, VArgs a, int K, double* out, void* stream) {
+    if (a.n < 0 || !m_ok(a.m)) return MRS_ERR_ARG;
+    if (a.n == 0) {
+        if (K && out) {
+            if (cudaMemsetAsync(out, 0, sizeof(double) * K * a.m, (cudaStream_t)stream) != cudaSuccess)
+                return MRS_ERR_CUDA;
+        }
+        return MRS_OK;
+    }
+    if (K) {
+        Scratch* s = nullptr;
+        int rc = get_scratch(K * a.m, &s);
+        if (rc) return rc;
+        a.red.partials = s->partials;
+        a.red.ticket = s->ticket;
+        a.red.out = out;
+        a.red.st = nullptr;
+        a.red.epi = EPI_NONE;
+    }
+    return launch_vec(op, a, (cudaStream_t)stream) == cudaSuccess ? MRS_OK : MRS_ERR_CUDA;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrs_version(void) { return 1; }
+
+const char* mrs_status_string(int32_t s) {
+    switch (s) {
+    case MRS_OK: return "ok";
+    case MRS_ERR_ARG: return "invalid argument (shape, dtype, mode or alias)";
+    case MRS_ERR_CUDA: return "CUDA runtime error";
+    case MRS_ERR_UNSUPPORTED: return "configuration not supported on the device path";
+    case MRS_ERR_ALLOC: return "allocation failed";
+    case MRS_ERR_BREAKDOWN: return "Krylov breakdown";
+    case MRS_ERR_SINGULAR: return "zero or missing diagonal entry";
+    case MRS_ERR_DEGENERATE: return "AMG setup degeneracy";
+    case MRS_ERR_STATE: return "call out of order";
+    }
+    return "unknown status";
+}
+
+// _ckernels.pyx:30-57
+int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_t mode,
+                 const double* b, void* stream) {
+    if (!A || !m_ok(m) || mode < 0 || mode > 3) return MRS_ERR_ARG;
+    if (A->idx_bytes != 1 && A->idx_bytes != 2 && A->idx_bytes != 4) return MRS_ERR_ARG;
+    if (A->val_bytes != 4 && A->val_bytes != 8) return MRS_ERR_ARG;
+    if (A->nrows < 0 || A->nnz < 0 || A->nnz > INT32_MAX) return MRS_ERR_ARG;
+    if (mode == MRS_MODE_RSUB && !b) return MRS_ERR_ARG;
+    if (x == y) return MRS_ERR_ARG;          // spmv output must not alias the input
+    if (A->nrows == 0) return MRS_OK;
+    DevCsr D;
+    D.nrows = A->nrows; D.ncols = A->ncols; D.nnz = A->nnz;
+    D.rp = const_cast<int32_t*>(A->row_ptr);
+    D.ci = const_cast<void*>(A->col_idx);
+    D.v = const_cast<void*>(A->values);
+    D.ib = A->idx_bytes; D.vb = A->val_bytes;
+    SpArgs a;
+    memset(&a, 0, sizeof(a));
+    a.x = x; a.y = y; a.b = b; a.mode = mode;
+    // unaligned views fall back to the scalar-per-column kernel
+    bool vec_ok = aligned16(x) && aligned16(y) && (!b || aligned16(b));
+    cudaError_t e = launch_spmm(OP_SPMV, D, a, m, (cudaStream_t)stream, !vec_ok && m > 1);
+    return e == cudaSuccess ? MRS_OK : MRS_ERR_CUDA;
+}
+
+int mrs_axpby(int64_t n, int64_t m, const double* a, const double* x, const double* b,
+              double* y, void* stream) {
+    VArgs A; memset(&A, 0, sizeof(A));
+    A.n = n; A.m = m; A.a = a; A.b = b; A.x = x; A.y = y;
+    return vec_call(V_AXPBY, A, 0, nullptr, stream);
+}
+
+int mrs_add2_scaled(int64_t n, int64_t m, double* y, const double* a, const double* u,
+                    const double* b, const double* v, void* stream) {
+    VArgs A; memset(&A, 0, sizeof(A));
+    A.n = n; A.m = m; A.y = y; A.a = a; A.u = u; A.b = b; A.v = v;
+    return vec_call(V_ADD2, A, 0, nullptr, stream);
+}
+
+int mrs_fused_paired_update(int64_t n, int64_t m, double* y1, const double* a,
+                            const double* u, const double* b, const double* s, double* y2,
+                            const double* c, const double* w, void* stream) {
+    if (y2 == s || y2 == w || y1 == y2) return MRS_ERR_ARG;
+    VArgs A; memset(&A, 0, sizeof(A));
+    A.n = n; A.m = m; A.y = y1; A.a = a; A.u = u; A.b = b; A.s = s; A.y2 = y2; A.c = c; A.w = w;
+    return vec_call(V_PAIRED, A, 0, nullptr, stream);
+}
+
+int mrs_dot(int64_t n, int64_t m, const double* x, const double* y, double* out, void* stream) {
+    VArgs A; memset(&A, 0, sizeof(A));
+    A.n = n; A.m = m; A.x = x; A.z = y;
+    return vec_call(V_DOT, A, 1, out, stream);
+}
+
+int mrs_fused_update_dot(int64_t n, int64_t m, const double* a, const double* x,
+                         const double* b, double* y, double* out, void* stream) {
+    VArgs A; memset(&A, 0, sizeof(A));
+    A.n = n; A.m = m; A.a = a; A.x = x; A.b = b; A.y = y;
+    return vec_call(V_UPDATE_DOT, A, 1, out, stream);
+}
+
+int mrs_fused_update_dot2(int64_t n, int64_t m, double* y, const double* u, const double* c,
+                          const double* w, const double* z, double* d1, double* d2,
+                          void* stream) {
+    if (!d1 || !d2) return MRS_ERR_ARG;
+    VArgs A; memset(&A, 0, sizeof(A));
+    A.n = n; A.m = m; A.y = y; A.u = u; A.c = c; A.w = w; A.z = z;
+    // results land as [d1 | d2] in scratch, then split
+    double* tmp = nullptr;
+    int rc;
+    if (cudaMallocAsync(&tmp, sizeof(double) * 2 * m, (cudaStream_t)stream) != cudaSuccess)
+        return MRS_ERR_ALLOC;
+    rc = vec_call(V_UPDATE_DOT2, A, 2, tmp, stream);
+    if (rc == MRS_OK) {
+        cudaStream_t s = (cudaStream_t)stream;
+        if (cudaMemcpyAsync(d1, tmp, sizeof(double) * m, cudaMemcpyDeviceToDevice, s) != cudaSuccess ||
+            cudaMemcpyAsync(d2, tmp + m, sizeof(double) * m, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+            rc = MRS_ERR_CUDA;
+    }
+    cudaFreeAsync(tmp, (cudaStream_t)stream);
+    return rc;
+}
+
+}  // extern "C"

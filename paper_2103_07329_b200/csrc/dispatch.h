@@ -1,0 +1,39 @@
+// dispatch.h -- host-side launchers shared by the C ABI (capi.cu) and the
+// solver plan (solver.cu).  Each picks the template instance for (m, index
+// width, value width) and a persistent grid.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/mrsolve_b200.h"
+#include "spmm.cuh"
+#include "blas.cuh"
+
+namespace mrs {
+
+struct DevCsr {
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int32_t* rp = nullptr;
+    void* ci = nullptr;
+    void* v = nullptr;
+    int ib = 4, vb = 8;
+    bool present() const { return rp != nullptr; }
+    // algorithmic bytes of one pass over the CSR arrays
+    double bytes() const { return (double)nnz * (ib + vb) + (double)(nrows + 1) * 4.0; }
+};
+
+// SpMM-family launch (OP = SpOp).  a.rp/ci/vals/nrows are filled from A.
+cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream_t s,
+                        bool generic = false);
+// Vector-family launch (OP = VecOp).
+cudaError_t launch_vec(int op, VArgs a, cudaStream_t s);
+// Dense coarse solve x = Ainv b for (nc, m) blocks.
+cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
+                          int64_t m, const int* guard, cudaStream_t s);
+// Grid the reduction kernels use (partials buffer sizing).
+int vec_grid(int64_t n, int64_t m);
+int spmm_grid(int64_t nrows, int64_t m);
+int max_grid();
+
+}  // namespace mrs

@@ -1,0 +1,145 @@
+// kernels.cu -- template instantiation and dispatch of the SpMM and vector
+// kernel families, and the dense coarse-level solve.
+#include "dispatch.h"
+
+namespace mrs {
+
+int max_grid() { return num_sms() * kMaxGridPerSM; }
+
+int spmm_grid(int64_t nrows, int64_t m) {
+    int rpb;
+    switch (m) {
+    case 1: rpb = Lay<1>::RPB; break;
+    case 2: rpb = Lay<2>::RPB; break;
+    case 4: rpb = Lay<4>::RPB; break;
+    case 8: rpb = Lay<8>::RPB; break;
+    case 16: rpb = Lay<16>::RPB; break;
+    case 32: rpb = Lay<32>::RPB; break;
+    case 64: rpb = Lay<64>::RPB; break;
+    default: rpb = kThreads / (int)m; break;
+    }
+    return grid_for(nrows, rpb);
+}
+
+int vec_grid(int64_t n, int64_t m) {
+    int rpb = kThreads / (int)m;
+    return grid_for(n, rpb * 4);
+}
+
+template <int OP, typename Tv, typename Ti>
+static cudaError_t spmm_m(const SpArgs& a, int64_t m, cudaStream_t s, bool generic) {
+    int g = spmm_grid(a.nrows, generic ? 3 : m);
+    switch (generic ? 0 : m) {
+    case 1: spmm_kernel<1, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 2: spmm_kernel<2, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 4: spmm_kernel<4, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 8: spmm_kernel<8, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 16: spmm_kernel<16, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 32: spmm_kernel<32, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 64: spmm_kernel<64, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    default: spmm_kernel_generic<OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    }
+    return cudaGetLastError();
+}
+
+template <int OP>
+static cudaError_t spmm_op(const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s, bool g) {
+    if (A.vb == 8) {
+        if (A.ib == 4) return spmm_m<OP, double, uint32_t>(a, m, s, g);
+        if (A.ib == 2) return spmm_m<OP, double, uint16_t>(a, m, s, g);
+        if constexpr (OP == OP_SPMV)
+            if (A.ib == 1) return spmm_m<OP, double, uint8_t>(a, m, s, g);
+    } else if (A.vb == 4) {
+        if (A.ib == 4) return spmm_m<OP, float, uint32_t>(a, m, s, g);
+        if (A.ib == 2) return spmm_m<OP, float, uint16_t>(a, m, s, g);
+        if constexpr (OP == OP_SPMV)
+            if (A.ib == 1) return spmm_m<OP, float, uint8_t>(a, m, s, g);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream_t s,
+                        bool generic) {
+    a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.nrows = A.nrows; a.m = m;
+    if (A.nrows == 0) return cudaSuccess;
+    switch (op) {
+    case OP_SPMV: return spmm_op<OP_SPMV>(A, a, m, s, generic);
+    case OP_JAC_ZERO_RES: return spmm_op<OP_JAC_ZERO_RES>(A, a, m, s, generic);
+    case OP_JAC_SWEEP: return spmm_op<OP_JAC_SWEEP>(A, a, m, s, generic);
+    case OP_JAC_ZERO2: return spmm_op<OP_JAC_ZERO2>(A, a, m, s, generic);
+    case OP_CHEB_FIRST: return spmm_op<OP_CHEB_FIRST>(A, a, m, s, generic);
+    case OP_CHEB_STEP: return spmm_op<OP_CHEB_STEP>(A, a, m, s, generic);
+    case OP_CHEB_STEP_ZERO: return spmm_op<OP_CHEB_STEP_ZERO>(A, a, m, s, generic);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int OP>
+static cudaError_t vec_op(const VArgs& a, cudaStream_t s) {
+    int g = vec_grid(a.n, a.m);
+    vec_kernel<OP><<<g, kThreads, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_vec(int op, VArgs a, cudaStream_t s) {
+    switch (op) {
+    case V_AXPBY: return vec_op<V_AXPBY>(a, s);
+    case V_ADD2: return vec_op<V_ADD2>(a, s);
+    case V_PAIRED: return vec_op<V_PAIRED>(a, s);
+    case V_DOT: return vec_op<V_DOT>(a, s);
+    case V_UPDATE_DOT: return vec_op<V_UPDATE_DOT>(a, s);
+    case V_UPDATE_DOT2: return vec_op<V_UPDATE_DOT2>(a, s);
+    case V_COPY: return vec_op<V_COPY>(a, s);
+    case V_CG_UPDATE: return vec_op<V_CG_UPDATE>(a, s);
+    case V_CG_UPDATE_JAC: return vec_op<V_CG_UPDATE_JAC>(a, s);
+    case V_P_UPDATE: return vec_op<V_P_UPDATE>(a, s);
+    case V_JAC_ZERO: return vec_op<V_JAC_ZERO>(a, s);
+    case V_CHEB_ZERO1: return vec_op<V_CHEB_ZERO1>(a, s);
+    case V_BICG_P: return vec_op<V_BICG_P>(a, s);
+    case V_BICG_S: return vec_op<V_BICG_S>(a, s);
+    case V_DOT3: return vec_op<V_DOT3>(a, s);
+    case V_BICG_XR: return vec_op<V_BICG_XR>(a, s);
+    case V_DOT2: return vec_op<V_DOT2>(a, s);
+    }
+    return cudaErrorInvalidValue;
+}
+
+// Coarsest level: x = Ainv b (replaces scipy lu_solve, solvers.py:644-649).
+// CTA handles kRows rows; thread (ks, c) folds k = ks, ks + kpb, ... for
+// column c, then the ks partials are folded in order (deterministic).
+constexpr int kCoarseRows = 4;
+
+__global__ void __launch_bounds__(kThreads) coarse_kernel(const double* __restrict__ inv, int64_t nc,
+                                                          const double* __restrict__ b,
+                                                          double* __restrict__ x, int m,
+                                                          const int* guard) {
+    if (guard && *guard) return;
+    __shared__ double s_t[kThreads];
+    const int kpb = kThreads / m;
+    const int c = threadIdx.x % m, ks = threadIdx.x / m;
+    for (int rr = 0; rr < kCoarseRows; ++rr) {
+        int64_t i = (int64_t)blockIdx.x * kCoarseRows + rr;
+        if (i >= nc) break;
+        double acc = 0.0;
+        if (ks < kpb)
+            for (int64_t k = ks; k < nc; k += kpb)
+                acc = add(acc, mul(__ldg(inv + i * nc + k), __ldg(b + k * m + c)));
+        s_t[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < m) {
+            double t = s_t[threadIdx.x];
+            for (int q = 1; q < kpb; ++q) t = add(t, s_t[q * m + threadIdx.x]);
+            x[i * m + threadIdx.x] = t;
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
+                          int64_t m, const int* guard, cudaStream_t s) {
+    int g = (int)((nc + kCoarseRows - 1) / kCoarseRows);
+    coarse_kernel<<<g, kThreads, 0, s>>>(inv, nc, b, x, (int)m, guard);
+    return cudaGetLastError();
+}
+
+}  // namespace mrs

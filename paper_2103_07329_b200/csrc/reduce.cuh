@@ -1,0 +1,278 @@
+// reduce.cuh -- deterministic multi-column reductions with a fused scalar
+// epilogue, and the per-solve device state the epilogues update.
+//
+// Every reduction in the solve path (dot, norm2, dot_many of the reference,
+// src/blas.py:173-221) is finished on the device in one kernel:
+//   thread partials -> warp/block tree (fixed shape) -> per-CTA partial row
+//   -> the last CTA to arrive (atomic ticket) folds the CTA partials in CTA
+//   order and runs the scalar epilogue (the reference's _coef / convergence
+//   test, src/solvers.py:111-123, :171, :180) on the reduced values.
+// Results depend only on (n, m, grid), never on scheduling: deterministic.
+#pragma once
+
+#include "common.cuh"
+
+namespace mrs {
+
+// Per-solve scalar state (device memory).  m <= kMaxM columns.
+constexpr int kMaxM = 64;
+
+struct SolveState {
+    double bscale[kMaxM];    // ||b_j|| or 1 (solvers._b_scale)
+    double rnorm[kMaxM];
+    double rho[kMaxM];
+    double rho_next[kMaxM];
+    double alpha[kMaxM];
+    double neg_alpha[kMaxM];
+    double beta[kMaxM];
+    double omega[kMaxM];
+    double neg_omega[kMaxM];
+    double final_rel[kMaxM];
+    double tol;
+    int m;
+    int max_iters;
+    int it;                  // completed-iteration counter (reference `it`)
+    int skip;                // remaining kernels of this iteration are no-ops
+    int stop;                // loop ends after this iteration
+    int err;                 // MRS_OK / MRS_ERR_BREAKDOWN
+    int err_col;
+    int err_site;
+    int merged;              // BiCGStab merged variant (snorm always from (s,s))
+    int has_cond;            // graph conditional handle valid
+    cudaGraphConditionalHandle cond;
+    double* history;         // (max_iters + 1) * m, device
+};
+
+enum Epilogue : int {
+    EPI_NONE = 0,
+    EPI_BSCALE,        // out = b.b            -> bscale
+    EPI_RNORM_INIT,    // out = r.r            -> rnorm, history[0], stop
+    EPI_RHO,           // out = r.z            -> rho
+    EPI_CG_ALPHA,      // out = p.q            -> it++, alpha = rho / pq
+    EPI_CG_RNORM,      // out = r.r            -> rnorm, history[it], skip/stop
+    EPI_CG_BETA,       // out = r.z            -> beta = rho_new / rho, rho = rho_new
+    EPI_BICG_ALPHA,    // out = r0.v           -> it++, alpha = rho / rv
+    EPI_BICG_OMEGA,    // out = (t.s, t.t, s.s) -> omega
+    EPI_BICG_RNORM,    // out = (r0.r, r.r)   -> rnorm, history, stop, beta
+    EPI_FINAL,         // out = r.r (true residual) -> final_rel
+    EPI_CG_RNORM_BETA, // out = (r.r, r.z)     -> EPI_CG_RNORM then, if not converged, EPI_CG_BETA
+};
+
+// Breakdown sites, reported to the host for the exception message.
+enum BreakSite : int {
+    BRK_CG_CURVATURE = 1, BRK_CG_RHO = 2, BRK_BICG_RV = 3, BRK_BICG_OMEGA = 4,
+    BRK_BICG_RHO = 5, BRK_BICG_OMEGA_PREV = 6,
+};
+
+struct RedArgs {
+    double* partials;        // [gridDim.x][K * m]
+    unsigned int* ticket;    // zero between uses; reset by the last CTA
+    double* out;             // [K * m] reduced values (device)
+    SolveState* st;          // may be null for EPI_NONE
+    int epi;
+};
+
+// _coef (solvers.py:111-123): num/den, zero den with nonzero rnorm is a
+// breakdown, zero den on a converged column yields 0.
+static __device__ __forceinline__ double coef(double num, double den, double rnorm, int c,
+                                       SolveState* st, int site, bool& bad) {
+    if (den == 0.0) {
+        if (rnorm > 0.0) {
+            bad = true;
+            atomicMin(&st->err_col, c);
+            st->err_site = site;
+        }
+        return 0.0;
+    }
+    return divd(num, den);
+}
+
+static __device__ __forceinline__ void set_loop(SolveState* st, bool keep_going) {
+    if (st->has_cond) cudaGraphSetConditional(st->cond, keep_going ? 1u : 0u);
+}
+
+// Runs on ONE block (the last to arrive), all threads; `v` = reduced values
+// in shared memory, laid out [K][m].
+static __device__ void run_epilogue(int epi, SolveState* st, const double* v, int m) {
+    const int c = threadIdx.x;
+    const bool act = c < m;
+    bool bad = false;
+    switch (epi) {
+    case EPI_NONE:
+        break;
+    case EPI_BSCALE:
+        if (act) { double nb = sqrt(v[c]); st->bscale[c] = nb > 0.0 ? nb : 1.0; }
+        break;
+    case EPI_RNORM_INIT: {
+        bool conv = true;
+        if (act) {
+            double rn = sqrt(v[c]);
+            st->rnorm[c] = rn;
+            st->history[c] = divd(rn, st->bscale[c]);
+            conv = rn <= mul(st->tol, st->bscale[c]);
+        }
+        int all = __syncthreads_and(conv);
+        if (threadIdx.x == 0) {
+            st->it = 0; st->skip = 0; st->err = MRS_OK; st->err_col = 1 << 30; st->err_site = 0;
+            st->stop = (all || st->max_iters <= 0) ? 1 : 0;
+            set_loop(st, !st->stop);
+        }
+        return;
+    }
+    case EPI_RHO:
+        if (act) st->rho[c] = v[c];
+        break;
+    case EPI_CG_ALPHA:
+        if (act) {
+            double a = coef(st->rho[c], v[c], st->rnorm[c], c, st, BRK_CG_CURVATURE, bad);
+            st->alpha[c] = a; st->neg_alpha[c] = -a;
+        }
+        if (threadIdx.x == 0) st->it += 1;
+        break;
+    case EPI_CG_RNORM: {
+        bool conv = true;
+        if (act) {
+            double rn = sqrt(v[c]);
+            st->rnorm[c] = rn;
+            st->history[(size_t)st->it * m + c] = divd(rn, st->bscale[c]);
+            conv = rn <= mul(st->tol, st->bscale[c]);
+        }
+        int all = __syncthreads_and(conv);
+        if (threadIdx.x == 0) {
+            if (all) { st->skip = 1; st->stop = 1; }
+            else if (st->it >= st->max_iters) st->stop = 1;
+            set_loop(st, !st->stop);
+        }
+        return;
+    }
+    case EPI_CG_RNORM_BETA: {
+        bool conv = true;
+        if (act) {
+            double rn = sqrt(v[c]);
+            st->rnorm[c] = rn;
+            st->history[(size_t)st->it * m + c] = divd(rn, st->bscale[c]);
+            conv = rn <= mul(st->tol, st->bscale[c]);
+        }
+        int all = __syncthreads_and(conv);
+        if (!all && act) {
+            st->beta[c] = coef(v[m + c], st->rho[c], st->rnorm[c], c, st, BRK_CG_RHO, bad);
+            st->rho[c] = v[m + c];
+        }
+        int anybad = __syncthreads_or(bad);
+        if (threadIdx.x == 0) {
+            if (all) { st->skip = 1; st->stop = 1; }
+            else if (st->it >= st->max_iters) st->stop = 1;
+            if (anybad) { st->err = MRS_ERR_BREAKDOWN; st->skip = 1; st->stop = 1; }
+            set_loop(st, !st->stop);
+        }
+        return;
+    }
+    case EPI_CG_BETA:
+        if (act) {
+            st->beta[c] = coef(v[c], st->rho[c], st->rnorm[c], c, st, BRK_CG_RHO, bad);
+            st->rho[c] = v[c];
+        }
+        break;
+    case EPI_BICG_ALPHA:
+        if (act) {
+            double a = coef(st->rho[c], v[c], st->rnorm[c], c, st, BRK_BICG_RV, bad);
+            st->alpha[c] = a; st->neg_alpha[c] = -a;
+        }
+        if (threadIdx.x == 0) st->it += 1;
+        break;
+    case EPI_BICG_OMEGA: {
+        // solvers.py:271-275: ||s|| replaces rnorm in the breakdown test
+        // only when np.any(tt == 0) over all columns.
+        int anyz = __syncthreads_or(act && v[m + c] == 0.0);
+        if (act) {
+            double ts = v[c], tt = v[m + c], ss = v[2 * m + c];
+            double snorm = (anyz || st->merged) ? sqrt(ss) : st->rnorm[c];
+            double w = coef(ts, tt, snorm, c, st, BRK_BICG_OMEGA, bad);
+            st->omega[c] = w; st->neg_omega[c] = -w;
+        }
+        break;
+    }
+    case EPI_BICG_RNORM: {
+        bool conv = true;
+        if (act) {
+            double rr = v[m + c];
+            double rn = sqrt(rr > 0.0 ? rr : 0.0);
+            st->rnorm[c] = rn;
+            st->rho_next[c] = v[c];
+            st->history[(size_t)st->it * m + c] = divd(rn, st->bscale[c]);
+            conv = rn <= mul(st->tol, st->bscale[c]);
+        }
+        int all = __syncthreads_and(conv);
+        int cont = !all && (st->it < st->max_iters);
+        if (cont && act) {
+            // next iteration's beta (solvers.py:246-249), evaluated only when
+            // the loop continues, exactly like the reference.
+            double rp = st->rho[c];
+            double rn_ = st->rho_next[c];
+            double b1 = coef(rn_, rp, st->rnorm[c], c, st, BRK_BICG_RHO, bad);
+            double b2 = coef(st->alpha[c], st->omega[c], st->rnorm[c], c, st,
+                             BRK_BICG_OMEGA_PREV, bad);
+            st->beta[c] = mul(b1, b2);
+            st->rho[c] = rn_;
+        }
+        int anybad = __syncthreads_or(bad);
+        if (threadIdx.x == 0) {
+            st->stop = cont ? 0 : 1;
+            if (anybad) { st->err = MRS_ERR_BREAKDOWN; st->stop = 1; st->skip = 1; }
+            set_loop(st, !st->stop);
+        }
+        return;
+    }
+    case EPI_FINAL:
+        if (act) st->final_rel[c] = divd(sqrt(v[c]), st->bscale[c]);
+        break;
+    }
+    int anybad = __syncthreads_or(bad);
+    if (anybad && threadIdx.x == 0) {
+        st->err = MRS_ERR_BREAKDOWN;
+        st->skip = 1;
+        st->stop = 1;
+        set_loop(st, false);
+    }
+}
+
+// Finish a reduction whose per-CTA partial (Km values) sits in smem `blk`.
+// All threads of every CTA call this.
+static __device__ void finish_reduction(const RedArgs& ra, const double* blk, int Km, int m) {
+    __shared__ bool s_last;
+    __shared__ double s_out[3 * kMaxM];
+    for (int i = threadIdx.x; i < Km; i += blockDim.x)
+        ra.partials[(size_t)blockIdx.x * Km + i] = blk[i];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = atomicAdd(ra.ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // fold CTA partials in CTA order; S slices per value for parallelism,
+    // slices combined in slice order: fixed shape -> deterministic.
+    const int S = blockDim.x / Km >= 1 ? blockDim.x / Km : 1;
+    __shared__ double s_sl[kThreads];
+    const int val = threadIdx.x % Km, sl = threadIdx.x / Km;
+    if (sl < S && threadIdx.x < S * Km) {
+        double acc = 0.0;
+        for (int b = sl; b < (int)gridDim.x; b += S)
+            acc = add(acc, __ldcg(ra.partials + (size_t)b * Km + val));
+        s_sl[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < Km; i += blockDim.x) {
+        double acc = s_sl[i];
+        for (int s = 1; s < S; ++s) acc = add(acc, s_sl[s * Km + i]);
+        s_out[i] = acc;
+        ra.out[i] = acc;
+    }
+    if (threadIdx.x == 0) *ra.ticket = 0u;
+    __syncthreads();
+    if (ra.epi != EPI_NONE) run_epilogue(ra.epi, ra.st, s_out, m);
+}
+
+}  // namespace mrs

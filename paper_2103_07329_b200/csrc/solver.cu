@@ -1,0 +1,749 @@
+// solver.cu -- the solver plan: uploaded hierarchy, static kernel schedule
+// of one solve, and its CUDA-graph execution with a device-side while loop.
+//
+// Replaces solvers.prepare(...).run(B, X) (src/solvers.py:850-959) for
+//   CG        (cg_solve, solvers.py:152-188)
+//   BiCGStab  (_bicgstab_classical, merged=0, solvers.py:219-293)
+// preconditioned by nothing, Jacobi sweeps (_SweepPrecond, :716-726) or a
+// MultiGrid V-cycle (solvers.py:615-675) with Jacobi (blas2.py:165-185) or
+// Chebyshev (solvers.py:520-571) smoothing and a dense coarsest solve.
+//
+// Execution model: the whole solve (prologue, iteration body, true-residual
+// epilogue) is a static sequence of kernel launches whose scalar decisions
+// (alpha, beta, omega, convergence, breakdown) are taken ON THE DEVICE by the
+// reduction epilogues (reduce.cuh).  It is captured once into a CUDA graph
+// whose iteration body sits under a conditional WHILE node that the
+// epilogues drive with cudaGraphSetConditional: one graph launch per solve,
+// no host round trip per iteration.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <vector>
+
+#include "dispatch.h"
+
+using namespace mrs;
+
+namespace {
+
+using Launch = std::function<cudaError_t(cudaStream_t)>;
+
+struct LevelDev {
+    DevCsr A, P, R;          // P: n_l x n_{l+1}, R: n_{l+1} x n_l
+    double* d = nullptr;     // diagonal (full precision of stored values)
+    double lmin = 0, lmax = 0;
+    double* b = nullptr;     // rhs buffer (levels >= 1)
+    double* xa = nullptr;
+    double* xb = nullptr;
+    double* r = nullptr;
+    double* dva = nullptr;
+    double* dvb = nullptr;
+};
+
+template <typename T> T* dalloc(size_t n, std::vector<void*>& owned) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    if (cudaMalloc(&p, n * sizeof(T)) != cudaSuccess) return nullptr;
+    owned.push_back(p);
+    return (T*)p;
+}
+
+}  // namespace
+
+struct mrs_plan {
+    mrs_plan_desc desc{};
+    int64_t n = 0, m = 0;
+    std::vector<LevelDev> L;
+    double* inv = nullptr;
+    int64_t nc = 0;
+    std::vector<void*> owned;
+    // Krylov workspace
+    double *B = nullptr, *X = nullptr, *r = nullptr, *r0 = nullptr, *p = nullptr, *q = nullptr;
+    double *v = nullptr, *s = nullptr, *t = nullptr, *ph = nullptr, *sh = nullptr, *z = nullptr,
+           *zt = nullptr;
+    // device state + reduction scratch
+    SolveState* st = nullptr;
+    double* history = nullptr;
+    double* partials = nullptr;
+    unsigned int* ticket = nullptr;
+    double* red_out = nullptr;
+    bool finalized = false;
+    // graphs (index: x_is_zero)
+    cudaGraph_t graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int body_kernels = 0;
+    int fixed_kernels = 0;
+    double it_bytes = 0;
+    ~mrs_plan() {
+        for (int i = 0; i < 2; ++i) {
+            if (exec[i]) cudaGraphExecDestroy(exec[i]);
+            if (graph[i]) cudaGraphDestroy(graph[i]);
+        }
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        for (void* p : owned) cudaFree(p);
+    }
+};
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// schedule builder
+// ---------------------------------------------------------------------------
+
+struct Builder {
+    mrs_plan* P;
+    std::vector<Launch>* out;
+    const int* guard = nullptr;       // body kernels: &st->skip
+    double bytes = 0;                 // algorithmic bytes accumulated
+    int kernels = 0;
+    double V(int64_t rows) const { return (double)rows * P->m * 8.0; }
+
+    RedArgs red(int epi) const {
+        RedArgs r;
+        r.partials = P->partials; r.ticket = P->ticket; r.out = P->red_out;
+        r.st = P->st; r.epi = epi;
+        return r;
+    }
+
+    void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
+        a.guard = guard;
+        int64_t m = P->m;
+        out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
+        bytes += A.bytes() + extra_bytes;
+        kernels++;
+    }
+    void vec(int op, VArgs a, double b) {
+        a.guard = a.guard ? a.guard : guard;
+        a.m = P->m;
+        out->push_back([=](cudaStream_t s) { return launch_vec(op, a, s); });
+        bytes += b;
+        kernels++;
+    }
+    static SpArgs sp0() { SpArgs a; memset(&a, 0, sizeof(a)); return a; }
+    static VArgs v0() { VArgs a; memset(&a, 0, sizeof(a)); return a; }
+
+    // y = A x (mode), optionally with fused dot x.y -> epilogue
+    void spmv(const DevCsr& A, const double* x, double* y, int mode, const double* b = nullptr,
+              int dot_epi = -1) {
+        SpArgs a = sp0();
+        a.x = x; a.y = y; a.b = b; a.mode = mode;
+        double vb = V(A.ncols) + V(A.nrows) + (mode == MRS_MODE_ASSIGN ? 0 : V(A.nrows));
+        if (dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); vb += V(A.nrows); }
+        spmm(OP_SPMV, A, a, vb);
+    }
+
+    void dot(const double* x, const double* y, int64_t n, int epi) {
+        VArgs a = v0(); a.n = n; a.x = x; a.z = y; a.red = red(epi);
+        vec(V_DOT, a, 2 * V(n));
+    }
+    void copy(const double* x, double* y, int64_t n) {
+        VArgs a = v0(); a.n = n; a.x = x; a.y = y;
+        vec(V_COPY, a, 2 * V(n));
+    }
+
+    // ---- smoothers -----------------------------------------------------
+    // Current-buffer bookkeeping: `cur` holds x; `alt` is the spare.
+    struct XB { double* cur; double* alt; void swap() { std::swap(cur, alt); } };
+
+    // One pre-smoothing application on a ZERO x, then r = b - A x in lv.r.
+    void pre_smooth_zero_and_residual(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x) {
+        const DevCsr& A = lv.A;
+        int64_t n = A.nrows;
+        if (sm.kind == MRS_SMOOTH_JACOBI) {
+            int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
+            if (sm.weight == 0.0) {
+                // weight 0: sweep is a no-op (blas2.py:487-489); x stays 0
+                VArgs z = v0(); z.n = n; z.x = b; z.y = x.cur; z.d = lv.d; z.wt = 0.0;
+                vec(V_JAC_ZERO, z, 2 * V(n) + 8.0 * n);
+                residual(lv, b, x.cur);
+                return;
+            }
+            if (sweeps == 1) {
+                SpArgs a = sp0(); a.b = b; a.d = lv.d; a.w = sm.weight; a.x_out = x.cur; a.r_out = lv.r;
+                spmm(OP_JAC_ZERO_RES, A, a, 3 * V(n) + 8.0 * n);
+                return;
+            }
+            SpArgs a = sp0(); a.b = b; a.d = lv.d; a.w = sm.weight; a.x_out = x.cur;
+            spmm(OP_JAC_ZERO2, A, a, 2 * V(n) + 8.0 * n);
+            for (int k = 2; k < sweeps; ++k) jacobi_sweep(lv, b, sm.weight, x);
+            residual(lv, b, x.cur);
+        } else {
+            chebyshev(lv, b, sm.order, /*zero=*/true, x);
+            residual(lv, b, x.cur);
+        }
+    }
+
+    void residual(LevelDev& lv, const double* b, const double* x) {
+        spmv(lv.A, x, lv.r, MRS_MODE_RSUB, b);
+    }
+
+    void jacobi_sweep(LevelDev& lv, const double* b, double w, XB& x) {
+        SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.w = w; a.x_out = x.alt;
+        spmm(OP_JAC_SWEEP, lv.A, a, 3 * V(lv.A.nrows) + 8.0 * lv.A.nrows);
+        x.swap();
+    }
+
+    // chebyshev_apply (solvers.py:520-571) on x (zero or not), result in x.cur.
+    void chebyshev(LevelDev& lv, const double* b, int order, bool zero, XB& x) {
+        const double lmin = lv.lmin, lmax = lv.lmax;
+        const double theta = 0.5 * (lmax + lmin);
+        const double delta = 0.5 * (lmax - lmin);
+        const double sigma = theta / delta;
+        double rho = 1.0 / sigma;
+        int64_t n = lv.A.nrows;
+        double* dv_cur = lv.dva;
+        double* dv_alt = lv.dvb;
+        if (order < 1) order = 1;
+        if (zero && order == 1) {
+            VArgs a = v0(); a.n = n; a.x = b; a.y = x.cur; a.d = lv.d; a.theta = theta;
+            vec(V_CHEB_ZERO1, a, 2 * V(n) + 8.0 * n);
+            return;
+        }
+        int k0 = 0;
+        if (zero) {
+            // first step (dv = b/(d*theta), x = dv) folded into the second
+            double rho_new = 1.0 / (2.0 * sigma - rho);
+            SpArgs a = sp0(); a.b = b; a.d = lv.d; a.theta = theta;
+            a.c1 = rho_new * rho; a.c2 = 2.0 * rho_new / delta;
+            a.x_out = x.cur;
+            bool more = order > 2;
+            a.r_out = more ? lv.r : nullptr;
+            a.dv_out = more ? dv_alt : nullptr;
+            spmm(OP_CHEB_STEP_ZERO, lv.A, a, V(n) + 8.0 * n + V(n) + (more ? 2 * V(n) : 0));
+            rho = rho_new;
+            std::swap(dv_cur, dv_alt);
+            k0 = 2;
+        } else {
+            SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.theta = theta;
+            a.x_out = x.alt; a.r_out = lv.r; a.dv_out = dv_cur;
+            spmm(OP_CHEB_FIRST, lv.A, a, 5 * V(n) + 8.0 * n);
+            x.swap();
+            k0 = 1;
+        }
+        for (int k = k0; k < order; ++k) {
+            double rho_new = 1.0 / (2.0 * sigma - rho);
+            SpArgs a = sp0(); a.x = dv_cur; a.x_in = x.cur; a.r_in = lv.r; a.d = lv.d;
+            a.c1 = rho_new * rho; a.c2 = 2.0 * rho_new / delta;
+            a.x_out = x.cur;
+            bool more = k + 1 < order;
+            a.r_out = more ? lv.r : nullptr;
+            a.dv_out = more ? dv_alt : nullptr;
+            spmm(OP_CHEB_STEP, lv.A, a, 4 * V(n) + 8.0 * n + (more ? 2 * V(n) : 0));
+            rho = rho_new;
+            std::swap(dv_cur, dv_alt);
+        }
+    }
+
+    void post_smooth(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x) {
+        if (sm.kind == MRS_SMOOTH_JACOBI) {
+            if (sm.weight == 0.0) return;
+            int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
+            for (int k = 0; k < sweeps; ++k) jacobi_sweep(lv, b, sm.weight, x);
+        } else {
+            chebyshev(lv, b, sm.order, false, x);
+        }
+    }
+
+    // pre-smooth on a NONZERO x then residual (second and later V-cycles)
+    void pre_smooth_nonzero_and_residual(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x) {
+        post_smooth(lv, b, sm, x);
+        residual(lv, b, x.cur);
+    }
+
+    // V-cycle on level l with rhs b; x given by buffers; zero = certified zero x.
+    void vcycle(int l, const double* b, bool zero, XB& x) {
+        mrs_plan& p = *P;
+        LevelDev& lv = p.L[l];
+        const int nl = (int)p.L.size();
+        if (l == nl - 1) {
+            // coarsest: x = A_c^{-1} b (solvers.py:644-649); x overwritten
+            int64_t m = p.m, nc = p.nc;
+            const double* inv = p.inv;
+            double* xo = x.cur;
+            const int* g = guard;
+            out->push_back([=](cudaStream_t s) { return launch_coarse(inv, nc, b, xo, m, g, s); });
+            bytes += (double)nc * nc * 8.0 + 2 * V(nc);
+            kernels++;
+            return;
+        }
+        if (zero) pre_smooth_zero_and_residual(lv, b, p.desc.pre, x);
+        else pre_smooth_nonzero_and_residual(lv, b, p.desc.pre, x);
+        LevelDev& lc = p.L[l + 1];
+        // rc = R r  (ASSIGN, solvers.py:660)
+        spmv(lv.R, lv.r, lc.b, MRS_MODE_ASSIGN);
+        XB xc{lc.xa, lc.xb};
+        vcycle(l + 1, lc.b, true, xc);
+        // x += P xc  (ADD, solvers.py:663)
+        spmv(lv.P, xc.cur, x.cur, MRS_MODE_ADD);
+        post_smooth(lv, b, p.desc.post, x);
+    }
+
+    // Preconditioner application z = M r; returns the buffer holding z.
+    // `dst`/`spare`: level-0 output buffers.
+    double* precond(const double* r, double* dst, double* spare) {
+        mrs_plan& p = *P;
+        const mrs_plan_desc& d = p.desc;
+        if (d.precond == MRS_PC_NONE) return const_cast<double*>(r);
+        XB x{dst, spare};
+        if (d.precond == MRS_PC_JACOBI) {
+            LevelDev& lv = p.L[0];
+            int64_t n = lv.A.nrows;
+            VArgs a = v0(); a.n = n; a.x = r; a.y = x.cur; a.d = lv.d; a.wt = d.pc_weight;
+            vec(V_JAC_ZERO, a, 2 * V(n) + 8.0 * n);
+            for (int k = 1; k < d.pc_sweeps; ++k) jacobi_sweep(lv, r, d.pc_weight, x);
+            return x.cur;
+        }
+        int cycles = d.mg_cycles < 1 ? 1 : d.mg_cycles;
+        for (int c = 0; c < cycles; ++c) vcycle(0, r, c == 0, x);
+        return x.cur;
+    }
+};
+
+// Dry-run the preconditioner to learn which of (dst, spare) ends up holding z,
+// then order the buffers so z lands in `want`.
+double* precond_into(mrs_plan* P, const int* guard, const double* r, double* want, double* spare,
+                     std::vector<Launch>& out, double& bytes, int& kernels) {
+    std::vector<Launch> dry;
+    Builder b0{P, &dry, guard};
+    double* got = b0.precond(r, want, spare);
+    if (got != want && got == spare) std::swap(want, spare);
+    Builder b{P, &out, guard};
+    double* res = b.precond(r, want, spare);
+    bytes += b.bytes;
+    kernels += b.kernels;
+    return res;
+}
+
+// ---------------------------------------------------------------------------
+// drivers
+// ---------------------------------------------------------------------------
+
+struct Program {
+    std::vector<Launch> pro, body, epi;
+    double body_bytes = 0;
+    int body_kernels = 0;
+};
+
+void build_cg(mrs_plan* P, bool x_zero, Program& pg) {
+    const int64_t n = P->n;
+    const int* skip = &P->st->skip;
+    const DevCsr& A = P->L[0].A;
+    const mrs_plan_desc& d = P->desc;
+    // prologue (solvers.py:156-168)
+    {
+        Builder b{P, &pg.pro, nullptr};
+        b.dot(P->B, P->B, n, EPI_BSCALE);
+        if (x_zero) b.copy(P->B, P->r, n);
+        else b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_RNORM_INIT);
+        double e = 0; int k = 0;
+        double* z = precond_into(P, nullptr, P->r, P->z, P->zt, pg.pro, e, k);
+        b.dot(P->r, z, n, EPI_RHO);
+        b.copy(z, P->p, n);
+    }
+    // body (solvers.py:171-186)
+    {
+        Builder b{P, &pg.body, skip};
+        b.spmv(A, P->p, P->q, MRS_MODE_ASSIGN, nullptr, EPI_CG_ALPHA);   // q = A p ; p.q -> alpha
+        const bool jac1 = d.precond == MRS_PC_JACOBI && d.pc_sweeps <= 1;
+        if (jac1) {
+            // X += a p ; r -= a q ; z = w r/d ; (r.r, r.z) -> rnorm, beta
+            VArgs a = Builder::v0(); a.n = n; a.y = P->X; a.x = P->p; a.y2 = P->r; a.u = P->q;
+            a.a = P->st->alpha; a.b = P->st->neg_alpha; a.y3 = P->z; a.d = P->L[0].d;
+            a.wt = d.pc_weight; a.red = b.red(EPI_CG_RNORM_BETA);
+            b.vec(V_CG_UPDATE_JAC, a, 6 * b.V(n) + 8.0 * n);
+            VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = P->z; pu.b = P->st->beta;
+            b.vec(V_P_UPDATE, pu, 3 * b.V(n));
+        } else {
+            VArgs a = Builder::v0(); a.n = n; a.y = P->X; a.x = P->p; a.y2 = P->r; a.u = P->q;
+            a.a = P->st->alpha; a.b = P->st->neg_alpha; a.red = b.red(EPI_CG_RNORM);
+            b.vec(V_CG_UPDATE, a, 5 * b.V(n));
+            double e = 0; int k = 0;
+            double* z = precond_into(P, skip, P->r, P->z, P->zt, pg.body, e, k);
+            b.bytes += e; b.kernels += k;
+            b.dot(P->r, z, n, EPI_CG_BETA);
+            VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = z; pu.b = P->st->beta;
+            b.vec(V_P_UPDATE, pu, 3 * b.V(n));
+        }
+        pg.body_bytes = b.bytes;
+        pg.body_kernels = b.kernels;
+    }
+    // true residual (solvers.py:126-141)
+    {
+        Builder b{P, &pg.epi, nullptr};
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_FINAL);
+    }
+}
+
+void build_bicgstab(mrs_plan* P, bool x_zero, Program& pg) {
+    const int64_t n = P->n;
+    const int* skip = &P->st->skip;
+    const DevCsr& A = P->L[0].A;
+    const bool pc = P->desc.precond != MRS_PC_NONE;
+    // prologue (solvers.py:220-243, first-iteration rho and p)
+    {
+        Builder b{P, &pg.pro, nullptr};
+        b.dot(P->B, P->B, n, EPI_BSCALE);
+        if (x_zero) b.copy(P->B, P->r, n);
+        else b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.copy(P->r, P->r0, n);
+        b.dot(P->r, P->r, n, EPI_RNORM_INIT);
+        b.dot(P->r0, P->r, n, EPI_RHO);
+        b.copy(P->r, P->p, n);
+    }
+    {
+        Builder b{P, &pg.body, skip};
+        // p = r + beta (p - omega v)  -- skipped in the first iteration (it == 0)
+        VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = P->r; pu.v = P->v;
+        pu.b = P->st->beta; pu.c = P->st->neg_omega; pu.guard_it = &P->st->it;
+        b.vec(V_BICG_P, pu, 4 * b.V(n));
+        double* ph = P->p;
+        if (pc) {
+            double e = 0; int k = 0;
+            ph = precond_into(P, skip, P->p, P->ph, P->zt, pg.body, e, k);
+            b.bytes += e; b.kernels += k;
+        }
+        b.spmv(A, ph, P->v, MRS_MODE_ASSIGN);                      // v = A ph
+        b.dot(P->r0, P->v, n, EPI_BICG_ALPHA);                     // alpha = rho / (r0, v)
+        VArgs sa = Builder::v0(); sa.n = n; sa.y = P->s; sa.x = P->r; sa.v = P->v;
+        sa.a = P->st->neg_alpha;
+        b.vec(V_BICG_S, sa, 3 * b.V(n));                           // s = r - alpha v
+        double* sh = P->s;
+        if (pc) {
+            double e = 0; int k = 0;
+            sh = precond_into(P, skip, P->s, P->sh, P->zt, pg.body, e, k);
+            b.bytes += e; b.kernels += k;
+        }
+        b.spmv(A, sh, P->t, MRS_MODE_ASSIGN);                      // t = A sh
+        VArgs d3 = Builder::v0(); d3.n = n; d3.x = P->t; d3.s = P->s; d3.red = b.red(EPI_BICG_OMEGA);
+        b.vec(V_DOT3, d3, 2 * b.V(n));                             // (t,s),(t,t),(s,s) -> omega
+        VArgs xr = Builder::v0(); xr.n = n; xr.y = P->X; xr.u = ph; xr.v = sh; xr.s = P->s;
+        xr.w = P->t; xr.y2 = P->r; xr.z = P->r0;
+        xr.a = P->st->alpha; xr.b = P->st->omega; xr.c = P->st->neg_omega;
+        xr.red = b.red(EPI_BICG_RNORM);
+        b.vec(V_BICG_XR, xr, 8 * b.V(n));                          // X, r, (r0,r), (r,r)
+        pg.body_bytes = b.bytes;
+        pg.body_kernels = b.kernels;
+    }
+    {
+        Builder b{P, &pg.epi, nullptr};
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_FINAL);
+    }
+}
+
+__global__ void set_cond_kernel(SolveState* st, cudaGraphConditionalHandle h, int has) {
+    st->has_cond = has;
+    st->cond = h;
+}
+
+cudaError_t run_list(const std::vector<Launch>& v, cudaStream_t s) {
+    for (auto& f : v) {
+        cudaError_t e = f(s);
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+}
+
+int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s) {
+    Program pg;
+    if (P->desc.method == MRS_METHOD_CG) build_cg(P, x_zero, pg);
+    else build_bicgstab(P, x_zero, pg);
+    int gi = x_zero ? 1 : 0;
+
+    cudaGraph_t g;
+    MRS_CUDA_OK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h;
+    MRS_CUDA_OK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+    // first node: publish this graph's handle to the epilogues
+    {
+        SolveState* st = P->st;
+        pg.pro.insert(pg.pro.begin(), [=](cudaStream_t s) {
+            set_cond_kernel<<<1, 1, 0, s>>>(st, h, 1);
+            return cudaGetLastError();
+        });
+    }
+
+    // 1) prologue
+    cudaStream_t cs;
+    MRS_CUDA_OK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    if (run_list(pg.pro, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &g); return MRS_ERR_CUDA; }
+    cudaGraph_t gg;
+    MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
+    // find the sink nodes of the prologue
+    size_t nn = 0;
+    MRS_CUDA_OK(cudaGraphGetNodes(g, nullptr, &nn));
+    std::vector<cudaGraphNode_t> nodes(nn);
+    MRS_CUDA_OK(cudaGraphGetNodes(g, nodes.data(), &nn));
+    std::vector<cudaGraphNode_t> sinks;
+    for (auto nd : nodes) {
+        size_t ndep = 0;
+        MRS_CUDA_OK(cudaGraphNodeGetDependentNodes(nd, nullptr, &ndep));
+        if (ndep == 0) sinks.push_back(nd);
+    }
+    // 2) WHILE node with the iteration body
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t wnode;
+    MRS_CUDA_OK(cudaGraphAddNode(&wnode, g, sinks.data(), sinks.size(), &cp));
+    cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+    MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    if (run_list(pg.body, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
+    MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
+    // 3) epilogue after the loop
+    MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
+    if (run_list(pg.epi, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
+    MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
+    cudaStreamDestroy(cs);
+    cudaGraphExec_t ex;
+    MRS_CUDA_OK(cudaGraphInstantiate(&ex, g, 0));
+    P->graph[gi] = g;
+    P->exec[gi] = ex;
+    return MRS_OK;
+}
+
+int upload_csr(const mrs_host_csr* h, DevCsr& d, std::vector<void*>& owned) {
+    if (!h) return MRS_OK;
+    if (h->nnz > INT32_MAX || h->nrows < 0) return MRS_ERR_UNSUPPORTED;
+    if (h->val_bytes != 4 && h->val_bytes != 8) return MRS_ERR_ARG;
+    if (h->idx_bytes != 1 && h->idx_bytes != 2 && h->idx_bytes != 4) return MRS_ERR_ARG;
+    d.nrows = h->nrows; d.ncols = h->ncols; d.nnz = h->nnz;
+    d.vb = h->val_bytes;
+    // device index width: >= 16 bit (u8 blocks are widened; they are tiny)
+    d.ib = h->idx_bytes == 1 ? 2 : h->idx_bytes;
+    std::vector<int32_t> rp(h->nrows + 1);
+    for (int64_t i = 0; i <= h->nrows; ++i) rp[i] = (int32_t)h->row_ptr[i];
+    d.rp = dalloc<int32_t>(h->nrows + 1, owned);
+    d.ci = dalloc<char>((size_t)h->nnz * d.ib, owned);
+    d.v = dalloc<char>((size_t)h->nnz * d.vb, owned);
+    if (!d.rp || !d.ci || !d.v) return MRS_ERR_ALLOC;
+    MRS_CUDA_OK(cudaMemcpy(d.rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
+    if (h->idx_bytes == 1) {
+        std::vector<uint16_t> w(h->nnz);
+        for (int64_t k = 0; k < h->nnz; ++k) w[k] = ((const uint8_t*)h->col_idx)[k];
+        MRS_CUDA_OK(cudaMemcpy(d.ci, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
+    } else {
+        MRS_CUDA_OK(cudaMemcpy(d.ci, h->col_idx, (size_t)h->nnz * d.ib, cudaMemcpyHostToDevice));
+    }
+    MRS_CUDA_OK(cudaMemcpy(d.v, h->values, (size_t)h->nnz * d.vb, cudaMemcpyHostToDevice));
+    return MRS_OK;
+}
+
+// diagonal of a host CSR in full precision (core.py:500-510); MRS_ERR_SINGULAR
+// when a row has no structural diagonal or a zero diagonal entry.
+int host_diag(const mrs_host_csr* h, std::vector<double>& d) {
+    d.assign(h->nrows, 0.0);
+    for (int64_t i = 0; i < h->nrows; ++i) {
+        bool found = false;
+        for (int64_t k = h->row_ptr[i]; k < h->row_ptr[i + 1]; ++k) {
+            int64_t c = h->idx_bytes == 4 ? ((const uint32_t*)h->col_idx)[k]
+                      : h->idx_bytes == 2 ? ((const uint16_t*)h->col_idx)[k]
+                                          : ((const uint8_t*)h->col_idx)[k];
+            if (c == i) {
+                d[i] = h->val_bytes == 8 ? ((const double*)h->values)[k]
+                                         : (double)((const float*)h->values)[k];
+                found = true;
+                break;
+            }
+        }
+        if (!found) return MRS_ERR_SINGULAR;
+    }
+    return MRS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int mrs_plan_create(const mrs_plan_desc* desc, mrs_plan** out) {
+    if (!desc || !out) return MRS_ERR_ARG;
+    if (desc->m < 1 || desc->m > kMaxM || desc->nrows < 1) return MRS_ERR_ARG;
+    if (desc->method != MRS_METHOD_CG && desc->method != MRS_METHOD_BICGSTAB) return MRS_ERR_UNSUPPORTED;
+    if (desc->precond < MRS_PC_NONE || desc->precond > MRS_PC_MG) return MRS_ERR_UNSUPPORTED;
+    int nl = desc->precond == MRS_PC_MG ? desc->nlevels : 1;
+    if (nl < 1) return MRS_ERR_ARG;
+    mrs_plan* p = new mrs_plan();
+    p->desc = *desc;
+    p->n = desc->nrows;
+    p->m = desc->m;
+    p->L.resize(nl);
+    *out = p;
+    return MRS_OK;
+}
+
+int mrs_plan_set_level(mrs_plan* p, int32_t l, const mrs_host_csr* A, const mrs_host_csr* P,
+                       const mrs_host_csr* R, double lmin, double lmax) {
+    if (!p || l < 0 || l >= (int)p->L.size() || !A) return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    LevelDev& lv = p->L[l];
+    int rc;
+    if ((rc = upload_csr(A, lv.A, p->owned))) return rc;
+    if ((rc = upload_csr(P, lv.P, p->owned))) return rc;
+    if ((rc = upload_csr(R, lv.R, p->owned))) return rc;
+    lv.lmin = lmin; lv.lmax = lmax;
+    std::vector<double> d;
+    const bool need_diag = !(l == (int)p->L.size() - 1 && p->desc.precond == MRS_PC_MG);
+    if (need_diag) {
+        if ((rc = host_diag(A, d))) return rc;
+        for (double v : d)
+            if (v == 0.0) return MRS_ERR_SINGULAR;
+        lv.d = dalloc<double>(d.size(), p->owned);
+        if (!lv.d) return MRS_ERR_ALLOC;
+        MRS_CUDA_OK(cudaMemcpy(lv.d, d.data(), d.size() * 8, cudaMemcpyHostToDevice));
+    }
+    return MRS_OK;
+}
+
+int mrs_plan_set_coarse_inverse(mrs_plan* p, const double* inv, int64_t nc) {
+    if (!p || !inv || nc < 1) return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    p->inv = dalloc<double>((size_t)nc * nc, p->owned);
+    if (!p->inv) return MRS_ERR_ALLOC;
+    p->nc = nc;
+    MRS_CUDA_OK(cudaMemcpy(p->inv, inv, (size_t)nc * nc * 8, cudaMemcpyHostToDevice));
+    return MRS_OK;
+}
+
+int mrs_plan_finalize(mrs_plan* p, void* stream) {
+    (void)stream;
+    if (!p) return MRS_ERR_ARG;
+    if (p->finalized) return MRS_OK;
+    const int64_t n = p->n, m = p->m;
+    auto& o = p->owned;
+    if (!p->L[0].A.present() || p->L[0].A.nrows != n) return MRS_ERR_STATE;
+    if (p->desc.precond == MRS_PC_MG) {
+        for (size_t l = 0; l + 1 < p->L.size(); ++l) {
+            LevelDev& lv = p->L[l];
+            if (!lv.A.present() || !lv.P.present() || !lv.R.present()) return MRS_ERR_STATE;
+        }
+        if (!p->inv || p->nc != p->L.back().A.nrows) return MRS_ERR_STATE;
+        for (size_t l = 0; l < p->L.size(); ++l) {
+            LevelDev& lv = p->L[l];
+            int64_t nl = lv.A.nrows;
+            if (l > 0) lv.b = dalloc<double>(nl * m, o);
+            lv.xa = dalloc<double>(nl * m, o);
+            lv.xb = dalloc<double>(nl * m, o);
+            lv.r = dalloc<double>(nl * m, o);
+            const mrs_plan_desc& d = p->desc;
+            bool cheb = d.pre.kind == MRS_SMOOTH_CHEBYSHEV || d.post.kind == MRS_SMOOTH_CHEBYSHEV;
+            if (cheb && l + 1 < p->L.size()) {
+                lv.dva = dalloc<double>(nl * m, o);
+                lv.dvb = dalloc<double>(nl * m, o);
+                if (!(lv.lmin > 0.0 && lv.lmin < lv.lmax)) return MRS_ERR_ARG;
+            }
+            if (!lv.xa || !lv.xb || !lv.r || (l > 0 && !lv.b)) return MRS_ERR_ALLOC;
+        }
+    } else if (p->desc.precond == MRS_PC_JACOBI) {
+        if (!p->L[0].d) return MRS_ERR_STATE;
+    }
+    size_t V = (size_t)n * m;
+    double** vecs[] = {&p->B, &p->X, &p->r, &p->r0, &p->p, &p->q, &p->v, &p->s,
+                       &p->t, &p->ph, &p->sh, &p->z, &p->zt};
+    for (double** v : vecs) {
+        *v = dalloc<double>(V, o);
+        if (!*v) return MRS_ERR_ALLOC;
+    }
+    p->st = dalloc<SolveState>(1, o);
+    p->history = dalloc<double>((size_t)(p->desc.max_iters + 1) * m, o);
+    p->partials = dalloc<double>((size_t)max_grid() * 3 * m, o);
+    p->ticket = dalloc<unsigned int>(1, o);
+    p->red_out = dalloc<double>(3 * m, o);
+    if (!p->st || !p->history || !p->partials || !p->ticket || !p->red_out) return MRS_ERR_ALLOC;
+    MRS_CUDA_OK(cudaMemset(p->ticket, 0, sizeof(unsigned int)));
+    SolveState hs;
+    memset(&hs, 0, sizeof(hs));
+    hs.tol = p->desc.rel_tol;
+    hs.m = (int)m;
+    hs.max_iters = p->desc.max_iters;
+    hs.history = p->history;
+    hs.err_col = 1 << 30;
+    hs.merged = p->desc.merged ? 1 : 0;
+    MRS_CUDA_OK(cudaMemcpy(p->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    MRS_CUDA_OK(cudaEventCreate(&p->ev0));
+    MRS_CUDA_OK(cudaEventCreate(&p->ev1));
+    p->finalized = true;
+    // estimate the per-iteration byte model / kernel count once
+    Program pg;
+    if (p->desc.method == MRS_METHOD_CG) build_cg(p, true, pg);
+    else build_bicgstab(p, true, pg);
+    p->it_bytes = pg.body_bytes;
+    p->body_kernels = (int)pg.body.size();
+    p->fixed_kernels = (int)(pg.pro.size() + pg.epi.size()) + 1;
+    return MRS_OK;
+}
+
+int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
+                   int32_t host_buffers, void* stream, mrs_stats* stats, double* final_rel,
+                   double* history) {
+    if (!p || !B || !X) return MRS_ERR_ARG;
+    if (!p->finalized) return MRS_ERR_STATE;
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)p->n * p->m * 8;
+    cudaMemcpyKind in = host_buffers ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    cudaMemcpyKind outk = host_buffers ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    MRS_CUDA_OK(cudaMemcpyAsync(p->B, B, bytes, in, s));
+    if (x_is_zero) MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
+    else MRS_CUDA_OK(cudaMemcpyAsync(p->X, X, bytes, in, s));
+    const bool eager = p->desc.exec == 1;
+    MRS_CUDA_OK(cudaEventRecord(p->ev0, s));
+    if (!eager) {
+        int gi = x_is_zero ? 1 : 0;
+        if (!p->exec[gi]) {
+            int rc = capture_graph(p, x_is_zero != 0, s);
+            if (rc) return rc;
+        }
+        MRS_CUDA_OK(cudaGraphLaunch(p->exec[gi], s));
+    } else {
+        Program pg;
+        // eager: no conditional handle; the host polls st->stop per iteration
+        set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);
+        MRS_CUDA_OK(cudaGetLastError());
+        if (p->desc.method == MRS_METHOD_CG) build_cg(p, x_is_zero != 0, pg);
+        else build_bicgstab(p, x_is_zero != 0, pg);
+        MRS_CUDA_OK(run_list(pg.pro, s));
+        for (;;) {
+            int stop = 0;
+            MRS_CUDA_OK(cudaMemcpyAsync(&stop, &p->st->stop, sizeof(int), cudaMemcpyDeviceToHost, s));
+            MRS_CUDA_OK(cudaStreamSynchronize(s));
+            if (stop) break;
+            MRS_CUDA_OK(run_list(pg.body, s));
+        }
+        MRS_CUDA_OK(run_list(pg.epi, s));
+    }
+    MRS_CUDA_OK(cudaEventRecord(p->ev1, s));
+    MRS_CUDA_OK(cudaMemcpyAsync(X, p->X, bytes, outk, s));
+    SolveState hs;
+    MRS_CUDA_OK(cudaMemcpyAsync(&hs, p->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    MRS_CUDA_OK(cudaStreamSynchronize(s));
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, p->ev0, p->ev1);
+    if (stats) {
+        stats->iterations = hs.it;
+        stats->status = hs.err;
+        stats->breakdown_column = hs.err == MRS_OK ? -1 : hs.err_col;
+        stats->breakdown_site = hs.err_site;
+        stats->device_ms = ms;
+    }
+    if (final_rel) memcpy(final_rel, hs.final_rel, sizeof(double) * p->m);
+    if (history) {
+        MRS_CUDA_OK(cudaMemcpy(history, p->history, sizeof(double) * (hs.it + 1) * p->m,
+                               cudaMemcpyDeviceToHost));
+    }
+    return hs.err == MRS_OK ? MRS_OK : MRS_ERR_BREAKDOWN;
+}
+
+double mrs_plan_iteration_bytes(const mrs_plan* p) { return p ? p->it_bytes : 0.0; }
+int mrs_plan_kernel_count(const mrs_plan* p) { return p ? p->body_kernels : 0; }
+int mrs_plan_fixed_kernel_count(const mrs_plan* p) { return p ? p->fixed_kernels : 0; }
+
+void mrs_plan_destroy(mrs_plan* p) { delete p; }
+
+}  // extern "C"

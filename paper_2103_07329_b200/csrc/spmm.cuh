@@ -1,0 +1,306 @@
+// spmm.cuh -- multi-RHS CSR SpMM engine and its fused smoother variants.
+//
+// Replaces the reference's `csr_spmv` (_ckernels.pyx:30-57) and the numpy
+// updates that follow it in the smoothers (blas2.py:176-181 Jacobi,
+// solvers.py:545-571 Chebyshev).
+//
+// Layout: the m right-hand sides of one row are contiguous (row-major (n, m)
+// block).  A row is owned by a group of LPR = M / CPL lanes; lane l owns the
+// CPL consecutive columns [l*CPL, (l+1)*CPL) and moves them with 16-byte
+// vector loads/stores, so a warp touches 32*CPL*8 contiguous bytes of y and
+// LPR*CPL*8 contiguous bytes of each gathered x row.  Each (row, column) is
+// accumulated sequentially in CSR entry order with separately rounded
+// mul/add, i.e. bitwise the reference kernel.
+//
+//   M   : 1  2  4  8  16  32  64   (0 = any m, generic path)
+//   CPL : 1  2  2  2   2   4   8
+//   LPR : 1  1  2  4   8   8   8
+//
+// Grid: persistent, min(rows/RPB, 8 * #SM) CTAs of 256 threads striding over
+// row groups (deterministic reduction shape for the fused dots).
+#pragma once
+
+#include "reduce.cuh"
+
+namespace mrs {
+
+template <int M> struct Lay {
+    static constexpr int CPL = (M == 1) ? 1 : (M <= 16 ? 2 : M / 8);
+    static constexpr int LPR = M / CPL;
+    static constexpr int RPB = kThreads / LPR;     // rows per CTA pass
+};
+
+// Kernel operation selector.
+enum SpOp : int {
+    OP_SPMV = 0,         // y op= A x by `mode`                         (csr_spmv)
+    OP_JAC_ZERO_RES,     // x1 = w*(b/d) (zero guess); r = b - A x1     (jacobi_sweep on zero x + residual)
+    OP_JAC_SWEEP,        // x' = x + w*((b - A x)/d)                    (jacobi_sweep)
+    OP_JAC_ZERO2,        // two sweeps from zero: x2 = x1 + w*((b - A x1)/d)
+    OP_CHEB_FIRST,       // r = b - A x; dv = r/(d*theta); x' = x + dv   (chebyshev_apply first step)
+    OP_CHEB_STEP,        // tmp = A dv; r -= tmp; dv' = dv*c1 + c2*(r/d); x += dv'
+    OP_CHEB_STEP_ZERO,   // same with dv = b/(d*theta), r = b, x = dv computed on the fly
+};
+
+struct SpArgs {
+    const int32_t* rp;
+    const void* ci;
+    const void* vals;
+    int64_t nrows;
+    int64_t m;              // runtime m (generic path / strides)
+    const double* x;        // gathered operand (x or dv)
+    const double* b;        // right-hand side (RSUB / smoothers)
+    const double* d;        // diagonal (smoothers)
+    double* y;              // OP_SPMV output
+    const double* x_in;     // own-row x (cheb step)
+    const double* r_in;     // own-row r (cheb step)
+    double* x_out;
+    double* r_out;
+    double* dv_out;
+    double w, theta, c1, c2;
+    int mode;
+    const int* guard;       // non-null: skip the kernel when *guard != 0
+    int dot;                // OP_SPMV: fuse sum_j x_own * y_out per column
+    RedArgs red;
+};
+
+// Value of the gathered operand at column `col` (CPL columns at cofs).
+template <int OP, int CPL>
+__device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t ld, int cofs) {
+    if constexpr (OP == OP_JAC_ZERO_RES || OP == OP_JAC_ZERO2) {
+        Vec<CPL> bb = load_vec<CPL>(a.b + col * ld + cofs);
+        double dd = __ldg(a.d + col);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) bb.v[i] = mul(a.w, divd(bb.v[i], dd));
+        return bb;
+    } else if constexpr (OP == OP_CHEB_STEP_ZERO) {
+        Vec<CPL> bb = load_vec<CPL>(a.b + col * ld + cofs);
+        double dt = mul(__ldg(a.d + col), a.theta);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) bb.v[i] = divd(bb.v[i], dt);
+        return bb;
+    } else {
+        return load_vec<CPL>(a.x + col * ld + cofs);
+    }
+}
+
+template <typename Ti>
+__device__ __forceinline__ int64_t colat(const void* ci, int64_t k) {
+    return (int64_t)__ldg(reinterpret_cast<const Ti*>(ci) + k);
+}
+
+// Accumulate one row: acc op= sum_k v_k * g(col_k), entry order.
+template <int OP, int CPL, typename Tv, typename Ti, bool SUBTRACT>
+__device__ __forceinline__ void row_accumulate(const SpArgs& a, int64_t lo, int64_t hi,
+                                               int64_t ld, int cofs, double (&acc)[CPL]) {
+    const Tv* __restrict__ vals = reinterpret_cast<const Tv*>(a.vals);
+    int64_t k = lo;
+    for (; k + 4 <= hi; k += 4) {
+        int64_t c0 = colat<Ti>(a.ci, k), c1 = colat<Ti>(a.ci, k + 1);
+        int64_t c2 = colat<Ti>(a.ci, k + 2), c3 = colat<Ti>(a.ci, k + 3);
+        double v0 = widen(__ldg(vals + k)), v1 = widen(__ldg(vals + k + 1));
+        double v2 = widen(__ldg(vals + k + 2)), v3 = widen(__ldg(vals + k + 3));
+        Vec<CPL> g0 = gather<OP, CPL>(a, c0, ld, cofs);
+        Vec<CPL> g1 = gather<OP, CPL>(a, c1, ld, cofs);
+        Vec<CPL> g2 = gather<OP, CPL>(a, c2, ld, cofs);
+        Vec<CPL> g3 = gather<OP, CPL>(a, c3, ld, cofs);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            if constexpr (SUBTRACT) {
+                acc[i] = sub(acc[i], mul(v0, g0.v[i]));
+                acc[i] = sub(acc[i], mul(v1, g1.v[i]));
+                acc[i] = sub(acc[i], mul(v2, g2.v[i]));
+                acc[i] = sub(acc[i], mul(v3, g3.v[i]));
+            } else {
+                acc[i] = add(acc[i], mul(v0, g0.v[i]));
+                acc[i] = add(acc[i], mul(v1, g1.v[i]));
+                acc[i] = add(acc[i], mul(v2, g2.v[i]));
+                acc[i] = add(acc[i], mul(v3, g3.v[i]));
+            }
+        }
+    }
+    for (; k < hi; ++k) {
+        int64_t c0 = colat<Ti>(a.ci, k);
+        double v0 = widen(__ldg(vals + k));
+        Vec<CPL> g0 = gather<OP, CPL>(a, c0, ld, cofs);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v0, g0.v[i]));
+            else acc[i] = add(acc[i], mul(v0, g0.v[i]));
+        }
+    }
+}
+
+// One (row, column-slice) of work for every op.  `dotp` accumulates the fused
+// dot (OP_SPMV with a.dot: x_own . y).
+template <int OP, int CPL, typename Tv, typename Ti>
+__device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld, int cofs,
+                                       double (&dotp)[CPL]) {
+    const int64_t lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
+    const int64_t o = row * ld + cofs;
+    double acc[CPL];
+    if constexpr (OP == OP_SPMV) {
+        const int mode = a.mode;
+        if (mode == MRS_MODE_ASSIGN) {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+        } else if (mode == MRS_MODE_RSUB) {
+            Vec<CPL> t = load_vec<CPL>(a.b + o);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
+        } else {
+            Vec<CPL> t = load_vec_rw<CPL>(a.y + o);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
+        }
+        if (mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD)
+            row_accumulate<OP, CPL, Tv, Ti, false>(a, lo, hi, ld, cofs, acc);
+        else
+            row_accumulate<OP, CPL, Tv, Ti, true>(a, lo, hi, ld, cofs, acc);
+        Vec<CPL> out;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
+        store_vec<CPL>(a.y + o, out);
+        if (a.dot) {
+            Vec<CPL> xo = load_vec<CPL>(a.x + o);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
+        }
+    } else if constexpr (OP == OP_JAC_ZERO_RES || OP == OP_JAC_SWEEP || OP == OP_JAC_ZERO2 ||
+                         OP == OP_CHEB_FIRST) {
+        // r = b - A x  (RSUB order: start at b, subtract in entry order)
+        Vec<CPL> bb = load_vec<CPL>(a.b + o);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
+        row_accumulate<OP, CPL, Tv, Ti, true>(a, lo, hi, ld, cofs, acc);
+        const double dd = __ldg(a.d + row);
+        Vec<CPL> xo;
+        if constexpr (OP == OP_JAC_ZERO_RES || OP == OP_JAC_ZERO2) {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) xo.v[i] = mul(a.w, divd(bb.v[i], dd));
+        } else {
+            xo = load_vec<CPL>(a.x + o);
+        }
+        Vec<CPL> out;
+        if constexpr (OP == OP_JAC_ZERO_RES) {
+            store_vec<CPL>(a.x_out + o, xo);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
+            store_vec<CPL>(a.r_out + o, out);
+        } else if constexpr (OP == OP_CHEB_FIRST) {
+            const double dt = mul(dd, a.theta);
+            Vec<CPL> dv;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                out.v[i] = acc[i];
+                dv.v[i] = divd(acc[i], dt);
+                xo.v[i] = add(xo.v[i], dv.v[i]);
+            }
+            store_vec<CPL>(a.r_out + o, out);
+            store_vec<CPL>(a.dv_out + o, dv);
+            store_vec<CPL>(a.x_out + o, xo);
+        } else {
+            // x + w * (r / d)   (blas2.py:181)
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) out.v[i] = add(xo.v[i], mul(a.w, divd(acc[i], dd)));
+            store_vec<CPL>(a.x_out + o, out);
+        }
+    } else {  // OP_CHEB_STEP / OP_CHEB_STEP_ZERO  (solvers.py:559-571)
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+        row_accumulate<OP, CPL, Tv, Ti, false>(a, lo, hi, ld, cofs, acc);   // tmp = A dv
+        const double dd = __ldg(a.d + row);
+        Vec<CPL> r, dv, xo;
+        if constexpr (OP == OP_CHEB_STEP_ZERO) {
+            r = load_vec<CPL>(a.b + o);
+            const double dt = mul(dd, a.theta);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) { dv.v[i] = divd(r.v[i], dt); xo.v[i] = dv.v[i]; }
+        } else {
+            r = load_vec<CPL>(a.r_in + o);
+            dv = load_vec<CPL>(a.x + o);
+            xo = load_vec_rw<CPL>(a.x_in + o);
+        }
+        Vec<CPL> dvn;
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            r.v[i] = sub(r.v[i], acc[i]);                                     // r -= A dv
+            dvn.v[i] = add(mul(dv.v[i], a.c1), mul(a.c2, divd(r.v[i], dd)));  // dv*c1 + c2*(r/d)
+            xo.v[i] = add(xo.v[i], dvn.v[i]);                                 // x += dv
+        }
+        store_vec<CPL>(a.x_out + o, xo);
+        if (a.r_out) store_vec<CPL>(a.r_out + o, r);
+        if (a.dv_out) store_vec<CPL>(a.dv_out + o, dvn);
+    }
+}
+
+template <int M, int OP, typename Tv, typename Ti>
+__global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
+    if (a.guard && *a.guard) return;
+    using L = Lay<M>;
+    constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
+    const int lane = threadIdx.x % LPR;
+    const int cofs = lane * CPL;
+    double dotp[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
+    for (int64_t row = (int64_t)blockIdx.x * RPB + threadIdx.x / LPR; row < a.nrows;
+         row += (int64_t)gridDim.x * RPB)
+        do_row<OP, CPL, Tv, Ti>(a, row, M, cofs, dotp);
+    if constexpr (OP == OP_SPMV) {
+        if (a.dot) {
+            // warp tree over row groups (lanes with equal column slice), then CTA
+            __shared__ double s_w[kThreads / 32][M];
+            __shared__ double s_blk[M];
+#pragma unroll
+            for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+                for (int i = 0; i < CPL; ++i)
+                    dotp[i] = add(dotp[i], __shfl_xor_sync(0xffffffffu, dotp[i], off));
+            const int warp = threadIdx.x / 32, wl = threadIdx.x % 32;
+            if (wl < LPR)
+#pragma unroll
+                for (int i = 0; i < CPL; ++i) s_w[warp][wl * CPL + i] = dotp[i];
+            __syncthreads();
+            if (threadIdx.x < M) {
+                double acc = s_w[0][threadIdx.x];
+                for (int w = 1; w < kThreads / 32; ++w) acc = add(acc, s_w[w][threadIdx.x]);
+                s_blk[threadIdx.x] = acc;
+            }
+            __syncthreads();
+            finish_reduction(a.red, s_blk, M, M);
+        }
+    }
+}
+
+// Generic m (any value, any layout): one thread per (row, column), thread
+// t of a CTA owns column t % m for RPB = 256 / m rows.
+template <int OP, typename Tv, typename Ti>
+__global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
+    if (a.guard && *a.guard) return;
+    const int m = (int)a.m;
+    const int rpb = kThreads / m;
+    const int c = threadIdx.x % m;
+    double dotp[1] = {0.0};
+    if (threadIdx.x < rpb * m) {
+        for (int64_t row = (int64_t)blockIdx.x * rpb + threadIdx.x / m; row < a.nrows;
+             row += (int64_t)gridDim.x * rpb)
+            do_row<OP, 1, Tv, Ti>(a, row, m, c, dotp);
+    }
+    if constexpr (OP == OP_SPMV) {
+        if (a.dot) {
+            __shared__ double s_t[kThreads];
+            __shared__ double s_blk[kMaxM];
+            s_t[threadIdx.x] = dotp[0];
+            __syncthreads();
+            if (threadIdx.x < m) {
+                double acc = s_t[threadIdx.x];
+                for (int t = threadIdx.x + m; t < rpb * m; t += m) acc = add(acc, s_t[t]);
+                s_blk[threadIdx.x] = acc;
+            }
+            __syncthreads();
+            finish_reduction(a.red, s_blk, m, m);
+        }
+    }
+}
+
+}  // namespace mrs

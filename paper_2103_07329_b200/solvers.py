@@ -1,0 +1,307 @@
+"""Solver composition on the GPU: ``prepare(config, A).run(B, X) -> SolveStats``.
+
+Drop-in for the reference's solve path (/root/reference/pkg/src/mrsolve/
+solvers.py:850-959): same ParamTree configuration, same SolveStats fields,
+same exception types.  ``prepare`` does all setup -- validation, the AMG
+hierarchy (native restatement of amg.setup, or a hierarchy passed in),
+Chebyshev eigenvalue bounds, the dense coarse inverse -- and uploads it
+once; ``run`` executes one whole solve on the device as a single CUDA graph
+launch (iteration loop driven on the device; see csrc/solver.cu).
+
+Device path: solver CG or BiCGStab (classical; merged=0/1),
+preconditioner none / Jacobi / MultiGrid V-cycle, smoothers Jacobi or
+Chebyshev.  Everything else the reference's ParamTree can express
+(Gauss-Seidel smoothing, RBiCGStab/PBiCGStab, Direct and stationary solvers)
+is outside this path and raises ConfigurationError -- there is no CPU
+fallback.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .amg import AmgParams, Hierarchy, coarse_inverse, estimate_eig_bounds, setup as amg_setup
+from .core import BlockVector, PrecisionTag, as_csr
+from .errors import (BreakdownError, ConfigurationError, InvalidArgumentError,
+                     ShapeMismatchError)
+from .params import METHOD_FAMILIES, ParamTree
+
+__all__ = ["SolveStats", "ConfiguredSolver", "prepare", "solve", "DevicePlan"]
+
+_BREAK_MSG = {
+    1: "CG search-direction curvature vanished",
+    2: "CG rho vanished",
+    3: "BiCGStab (r0, Ap) vanished",
+    4: "BiCGStab stabilization step vanished",
+    5: "BiCGStab rho vanished",
+    6: "BiCGStab omega vanished",
+}
+
+
+@dataclass
+class SolveStats:
+    """solvers.py:80-92."""
+
+    iterations: int
+    converged: np.ndarray
+    final_rel_residual: np.ndarray
+    residual_history: list = field(default_factory=list)
+    method: str = ""
+    device_ms: float = 0.0
+
+    @property
+    def all_converged(self) -> bool:
+        return bool(np.all(self.converged))
+
+
+@dataclass
+class ConfiguredSolver:
+    method: str
+    run: object
+    hierarchy: Hierarchy | None = None
+    plan_factory: object = None
+
+
+def _smoother(plist) -> _lib.mrs_smoother:
+    if plist is None:
+        raise ConfigurationError(
+            "MultiGrid needs explicit pre/post smoothers on the device path (the reference "
+            "default, hybrid Gauss-Seidel, is not implemented here; SURVEY.md 8(f))")
+    if plist.method == "Jacobi":
+        return _lib.mrs_smoother(_lib.SMOOTH_JACOBI, plist.get_int("max_iters"),
+                                 plist.get_float("weight"), 0)
+    if plist.method == "Chebyshev":
+        order = plist.get_int("polynomial_order")
+        if order < 1:
+            raise InvalidArgumentError("polynomial_order must be >= 1")
+        return _lib.mrs_smoother(_lib.SMOOTH_CHEBYSHEV, 1, 0.0, order)
+    raise ConfigurationError(f"smoother {plist.method!r} is not on the device path")
+
+
+class DevicePlan:
+    """One uploaded solver instance for a fixed RHS count m (owns a C plan)."""
+
+    def __init__(self, desc: _lib.mrs_plan_desc, levels, inv, method_name: str):
+        self.L = _lib.lib()
+        self.desc = desc
+        self.method = method_name
+        h = C.c_void_p()
+        _lib.check(self.L.mrs_plan_create(C.byref(desc), C.byref(h)), "plan create")
+        self.h = h
+        try:
+            for l, (A, P, R, bounds) in enumerate(levels):
+                keep: list = []
+                a = _lib.host_csr(A, keep)
+                p = _lib.host_csr(P, keep) if P is not None else None
+                r = _lib.host_csr(R, keep) if R is not None else None
+                lo, hi = bounds if bounds is not None else (0.0, 0.0)
+                _lib.check(self.L.mrs_plan_set_level(h, l, C.byref(a),
+                                                     C.byref(p) if p is not None else None,
+                                                     C.byref(r) if r is not None else None,
+                                                     float(lo), float(hi)), f"upload level {l}")
+            if inv is not None:
+                inv = np.ascontiguousarray(inv, dtype=np.float64)
+                _lib.check(self.L.mrs_plan_set_coarse_inverse(h, inv.ctypes.data, inv.shape[0]),
+                           "coarse inverse")
+            _lib.check(self.L.mrs_plan_finalize(h, None), "plan finalize")
+        except Exception:
+            self.L.mrs_plan_destroy(h)
+            self.h = None
+            raise
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            try:
+                self.L.mrs_plan_destroy(self.h)
+            except Exception:
+                pass
+            self.h = None
+
+    @property
+    def iteration_bytes(self) -> float:
+        return self.L.mrs_plan_iteration_bytes(self.h)
+
+    @property
+    def kernels_per_iteration(self) -> int:
+        return self.L.mrs_plan_kernel_count(self.h)
+
+    def kernel_launches(self, iterations: int) -> int:
+        """Kernels one solve of `iterations` iterations launches."""
+        return self.L.mrs_plan_fixed_kernel_count(self.h) + iterations * self.kernels_per_iteration
+
+    def solve(self, Bp: int, Xp: int, x_zero: bool, host: bool, stream=None):
+        m, maxit = int(self.desc.m), int(self.desc.max_iters)
+        st = _lib.mrs_stats()
+        rel = np.zeros(m)
+        hist = np.zeros((maxit + 1) * m)
+        rc = self.L.mrs_plan_solve(self.h, Bp, Xp, int(bool(x_zero)), int(bool(host)), stream,
+                                   C.byref(st), rel.ctypes.data, hist.ctypes.data)
+        if rc == _lib.MRS_ERR_BREAKDOWN:
+            raise BreakdownError(_BREAK_MSG.get(st.breakdown_site, "Krylov breakdown"),
+                                 column=int(st.breakdown_column))
+        _lib.check(rc, "solve")
+        it = int(st.iterations)
+        history = [hist[i * m:(i + 1) * m].copy() for i in range(it + 1)]
+        tol = float(self.desc.rel_tol)
+        return SolveStats(it, rel <= tol, rel, history, self.method, float(st.device_ms))
+
+
+def _vector_args(B, X):
+    """Resolve (B, X) into pointers: host BlockVectors/ndarrays or CUDA tensors."""
+    try:
+        import torch
+        is_t = isinstance(B, torch.Tensor)
+    except ImportError:       # pragma: no cover
+        is_t = False
+    if is_t:
+        import torch
+        for t, nm in ((B, "B"), (X, "X")):
+            if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64
+                    and t.dim() == 2 and t.is_contiguous()):
+                raise InvalidArgumentError(f"{nm} must be a contiguous (n, m) float64 CUDA tensor")
+        if B.shape != X.shape:
+            raise ShapeMismatchError(f"block vector shapes differ: {tuple(B.shape)} vs {tuple(X.shape)}")
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        return B.shape, B.data_ptr(), X.data_ptr(), False, False, stream, None
+    Bv = B if hasattr(B, "flags") and hasattr(B, "data") else BlockVector.from_array(B)
+    if not (hasattr(X, "flags") and hasattr(X, "data")):
+        raise InvalidArgumentError("X must be a BlockVector (or CUDA tensor)")
+    if Bv.data.shape != X.data.shape:
+        raise ShapeMismatchError(f"block vector shapes differ: {Bv.data.shape} vs {X.data.shape}")
+    if not Bv.flags.initialized:
+        raise InvalidArgumentError("residual needs an initialized right-hand side")
+    b = np.ascontiguousarray(Bv.data, dtype=np.float64)
+    if not X.data.flags.c_contiguous or X.data.dtype != np.float64:
+        raise InvalidArgumentError("X data must be C-contiguous float64")
+    x_zero = bool(X.flags.zero)
+    if not x_zero and not X.flags.initialized:
+        raise InvalidArgumentError("residual input vector is not initialized")
+    import torch
+    stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+    return b.shape, b.ctypes.data, X.data.ctypes.data, x_zero, True, stream, (b, X)
+
+
+def prepare(config: ParamTree, A, team=None, *, hierarchy=None, exec_mode: str = "graph",
+            eig_bounds=None) -> ConfiguredSolver:
+    """Build the device solver combination described by ``config``.
+
+    ``hierarchy``: optional pre-built hierarchy (ours or a reference
+    ``amg.Hierarchy``); otherwise the native reference setup runs here.
+    ``exec_mode``: "graph" (default, device-driven loop) or "eager".
+    ``team``: a :class:`~paper_2103_07329_b200.team.GpuTeam` for the
+    row-partitioned multi-GPU path (None = this process's current GPU).
+    """
+    if not config.finalized:
+        config.set_defaults()
+    violations = config.validate()
+    if violations:
+        raise ConfigurationError("; ".join(violations))
+    if team is not None and getattr(team, "world_size", 1) > 1:
+        from .team import prepare_distributed
+        return prepare_distributed(config, A, team, hierarchy=hierarchy, exec_mode=exec_mode)
+    Ab = as_csr(A)
+    if Ab.nrows != Ab.ncols:
+        raise InvalidArgumentError("the system matrix must be square")
+    sp = config.role("solver")
+    method = sp.method
+    family = METHOD_FAMILIES[method]
+    if family not in ("CG", "BiCGStab") or method in ("RBiCGStab", "PBiCGStab"):
+        raise ConfigurationError(
+            f"solver {method!r} is not on the device solve path (CG and classical BiCGStab "
+            "are; see SURVEY.md 8(f))")
+    tol = sp.get_float("rel_tolerance")
+    iters = sp.get_int("max_iters")
+    merged = bool(sp.get_int("merged")) if family == "BiCGStab" else False
+    name = "CG" if family == "CG" else ("BiCGStab" + ("/merged" if merged else ""))
+
+    pl = config.role("preconditioner")
+    desc = _lib.mrs_plan_desc()
+    desc.method = _lib.METHOD_CG if family == "CG" else _lib.METHOD_BICGSTAB
+    desc.nrows = Ab.nrows
+    desc.rel_tol = tol
+    desc.max_iters = iters
+    desc.exec = 0 if exec_mode == "graph" else 1
+    desc.merged = int(merged)
+    desc.mg_cycles = 1
+    desc.nlevels = 1
+    levels, inv, h = None, None, None
+    if pl is None:
+        desc.precond = _lib.PC_NONE
+        levels = [(Ab, None, None, None)]
+    elif pl.method == "Jacobi":
+        desc.precond = _lib.PC_JACOBI
+        desc.pc_weight = pl.get_float("weight")
+        desc.pc_sweeps = pl.get_int("max_iters")
+        levels = [(Ab, None, None, None)]
+    elif pl.method == "MultiGrid":
+        if pl.get_str("mg_cycle") != "V":
+            raise ConfigurationError("only the V cycle is implemented")
+        desc.precond = _lib.PC_MG
+        desc.mg_cycles = max(pl.get_int("max_iters"), 1)
+        desc.pre = _smoother(config.role("pre_smoother"))
+        desc.post = _smoother(config.role("post_smoother"))
+        if hierarchy is None:
+            params = AmgParams(strength_threshold=pl.get_float("mg_strength_threshold"),
+                               agg_num_levels=pl.get_int("mg_agg_num_levels"),
+                               num_paths=pl.get_int("mg_num_paths"),
+                               coarse_matrix_size=pl.get_int("mg_coarse_matrix_size"),
+                               max_levels=pl.get_int("mg_max_levels"))
+            h = amg_setup(Ab, params, mixed_precision=bool(pl.get_int("mg_mixed_precision")))
+        else:
+            h = Hierarchy.of(hierarchy)
+        cheb = _lib.SMOOTH_CHEBYSHEV in (desc.pre.kind, desc.post.kind)
+        levels = []
+        for l, lv in enumerate(h.levels):
+            bounds = None
+            if cheb and l < h.nlevels - 1:
+                if eig_bounds is not None:
+                    lv.eig_bounds = tuple(eig_bounds[l])
+                if lv.eig_bounds is None:
+                    lv.eig_bounds = estimate_eig_bounds(lv.A)
+                bounds = lv.eig_bounds
+                lmin, lmax = bounds
+                if not (0.0 < lmin < lmax):
+                    raise InvalidArgumentError(
+                        f"eigenvalue bounds must satisfy 0 < lmin < lmax, got {bounds}")
+            levels.append((lv.A, lv.P, lv.R, bounds))
+        inv = coarse_inverse(h.coarsest.A)
+        h.coarsest.lu = inv
+        desc.nlevels = h.nlevels
+    else:
+        raise ConfigurationError(f"preconditioner {pl.method!r} is not on the device path")
+
+    plans: dict = {}
+
+    def plan_for(m: int) -> DevicePlan:
+        if m not in plans:
+            d = _lib.mrs_plan_desc.from_buffer_copy(desc)
+            d.m = m
+            plans[m] = DevicePlan(d, levels, inv, name)
+        return plans[m]
+
+    def run(B, X, x_is_zero=None) -> SolveStats:
+        """Solve in place on X.  Host BlockVectors: the zero flag of X selects the
+        zero-guess path (like the reference); CUDA tensors: pass x_is_zero."""
+        shape, bp, xp, x_zero, host, stream, keep = _vector_args(B, X)
+        if x_is_zero is not None:
+            x_zero = bool(x_is_zero)
+        if shape[0] != Ab.nrows:
+            raise ShapeMismatchError(f"vector has {shape[0]} rows, matrix has {Ab.nrows}")
+        if shape[1] > 64:
+            raise InvalidArgumentError("at most 64 right-hand sides per solve")
+        stats = plan_for(shape[1]).solve(bp, xp, x_zero, host, stream)
+        if host:
+            X.flags.zero = False
+            X.flags.initialized = True
+        return stats
+
+    return ConfiguredSolver(method, run, h, plan_for)
+
+
+def solve(config: ParamTree, A, B, X, team=None) -> SolveStats:
+    """Prepare and run (solvers.py:956-959)."""
+    return prepare(config, A, team).run(B, X)

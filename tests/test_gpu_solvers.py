@@ -1,0 +1,193 @@
+"""Device solves vs the reference (golden) and the oracle.
+
+Parity contract (BASELINE.json north star): iteration counts within +-1 of
+the reference on the same seeded inputs and hierarchy, every column's
+recomputed final relative residual <= tol; here the arithmetic differs from
+the reference only in the dot-reduction order, so solutions agree far
+tighter (checked at 1e-6 relative to ||x||).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2103_07329_b200 import BlockVector, CsrBlock, gen_poisson3d  # noqa: E402
+from paper_2103_07329_b200.errors import BreakdownError, ConfigurationError  # noqa: E402
+from paper_2103_07329_b200.params import tree  # noqa: E402
+from paper_2103_07329_b200.solvers import prepare, solve  # noqa: E402
+
+import oracle.gen_golden as GG  # noqa: E402
+
+CASES = list(GG.SOLVE_CASES)
+
+
+@pytest.mark.parametrize("name", CASES)
+@pytest.mark.parametrize("mode", ["graph", "eager"])
+def test_golden_solves(golden_solves, name, mode):
+    g = golden_solves
+    grid, m, seed, roles = GG.SOLVE_CASES[name]
+    A, _ = gen_poisson3d(*grid)
+    B = g[f"{name}_B"]
+    cs = prepare(tree(roles), A, exec_mode=mode)
+    X = BlockVector.zeros(A.nrows, m)
+    st = cs.run(BlockVector.from_array(B), X)
+    it_ref = int(g[f"{name}_iters"])
+    tol = float(roles["solver"].get("rel_tolerance", 1e-8))
+    assert abs(st.iterations - it_ref) <= 1, (st.iterations, it_ref)
+    assert st.all_converged and np.all(st.final_rel_residual <= tol)
+    Xr = g[f"{name}_X"]
+    if st.iterations == it_ref:
+        err = np.linalg.norm(X.data - Xr, axis=0) / np.linalg.norm(Xr, axis=0)
+        assert err.max() < 1e-6, err
+        h = np.array(st.residual_history)
+        np.testing.assert_allclose(h, g[f"{name}_hist"], rtol=1e-5, atol=1e-14)
+
+
+def test_graph_and_eager_agree_bitwise():
+    A, _ = gen_poisson3d(12, 12, 12)
+    B = np.random.default_rng(3).uniform(-1, 1, (A.nrows, 4))
+    roles = GG.SOLVE_CASES["c2_amg_pcg"][3]
+    out = []
+    for mode in ("graph", "eager", "graph"):
+        X = BlockVector.zeros(A.nrows, 4)
+        st = prepare(tree(roles), A, exec_mode=mode).run(BlockVector.from_array(B), X)
+        out.append((st.iterations, X.data.copy()))
+    assert out[0][0] == out[1][0] == out[2][0]
+    np.testing.assert_array_equal(out[0][1], out[1][1])
+    np.testing.assert_array_equal(out[0][1], out[2][1])
+
+
+def test_rerun_same_prepared_solver_is_reproducible():
+    A, b = gen_poisson3d(8, 8, 8)
+    cs = prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"},
+                       "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+                       "post_smoother": {"method": "Jacobi", "weight": "0.8"}}), A)
+    x1 = BlockVector.zeros(512, 1)
+    s1 = cs.run(b, x1)
+    x2 = BlockVector.zeros(512, 1)
+    s2 = cs.run(b, x2)
+    np.testing.assert_array_equal(x1.data, x2.data)
+    assert s1.iterations == s2.iterations and s1.all_converged
+
+
+def test_cg_two_by_two_exact():
+    a = np.array([[4.0, 1.0], [1.0, 3.0]])
+    x = BlockVector.zeros(2, 1)
+    st = solve(tree({"solver": {"method": "CG", "rel_tolerance": "1e-14"}}),
+               CsrBlock.from_dense(a), BlockVector.from_array([1.0, 2.0]), x)
+    np.testing.assert_allclose(x.data[:, 0], [1 / 11, 7 / 11], rtol=1e-12)
+    assert st.iterations <= 2 and st.all_converged
+
+
+def test_bicgstab_identity_one_iteration():
+    x = BlockVector.zeros(5, 2)
+    b = np.arange(10.0).reshape(5, 2) + 1
+    st = solve(tree({"solver": {"method": "BiCGStab"}}), CsrBlock.from_dense(np.eye(5)),
+               BlockVector.from_array(b), x)
+    assert st.iterations == 1
+    np.testing.assert_allclose(x.data, b, rtol=1e-14)
+
+
+def test_zero_rhs_zero_iterations():
+    A, _ = gen_poisson3d(4, 4, 4)
+    x = BlockVector.zeros(64, 2)
+    st = solve(tree({"solver": {"method": "CG"}}), A, BlockVector.zeros(64, 2), x)
+    assert st.iterations == 0 and st.all_converged
+    np.testing.assert_array_equal(x.data, 0.0)
+
+
+def test_zero_rhs_column_stays_zero():
+    A, _ = gen_poisson3d(5, 5, 5)
+    b = np.zeros((125, 2))
+    b[:, 1] = np.random.default_rng(0).standard_normal(125)
+    x = BlockVector.zeros(125, 2)
+    st = solve(tree({"solver": {"method": "CG", "rel_tolerance": "1e-10"}}), A,
+               BlockVector.from_array(b), x)
+    assert st.all_converged
+    np.testing.assert_array_equal(x.data[:, 0], 0.0)
+
+
+def test_breakdown_raises_with_column():
+    a = np.array([[1.0, 0.0], [0.0, -1.0]])
+    with pytest.raises(BreakdownError) as ei:
+        solve(tree({"solver": {"method": "CG"}}), CsrBlock.from_dense(a),
+              BlockVector.from_array([1.0, 1.0]), BlockVector.zeros(2, 1))
+    assert ei.value.column == 0
+
+
+def test_nonzero_initial_guess_at_solution():
+    A, b = gen_poisson3d(6, 6, 6)
+    x = BlockVector.from_array(np.ones(216))
+    st = solve(tree({"solver": {"method": "CG", "rel_tolerance": "1e-10"}}), A, b, x)
+    assert st.iterations == 0
+
+
+def test_max_iters_respected():
+    A, _ = gen_poisson3d(10, 10, 10)
+    B = np.random.default_rng(1).uniform(-1, 1, (1000, 2))
+    x = BlockVector.zeros(1000, 2)
+    st = solve(tree({"solver": {"method": "CG", "max_iters": "5"}}), A, BlockVector.from_array(B), x)
+    assert st.iterations == 5 and not st.all_converged
+    assert len(st.residual_history) == 6
+
+
+def test_joint_equals_single_rhs():
+    """Joint m-RHS solve equals m single-RHS solves (tests/test_acceptance.py:97-136)."""
+    A, _ = gen_poisson3d(10, 10, 10)
+    B = np.random.default_rng(5).uniform(-1, 1, (1000, 4))
+    roles = {"solver": {"method": "BiCGStab", "rel_tolerance": "1e-10"},
+             "preconditioner": {"method": "MultiGrid", "mg_coarse_matrix_size": "60"},
+             "pre_smoother": {"method": "Chebyshev"}, "post_smoother": {"method": "Chebyshev"}}
+    cs = prepare(tree(roles), A)
+    X = BlockVector.zeros(1000, 4)
+    cs.run(BlockVector.from_array(B), X)
+    for j in range(4):
+        xj = BlockVector.zeros(1000, 1)
+        cs.run(BlockVector.from_array(B[:, j:j + 1]), xj)
+        np.testing.assert_allclose(X.data[:, j], xj.data[:, 0], rtol=1e-10, atol=1e-12)
+
+
+def test_device_tensor_run_matches_host_run():
+    A, _ = gen_poisson3d(12, 12, 12)
+    B = np.random.default_rng(2).uniform(-1, 1, (A.nrows, 8))
+    cs = prepare(tree(GG.SOLVE_CASES["c2_amg_pcg"][3]), A)
+    Xh = BlockVector.zeros(A.nrows, 8)
+    s1 = cs.run(BlockVector.from_array(B), Xh)
+    Bd = torch.from_numpy(B).cuda()
+    Xd = torch.zeros_like(Bd)
+    s2 = cs.run(Bd, Xd)
+    assert s1.iterations == s2.iterations
+    np.testing.assert_array_equal(Xd.cpu().numpy(), Xh.data)
+
+
+def test_unsupported_configs_raise():
+    A, _ = gen_poisson3d(4, 4, 4)
+    with pytest.raises(ConfigurationError):
+        prepare(tree({"solver": {"method": "PBiCGStab"}}), A)
+    with pytest.raises(ConfigurationError):
+        prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"}}), A)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 16, 32, 64])
+def test_rhs_counts_vs_oracle_iterations(m):
+    from oracle import oracle as O
+    from oracle.amg_setup import setup as osetup
+    A, _ = gen_poisson3d(14, 13, 12)
+    B = np.random.default_rng(m).uniform(-1, 1, (A.nrows, m))
+    roles = {"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"},
+             "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+             "post_smoother": {"method": "Jacobi", "weight": "0.8"}}
+    X = BlockVector.zeros(A.nrows, m)
+    st = prepare(tree(roles), A).run(BlockVector.from_array(B), X)
+    Ao = O.Csr.of(A)
+    mg = O.MultiGrid(osetup(Ao), ("jacobi", 0.8, 1), ("jacobi", 0.8, 1))
+    Xo = np.zeros_like(B)
+    so = O.cg_solve(Ao, B, Xo, mg, 1e-8, 100)
+    assert abs(st.iterations - so.iterations) <= 1
+    assert st.all_converged
+    np.testing.assert_allclose(X.data, Xo, rtol=1e-6, atol=1e-9)
