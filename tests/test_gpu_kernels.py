@@ -54,11 +54,9 @@ def test_spmv_golden_bitwise(golden_kernels):
 @pytest.mark.parametrize("vdt", [np.float64, np.float32])
 @pytest.mark.parametrize("width", [np.uint16, np.uint32])
 def test_spmv_random_vs_oracle_bitwise(m, vdt, width, rng):
+    from mrs_testutil import random_csr
     n = 3000 if width == np.uint16 else 70001
-    import scipy.sparse as sp
-    A = sp.random(n, n, density=12.0 / n, random_state=int(rng.integers(1 << 30)), format="csr")
-    A = A + sp.eye(n) * 3.0
-    blk = CsrBlock.from_scipy(A)
+    blk = random_csr(n, n, 12.0, rng)
     ci = blk.col_idx.astype(width)
     v = blk.values.astype(vdt)
     x = rng.standard_normal((n, m))
