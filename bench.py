@@ -78,6 +78,9 @@ def parse():
     ap.add_argument("--no-spmm", action="store_true", help="skip the config-5 SpMM sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--quick", action="store_true", help="small SpMM sweep (m=8 only)")
+    ap.add_argument("--exec", default="graph", choices=["graph", "eager"],
+                    help="eager: per-kernel launches (ncu cannot profile kernels inside "
+                         "graphs with conditional nodes)")
     return ap.parse_args()
 
 
@@ -270,7 +273,7 @@ def main():
     n = A.nrows
     B = np.random.default_rng(SEED).uniform(-1.0, 1.0, (n, M))
     t0 = time.perf_counter()
-    cs = prepare(tree(ROLES), A)
+    cs = prepare(tree(ROLES), A, exec_mode=args.exec)
     plan = cs.plan_factory(M)
     setup_s = time.perf_counter() - t0
     Bd = torch.from_numpy(B).cuda()

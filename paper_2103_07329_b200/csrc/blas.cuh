@@ -25,8 +25,7 @@ enum VecOp : int {
     V_CG_UPDATE,      // x += a*p; r += na*q; sum r*r          (cg_solve:176-178)
     V_CG_UPDATE_JAC,  // ... and z = w*(r/d); sum r*z          (+ Jacobi preconditioner)
     V_P_UPDATE,       // p = b*p + z                            (cg_solve:185)
-    V_JAC_ZERO,       // x = w*(b/d)                            (jacobi_sweep, zero x)
-    V_CHEB_ZERO1,     // x = b/(d*theta)                        (chebyshev order 1, zero x)
+    V_SEED,           // y = seed(x): w*(x/d) or x/(d*theta)     (zero-guess first smoother step)
     V_BICG_P,         // p = beta*(p + nw*v) + r                (bicgstab:250-251)
     V_BICG_S,         // s = r + na*v                           (bicgstab:262-263)
     V_DOT3,           // (t.s, t.t, s.s)                        (bicgstab:271 + :273)
@@ -54,6 +53,10 @@ struct VArgs {
     double wt, theta;                                      // Jacobi weight / Chebyshev theta
     const int* guard;
     const int* guard_it;     // V_BICG_P: no-op while *guard_it == 0 (first iteration)
+    int seed;                // 1/2: also write seed_out = seed(produced vector) (spmm.cuh)
+    double* seed_out;
+    const double* seed_d;
+    double seed_w;           // Jacobi weight or Chebyshev theta
     RedArgs red;
 };
 
@@ -94,6 +97,12 @@ __device__ __forceinline__ void block_reduce_cols(double (&acc)[K], int m, doubl
     __syncthreads();
 }
 
+// Zero-guess smoother seed of a produced value v at row i (spmm.cuh seed_value).
+__device__ __forceinline__ double seed_of(const VArgs& A, double v, int64_t i) {
+    const double d = __ldg(A.seed_d + i);
+    return A.seed == 1 ? mul(A.seed_w, divd(v, d)) : divd(v, mul(d, A.seed_w));
+}
+
 template <int OP>
 __device__ __forceinline__ void vec_elem(const VArgs& A, int64_t i, int64_t e, int c,
                                          double sa, double sb, double sc,
@@ -118,13 +127,16 @@ __device__ __forceinline__ void vec_elem(const VArgs& A, int64_t i, int64_t e, i
         acc[0] = add(acc[0], mul(__ldg(A.z + e), t));
         acc[1] = add(acc[1], mul(t, t));
     } else if constexpr (OP == V_COPY) {
-        A.y[e] = __ldg(A.x + e);
+        const double v = __ldg(A.x + e);
+        A.y[e] = v;
+        if (A.seed) A.seed_out[e] = seed_of(A, v, i);
     } else if constexpr (OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC) {
         // X = 1*X + alpha*p ; r = 1*r + (-alpha)*q   (axpby, blas.py:144)
         A.y[e] = add(A.y[e], mul(sa, __ldg(A.x + e)));
         double r = add(A.y2[e], mul(sb, __ldg(A.u + e)));
         A.y2[e] = r;
         acc[0] = add(acc[0], mul(r, r));
+        if (A.seed) A.seed_out[e] = seed_of(A, r, i);
         if constexpr (OP == V_CG_UPDATE_JAC) {
             // z = 0 + w*(r/d) (jacobi_sweep from a zero guess, blas2.py:181)
             double zz = mul(A.wt, divd(r, __ldg(A.d + i)));
@@ -133,16 +145,18 @@ __device__ __forceinline__ void vec_elem(const VArgs& A, int64_t i, int64_t e, i
         }
     } else if constexpr (OP == V_P_UPDATE) {
         A.y[e] = add(mul(sb, A.y[e]), __ldg(A.x + e));
-    } else if constexpr (OP == V_JAC_ZERO) {
-        A.y[e] = mul(A.wt, divd(__ldg(A.x + e), __ldg(A.d + i)));
-    } else if constexpr (OP == V_CHEB_ZERO1) {
-        A.y[e] = divd(__ldg(A.x + e), mul(__ldg(A.d + i), A.theta));
+    } else if constexpr (OP == V_SEED) {
+        A.y[e] = seed_of(A, __ldg(A.x + e), i);
     } else if constexpr (OP == V_BICG_P) {
         // p -= omega v ; p = r + beta p  (two axpby passes fused, same rounding)
         double t = add(A.y[e], mul(sc, __ldg(A.v + e)));
-        A.y[e] = add(mul(sb, t), __ldg(A.x + e));
+        double p = add(mul(sb, t), __ldg(A.x + e));
+        A.y[e] = p;
+        if (A.seed) A.seed_out[e] = seed_of(A, p, i);
     } else if constexpr (OP == V_BICG_S) {
-        A.y[e] = add(__ldg(A.x + e), mul(sa, __ldg(A.v + e)));
+        double s = add(__ldg(A.x + e), mul(sa, __ldg(A.v + e)));
+        A.y[e] = s;
+        if (A.seed) A.seed_out[e] = seed_of(A, s, i);
     } else if constexpr (OP == V_DOT3) {
         double t = __ldg(A.x + e), s = __ldg(A.s + e);
         acc[0] = add(acc[0], mul(t, s));

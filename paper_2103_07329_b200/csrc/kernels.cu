@@ -64,12 +64,9 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
     if (A.nrows == 0) return cudaSuccess;
     switch (op) {
     case OP_SPMV: return spmm_op<OP_SPMV>(A, a, m, s, generic);
-    case OP_JAC_ZERO_RES: return spmm_op<OP_JAC_ZERO_RES>(A, a, m, s, generic);
     case OP_JAC_SWEEP: return spmm_op<OP_JAC_SWEEP>(A, a, m, s, generic);
-    case OP_JAC_ZERO2: return spmm_op<OP_JAC_ZERO2>(A, a, m, s, generic);
     case OP_CHEB_FIRST: return spmm_op<OP_CHEB_FIRST>(A, a, m, s, generic);
     case OP_CHEB_STEP: return spmm_op<OP_CHEB_STEP>(A, a, m, s, generic);
-    case OP_CHEB_STEP_ZERO: return spmm_op<OP_CHEB_STEP_ZERO>(A, a, m, s, generic);
     }
     return cudaErrorInvalidValue;
 }
@@ -93,8 +90,7 @@ cudaError_t launch_vec(int op, VArgs a, cudaStream_t s) {
     case V_CG_UPDATE: return vec_op<V_CG_UPDATE>(a, s);
     case V_CG_UPDATE_JAC: return vec_op<V_CG_UPDATE_JAC>(a, s);
     case V_P_UPDATE: return vec_op<V_P_UPDATE>(a, s);
-    case V_JAC_ZERO: return vec_op<V_JAC_ZERO>(a, s);
-    case V_CHEB_ZERO1: return vec_op<V_CHEB_ZERO1>(a, s);
+    case V_SEED: return vec_op<V_SEED>(a, s);
     case V_BICG_P: return vec_op<V_BICG_P>(a, s);
     case V_BICG_S: return vec_op<V_BICG_S>(a, s);
     case V_DOT3: return vec_op<V_DOT3>(a, s);

@@ -56,6 +56,7 @@ enum Epilogue : int {
     EPI_BICG_RNORM,    // out = (r0.r, r.r)   -> rnorm, history, stop, beta
     EPI_FINAL,         // out = r.r (true residual) -> final_rel
     EPI_CG_RNORM_BETA, // out = (r.r, r.z)     -> EPI_CG_RNORM then, if not converged, EPI_CG_BETA
+    EPI_CG_RNORM_BETA1,// out = r.r, z = r (no preconditioner): same with r.z = r.r
 };
 
 // Breakdown sites, reported to the host for the exception message.
@@ -145,7 +146,9 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
         }
         return;
     }
-    case EPI_CG_RNORM_BETA: {
+    case EPI_CG_RNORM_BETA:
+    case EPI_CG_RNORM_BETA1: {
+        const int zo = epi == EPI_CG_RNORM_BETA ? m : 0;
         bool conv = true;
         if (act) {
             double rn = sqrt(v[c]);
@@ -155,8 +158,8 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
         }
         int all = __syncthreads_and(conv);
         if (!all && act) {
-            st->beta[c] = coef(v[m + c], st->rho[c], st->rnorm[c], c, st, BRK_CG_RHO, bad);
-            st->rho[c] = v[m + c];
+            st->beta[c] = coef(v[zo + c], st->rho[c], st->rnorm[c], c, st, BRK_CG_RHO, bad);
+            st->rho[c] = v[zo + c];
         }
         int anybad = __syncthreads_or(bad);
         if (threadIdx.x == 0) {

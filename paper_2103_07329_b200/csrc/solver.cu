@@ -93,6 +93,17 @@ namespace {
 // schedule builder
 // ---------------------------------------------------------------------------
 
+// Where the zero-guess first smoother step of a level lands (see spmm.cuh
+// seed_value): the producer of the level's right-hand side writes it.
+struct Seed {
+    int mode = 0;             // 0 none, 1 Jacobi w*(b/d), 2 Chebyshev b/(d*theta)
+    double* out = nullptr;
+    const double* d = nullptr;
+    double w = 0.0;           // Jacobi weight or Chebyshev theta
+};
+
+struct XB { double* cur; double* alt; void swap() { std::swap(cur, alt); } };
+
 struct Builder {
     mrs_plan* P;
     std::vector<Launch>* out;
@@ -107,6 +118,8 @@ struct Builder {
         r.st = P->st; r.epi = epi;
         return r;
     }
+    static SpArgs sp0() { SpArgs a; memset(&a, 0, sizeof(a)); return a; }
+    static VArgs v0() { VArgs a; memset(&a, 0, sizeof(a)); return a; }
 
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
@@ -122,144 +135,160 @@ struct Builder {
         bytes += b;
         kernels++;
     }
-    static SpArgs sp0() { SpArgs a; memset(&a, 0, sizeof(a)); return a; }
-    static VArgs v0() { VArgs a; memset(&a, 0, sizeof(a)); return a; }
+    static void set_seed(VArgs& a, const Seed& sd) {
+        a.seed = sd.mode; a.seed_out = sd.out; a.seed_d = sd.d; a.seed_w = sd.w;
+    }
+    double seed_bytes(const Seed& sd, int64_t n) const {
+        return sd.mode ? V(n) + 8.0 * n : 0.0;
+    }
 
-    // y = A x (mode), optionally with fused dot x.y -> epilogue
+    // y = A x (mode); optional fused dot (dvec or x own row) . y -> epilogue;
+    // optional seed of y for the level whose diagonal is sd.d.
     void spmv(const DevCsr& A, const double* x, double* y, int mode, const double* b = nullptr,
-              int dot_epi = -1) {
+              int dot_epi = -1, const double* dvec = nullptr, const Seed& sd = Seed()) {
         SpArgs a = sp0();
         a.x = x; a.y = y; a.b = b; a.mode = mode;
         double vb = V(A.ncols) + V(A.nrows) + (mode == MRS_MODE_ASSIGN ? 0 : V(A.nrows));
-        if (dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); vb += V(A.nrows); }
+        if (dot_epi >= 0) {
+            a.dot = 1; a.red = red(dot_epi); a.x_in = dvec; vb += V(A.nrows);
+        }
+        if (sd.mode) {
+            a.seed = sd.mode; a.seed_out = sd.out; a.d = sd.d;
+            if (sd.mode == 1) a.w = sd.w; else a.theta = sd.w;
+            vb += seed_bytes(sd, A.nrows);
+        }
         spmm(OP_SPMV, A, a, vb);
     }
-
     void dot(const double* x, const double* y, int64_t n, int epi) {
         VArgs a = v0(); a.n = n; a.x = x; a.z = y; a.red = red(epi);
         vec(V_DOT, a, 2 * V(n));
     }
-    void copy(const double* x, double* y, int64_t n) {
-        VArgs a = v0(); a.n = n; a.x = x; a.y = y;
-        vec(V_COPY, a, 2 * V(n));
+    void copy(const double* x, double* y, int64_t n, const Seed& sd = Seed()) {
+        VArgs a = v0(); a.n = n; a.x = x; a.y = y; set_seed(a, sd);
+        vec(V_COPY, a, 2 * V(n) + seed_bytes(sd, n));
+    }
+    void seed_kernel(const double* b, int64_t n, const Seed& sd) {
+        VArgs a = v0(); a.n = n; a.x = b; a.y = sd.out; set_seed(a, sd);
+        vec(V_SEED, a, 2 * V(n) + 8.0 * n);
     }
 
     // ---- smoothers -----------------------------------------------------
-    // Current-buffer bookkeeping: `cur` holds x; `alt` is the spare.
-    struct XB { double* cur; double* alt; void swap() { std::swap(cur, alt); } };
+    static bool coarsest(const mrs_plan& p, int l) {
+        return p.desc.precond == MRS_PC_MG && l == (int)p.L.size() - 1;
+    }
 
-    // One pre-smoothing application on a ZERO x, then r = b - A x in lv.r.
-    void pre_smooth_zero_and_residual(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x) {
-        const DevCsr& A = lv.A;
-        int64_t n = A.nrows;
+    // Seed a level needs when entered with a zero x (buffers of x given).
+    Seed level_seed(int l, const XB& x) const {
+        const mrs_plan& p = *P;
+        Seed sd;
+        if (coarsest(p, l)) return sd;
+        const LevelDev& lv = p.L[l];
+        const mrs_smoother& sm = p.desc.precond == MRS_PC_JACOBI
+                                     ? mrs_smoother{MRS_SMOOTH_JACOBI, p.desc.pc_sweeps,
+                                                    p.desc.pc_weight, 0}
+                                     : p.desc.pre;
+        sd.d = lv.d;
         if (sm.kind == MRS_SMOOTH_JACOBI) {
-            int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
-            if (sm.weight == 0.0) {
-                // weight 0: sweep is a no-op (blas2.py:487-489); x stays 0
-                VArgs z = v0(); z.n = n; z.x = b; z.y = x.cur; z.d = lv.d; z.wt = 0.0;
-                vec(V_JAC_ZERO, z, 2 * V(n) + 8.0 * n);
-                residual(lv, b, x.cur);
-                return;
-            }
-            if (sweeps == 1) {
-                SpArgs a = sp0(); a.b = b; a.d = lv.d; a.w = sm.weight; a.x_out = x.cur; a.r_out = lv.r;
-                spmm(OP_JAC_ZERO_RES, A, a, 3 * V(n) + 8.0 * n);
-                return;
-            }
-            SpArgs a = sp0(); a.b = b; a.d = lv.d; a.w = sm.weight; a.x_out = x.cur;
-            spmm(OP_JAC_ZERO2, A, a, 2 * V(n) + 8.0 * n);
-            for (int k = 2; k < sweeps; ++k) jacobi_sweep(lv, b, sm.weight, x);
-            residual(lv, b, x.cur);
+            sd.mode = 1; sd.out = x.cur; sd.w = sm.weight;
         } else {
-            chebyshev(lv, b, sm.order, /*zero=*/true, x);
-            residual(lv, b, x.cur);
+            sd.mode = 2; sd.w = 0.5 * (lv.lmax + lv.lmin);
+            sd.out = sm.order <= 1 ? x.cur : lv.dva;
         }
+        return sd;
     }
 
-    void residual(LevelDev& lv, const double* b, const double* x) {
-        spmv(lv.A, x, lv.r, MRS_MODE_RSUB, b);
-    }
-
-    void jacobi_sweep(LevelDev& lv, const double* b, double w, XB& x) {
+    void jacobi_sweep(LevelDev& lv, const double* b, double w, XB& x, int dot_epi) {
         SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.w = w; a.x_out = x.alt;
-        spmm(OP_JAC_SWEEP, lv.A, a, 3 * V(lv.A.nrows) + 8.0 * lv.A.nrows);
+        double eb = 3 * V(lv.A.nrows) + 8.0 * lv.A.nrows;
+        if (dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); }
+        spmm(OP_JAC_SWEEP, lv.A, a, eb);
         x.swap();
     }
 
-    // chebyshev_apply (solvers.py:520-571) on x (zero or not), result in x.cur.
-    void chebyshev(LevelDev& lv, const double* b, int order, bool zero, XB& x) {
+    // Chebyshev recurrence steps k0..order-1 (solvers.py:559-571); dv_cur holds dv.
+    void cheb_steps(LevelDev& lv, const double* b, int order, int k0, double rho,
+                    const double* r_in, const double* x_in, double* dv_cur, double* dv_alt,
+                    XB& x, int dot_epi) {
         const double lmin = lv.lmin, lmax = lv.lmax;
-        const double theta = 0.5 * (lmax + lmin);
-        const double delta = 0.5 * (lmax - lmin);
+        const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin);
         const double sigma = theta / delta;
-        double rho = 1.0 / sigma;
-        int64_t n = lv.A.nrows;
-        double* dv_cur = lv.dva;
-        double* dv_alt = lv.dvb;
-        if (order < 1) order = 1;
-        if (zero && order == 1) {
-            VArgs a = v0(); a.n = n; a.x = b; a.y = x.cur; a.d = lv.d; a.theta = theta;
-            vec(V_CHEB_ZERO1, a, 2 * V(n) + 8.0 * n);
+        const int64_t n = lv.A.nrows;
+        for (int k = k0; k < order; ++k) {
+            const double rho_new = 1.0 / (2.0 * sigma - rho);
+            SpArgs a = sp0(); a.x = dv_cur; a.x_in = x_in; a.r_in = r_in; a.d = lv.d; a.b = b;
+            a.c1 = rho_new * rho; a.c2 = 2.0 * rho_new / delta;
+            a.x_out = x.cur;
+            const bool more = k + 1 < order;
+            a.r_out = more ? lv.r : nullptr;
+            a.dv_out = more ? dv_alt : nullptr;
+            double eb = 4 * V(n) + 8.0 * n + (more ? 2 * V(n) : 0);
+            if (!more && dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); eb += V(n); }
+            spmm(OP_CHEB_STEP, lv.A, a, eb);
+            rho = rho_new;
+            std::swap(dv_cur, dv_alt);
+            r_in = lv.r;
+            x_in = x.cur;
+        }
+    }
+
+    // Smoother on a NONZERO x (post-smoothing; pre-smoothing of later cycles).
+    void smooth_nonzero(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x, int dot_epi) {
+        const int64_t n = lv.A.nrows;
+        if (sm.kind == MRS_SMOOTH_JACOBI) {
+            if (sm.weight == 0.0) {          // blas2.py:487-489: no-op
+                if (dot_epi >= 0) dot(b, x.cur, n, dot_epi);
+                return;
+            }
+            const int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
+            for (int k = 0; k < sweeps; ++k)
+                jacobi_sweep(lv, b, sm.weight, x, k == sweeps - 1 ? dot_epi : -1);
             return;
         }
-        int k0 = 0;
-        if (zero) {
-            // first step (dv = b/(d*theta), x = dv) folded into the second
-            double rho_new = 1.0 / (2.0 * sigma - rho);
-            SpArgs a = sp0(); a.b = b; a.d = lv.d; a.theta = theta;
-            a.c1 = rho_new * rho; a.c2 = 2.0 * rho_new / delta;
-            a.x_out = x.cur;
-            bool more = order > 2;
-            a.r_out = more ? lv.r : nullptr;
-            a.dv_out = more ? dv_alt : nullptr;
-            spmm(OP_CHEB_STEP_ZERO, lv.A, a, V(n) + 8.0 * n + V(n) + (more ? 2 * V(n) : 0));
-            rho = rho_new;
-            std::swap(dv_cur, dv_alt);
-            k0 = 2;
-        } else {
-            SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.theta = theta;
-            a.x_out = x.alt; a.r_out = lv.r; a.dv_out = dv_cur;
-            spmm(OP_CHEB_FIRST, lv.A, a, 5 * V(n) + 8.0 * n);
-            x.swap();
-            k0 = 1;
-        }
-        for (int k = k0; k < order; ++k) {
-            double rho_new = 1.0 / (2.0 * sigma - rho);
-            SpArgs a = sp0(); a.x = dv_cur; a.x_in = x.cur; a.r_in = lv.r; a.d = lv.d;
-            a.c1 = rho_new * rho; a.c2 = 2.0 * rho_new / delta;
-            a.x_out = x.cur;
-            bool more = k + 1 < order;
-            a.r_out = more ? lv.r : nullptr;
-            a.dv_out = more ? dv_alt : nullptr;
-            spmm(OP_CHEB_STEP, lv.A, a, 4 * V(n) + 8.0 * n + (more ? 2 * V(n) : 0));
-            rho = rho_new;
-            std::swap(dv_cur, dv_alt);
-        }
+        const int order = sm.order < 1 ? 1 : sm.order;
+        const double theta = 0.5 * (lv.lmax + lv.lmin), delta = 0.5 * (lv.lmax - lv.lmin);
+        SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.theta = theta;
+        a.x_out = x.alt;
+        const bool more = order > 1;
+        a.r_out = more ? lv.r : nullptr;
+        a.dv_out = more ? lv.dva : nullptr;
+        double eb = 3 * V(n) + 8.0 * n + (more ? 2 * V(n) : 0);
+        if (!more && dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); }
+        spmm(OP_CHEB_FIRST, lv.A, a, eb);
+        x.swap();
+        if (more)
+            cheb_steps(lv, b, order, 1, 1.0 / (theta / delta), lv.r, x.cur, lv.dva, lv.dvb, x,
+                       dot_epi);
     }
 
-    void post_smooth(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x) {
+    // Pre-smoother on a ZERO x whose seed is already in place (level_seed).
+    void smooth_zero_seeded(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x,
+                            int dot_epi) {
+        const int64_t n = lv.A.nrows;
         if (sm.kind == MRS_SMOOTH_JACOBI) {
-            if (sm.weight == 0.0) return;
-            int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
-            for (int k = 0; k < sweeps; ++k) jacobi_sweep(lv, b, sm.weight, x);
-        } else {
-            chebyshev(lv, b, sm.order, false, x);
+            const int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
+            if (sm.weight != 0.0)
+                for (int k = 1; k < sweeps; ++k)
+                    jacobi_sweep(lv, b, sm.weight, x, k == sweeps - 1 ? dot_epi : -1);
+            if ((sweeps == 1 || sm.weight == 0.0) && dot_epi >= 0) dot(b, x.cur, n, dot_epi);
+            return;
         }
+        const int order = sm.order < 1 ? 1 : sm.order;
+        if (order == 1) {                    // x = dv0 = b/(d*theta)
+            if (dot_epi >= 0) dot(b, x.cur, n, dot_epi);
+            return;
+        }
+        const double theta = 0.5 * (lv.lmax + lv.lmin), delta = 0.5 * (lv.lmax - lv.lmin);
+        // after the first step: x = dv0 (in lv.dva), r = b
+        cheb_steps(lv, b, order, 1, 1.0 / (theta / delta), b, lv.dva, lv.dva, lv.dvb, x, dot_epi);
     }
 
-    // pre-smooth on a NONZERO x then residual (second and later V-cycles)
-    void pre_smooth_nonzero_and_residual(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x) {
-        post_smooth(lv, b, sm, x);
-        residual(lv, b, x.cur);
-    }
-
-    // V-cycle on level l with rhs b; x given by buffers; zero = certified zero x.
-    void vcycle(int l, const double* b, bool zero, XB& x) {
+    // V-cycle on level l (solvers.py:651-664).  zero: x certified zero and its
+    // seed already written by the producer of b (seeded) or by a seed kernel.
+    void vcycle(int l, const double* b, bool zero, bool seeded, XB& x, int dot_epi) {
         mrs_plan& p = *P;
         LevelDev& lv = p.L[l];
-        const int nl = (int)p.L.size();
-        if (l == nl - 1) {
-            // coarsest: x = A_c^{-1} b (solvers.py:644-649); x overwritten
+        if (coarsest(p, l)) {
+            // x = A_c^{-1} b (replaces the LU solve, solvers.py:644-649)
             int64_t m = p.m, nc = p.nc;
             const double* inv = p.inv;
             double* xo = x.cur;
@@ -267,54 +296,73 @@ struct Builder {
             out->push_back([=](cudaStream_t s) { return launch_coarse(inv, nc, b, xo, m, g, s); });
             bytes += (double)nc * nc * 8.0 + 2 * V(nc);
             kernels++;
+            if (dot_epi >= 0) dot(b, x.cur, nc, dot_epi);
             return;
         }
-        if (zero) pre_smooth_zero_and_residual(lv, b, p.desc.pre, x);
-        else pre_smooth_nonzero_and_residual(lv, b, p.desc.pre, x);
-        LevelDev& lc = p.L[l + 1];
-        // rc = R r  (ASSIGN, solvers.py:660)
-        spmv(lv.R, lv.r, lc.b, MRS_MODE_ASSIGN);
-        XB xc{lc.xa, lc.xb};
-        vcycle(l + 1, lc.b, true, xc);
-        // x += P xc  (ADD, solvers.py:663)
-        spmv(lv.P, xc.cur, x.cur, MRS_MODE_ADD);
-        post_smooth(lv, b, p.desc.post, x);
-    }
-
-    // Preconditioner application z = M r; returns the buffer holding z.
-    // `dst`/`spare`: level-0 output buffers.
-    double* precond(const double* r, double* dst, double* spare) {
-        mrs_plan& p = *P;
-        const mrs_plan_desc& d = p.desc;
-        if (d.precond == MRS_PC_NONE) return const_cast<double*>(r);
-        XB x{dst, spare};
-        if (d.precond == MRS_PC_JACOBI) {
-            LevelDev& lv = p.L[0];
-            int64_t n = lv.A.nrows;
-            VArgs a = v0(); a.n = n; a.x = r; a.y = x.cur; a.d = lv.d; a.wt = d.pc_weight;
-            vec(V_JAC_ZERO, a, 2 * V(n) + 8.0 * n);
-            for (int k = 1; k < d.pc_sweeps; ++k) jacobi_sweep(lv, r, d.pc_weight, x);
-            return x.cur;
+        const mrs_smoother& pre = p.desc.pre;
+        if (zero) {
+            if (!seeded) seed_kernel(b, lv.A.nrows, level_seed(l, x));
+            smooth_zero_seeded(lv, b, pre, x, -1);
+        } else {
+            smooth_nonzero(lv, b, pre, x, -1);
         }
-        int cycles = d.mg_cycles < 1 ? 1 : d.mg_cycles;
-        for (int c = 0; c < cycles; ++c) vcycle(0, r, c == 0, x);
-        return x.cur;
+        LevelDev& lc = p.L[l + 1];
+        spmv(lv.A, x.cur, lv.r, MRS_MODE_RSUB, b);                    // r = b - A x
+        XB xc{lc.xa, lc.xb};
+        spmv(lv.R, lv.r, lc.b, MRS_MODE_ASSIGN, nullptr, -1, nullptr,
+             level_seed(l + 1, xc));                                  // rc = R r (+ seed)
+        vcycle(l + 1, lc.b, true, true, xc, -1);
+        spmv(lv.P, xc.cur, x.cur, MRS_MODE_ADD);                      // x += P xc
+        smooth_nonzero(lv, b, p.desc.post, x, dot_epi);
     }
 };
 
-// Dry-run the preconditioner to learn which of (dst, spare) ends up holding z,
-// then order the buffers so z lands in `want`.
-double* precond_into(mrs_plan* P, const int* guard, const double* r, double* want, double* spare,
-                     std::vector<Launch>& out, double& bytes, int& kernels) {
-    std::vector<Launch> dry;
-    Builder b0{P, &dry, guard};
-    double* got = b0.precond(r, want, spare);
-    if (got != want && got == spare) std::swap(want, spare);
-    Builder b{P, &out, guard};
-    double* res = b.precond(r, want, spare);
-    bytes += b.bytes;
-    kernels += b.kernels;
-    return res;
+// A planned preconditioner application z = M r at level 0.
+struct PCPlan {
+    std::vector<Launch> ops;
+    double* out = nullptr;     // buffer holding z
+    Seed seed;                 // level-0 seed the producer of r must write
+    double bytes = 0;
+    int kernels = 0;
+};
+
+// Build z = M r into `want` (buffers want/spare).  producer_seeds: the kernel
+// producing r also writes the level-0 seed (plan.seed); otherwise a seed
+// kernel is emitted.  dot_epi >= 0: the last kernel also reduces (r, z).
+PCPlan plan_precond(mrs_plan* P, const int* guard, const double* r, double* want,
+                    double* spare, bool producer_seeds, int dot_epi) {
+    const mrs_plan_desc& d = P->desc;
+    auto build = [&](double* a, double* b, PCPlan& pc) {
+        Builder bd{P, &pc.ops, guard};
+        XB x{a, b};
+        if (d.precond == MRS_PC_NONE) {
+            pc.out = const_cast<double*>(r);
+            if (dot_epi >= 0) bd.dot(r, r, P->n, dot_epi);
+        } else if (d.precond == MRS_PC_JACOBI) {
+            LevelDev& lv = P->L[0];
+            pc.seed = bd.level_seed(0, x);
+            if (!producer_seeds) bd.seed_kernel(r, P->n, pc.seed);
+            mrs_smoother sm{MRS_SMOOTH_JACOBI, d.pc_sweeps, d.pc_weight, 0};
+            bd.smooth_zero_seeded(lv, r, sm, x, dot_epi);
+            pc.out = x.cur;
+        } else {
+            const int cycles = d.mg_cycles < 1 ? 1 : d.mg_cycles;
+            pc.seed = bd.level_seed(0, x);
+            for (int c = 0; c < cycles; ++c)
+                bd.vcycle(0, r, c == 0, c == 0 && producer_seeds, x,
+                          c == cycles - 1 ? dot_epi : -1);
+            pc.out = x.cur;
+        }
+        if (!producer_seeds) pc.seed = Seed();
+        pc.bytes = bd.bytes;
+        pc.kernels = bd.kernels;
+    };
+    PCPlan dry;
+    build(want, spare, dry);
+    if (dry.out == spare) std::swap(want, spare);
+    PCPlan pc;
+    build(want, spare, pc);
+    return pc;
 }
 
 // ---------------------------------------------------------------------------
@@ -327,47 +375,54 @@ struct Program {
     int body_kernels = 0;
 };
 
+void append(std::vector<Launch>& dst, std::vector<Launch>& src) {
+    dst.insert(dst.end(), src.begin(), src.end());
+}
+
 void build_cg(mrs_plan* P, bool x_zero, Program& pg) {
     const int64_t n = P->n;
     const int* skip = &P->st->skip;
     const DevCsr& A = P->L[0].A;
     const mrs_plan_desc& d = P->desc;
+    const bool pc_on = d.precond != MRS_PC_NONE;
     // prologue (solvers.py:156-168)
     {
         Builder b{P, &pg.pro, nullptr};
         b.dot(P->B, P->B, n, EPI_BSCALE);
-        if (x_zero) b.copy(P->B, P->r, n);
-        else b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        PCPlan pc = plan_precond(P, nullptr, P->r, P->z, P->zt, pc_on, EPI_RHO);
+        if (x_zero) b.copy(P->B, P->r, n, pc.seed);
+        else b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B, -1, nullptr, pc.seed);
         b.dot(P->r, P->r, n, EPI_RNORM_INIT);
-        double e = 0; int k = 0;
-        double* z = precond_into(P, nullptr, P->r, P->z, P->zt, pg.pro, e, k);
-        b.dot(P->r, z, n, EPI_RHO);
-        b.copy(z, P->p, n);
+        append(pg.pro, pc.ops);
+        b.copy(pc.out, P->p, n);
     }
     // body (solvers.py:171-186)
     {
         Builder b{P, &pg.body, skip};
-        b.spmv(A, P->p, P->q, MRS_MODE_ASSIGN, nullptr, EPI_CG_ALPHA);   // q = A p ; p.q -> alpha
+        b.spmv(A, P->p, P->q, MRS_MODE_ASSIGN, nullptr, EPI_CG_ALPHA);   // q = A p ; alpha
         const bool jac1 = d.precond == MRS_PC_JACOBI && d.pc_sweeps <= 1;
+        double* z;
         if (jac1) {
             // X += a p ; r -= a q ; z = w r/d ; (r.r, r.z) -> rnorm, beta
             VArgs a = Builder::v0(); a.n = n; a.y = P->X; a.x = P->p; a.y2 = P->r; a.u = P->q;
             a.a = P->st->alpha; a.b = P->st->neg_alpha; a.y3 = P->z; a.d = P->L[0].d;
             a.wt = d.pc_weight; a.red = b.red(EPI_CG_RNORM_BETA);
             b.vec(V_CG_UPDATE_JAC, a, 6 * b.V(n) + 8.0 * n);
-            VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = P->z; pu.b = P->st->beta;
-            b.vec(V_P_UPDATE, pu, 3 * b.V(n));
+            z = P->z;
         } else {
+            PCPlan pc = plan_precond(P, skip, P->r, P->z, P->zt, pc_on,
+                                     pc_on ? EPI_CG_BETA : -1);
             VArgs a = Builder::v0(); a.n = n; a.y = P->X; a.x = P->p; a.y2 = P->r; a.u = P->q;
-            a.a = P->st->alpha; a.b = P->st->neg_alpha; a.red = b.red(EPI_CG_RNORM);
-            b.vec(V_CG_UPDATE, a, 5 * b.V(n));
-            double e = 0; int k = 0;
-            double* z = precond_into(P, skip, P->r, P->z, P->zt, pg.body, e, k);
-            b.bytes += e; b.kernels += k;
-            b.dot(P->r, z, n, EPI_CG_BETA);
-            VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = z; pu.b = P->st->beta;
-            b.vec(V_P_UPDATE, pu, 3 * b.V(n));
+            a.a = P->st->alpha; a.b = P->st->neg_alpha;
+            a.red = b.red(pc_on ? EPI_CG_RNORM : EPI_CG_RNORM_BETA1);
+            Builder::set_seed(a, pc.seed);
+            b.vec(V_CG_UPDATE, a, 5 * b.V(n) + b.seed_bytes(pc.seed, n));
+            append(pg.body, pc.ops);
+            b.bytes += pc.bytes; b.kernels += pc.kernels;
+            z = pc.out;
         }
+        VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = z; pu.b = P->st->beta;
+        b.vec(V_P_UPDATE, pu, 3 * b.V(n));
         pg.body_bytes = b.bytes;
         pg.body_kernels = b.kernels;
     }
@@ -383,8 +438,10 @@ void build_bicgstab(mrs_plan* P, bool x_zero, Program& pg) {
     const int64_t n = P->n;
     const int* skip = &P->st->skip;
     const DevCsr& A = P->L[0].A;
-    const bool pc = P->desc.precond != MRS_PC_NONE;
-    // prologue (solvers.py:220-243, first-iteration rho and p)
+    const bool pc_on = P->desc.precond != MRS_PC_NONE;
+    PCPlan pph = plan_precond(P, skip, P->p, P->ph, P->zt, pc_on, -1);
+    PCPlan psh = plan_precond(P, skip, P->s, P->sh, P->zt, pc_on, -1);
+    // prologue (solvers.py:220-243 and the first-iteration rho, p = r)
     {
         Builder b{P, &pg.pro, nullptr};
         b.dot(P->B, P->B, n, EPI_BSCALE);
@@ -393,39 +450,34 @@ void build_bicgstab(mrs_plan* P, bool x_zero, Program& pg) {
         b.copy(P->r, P->r0, n);
         b.dot(P->r, P->r, n, EPI_RNORM_INIT);
         b.dot(P->r0, P->r, n, EPI_RHO);
-        b.copy(P->r, P->p, n);
+        b.copy(P->r, P->p, n, pph.seed);       // p = r, and the seed for ph = M p
     }
     {
         Builder b{P, &pg.body, skip};
-        // p = r + beta (p - omega v)  -- skipped in the first iteration (it == 0)
+        // p = r + beta (p - omega v)  -- not in the first iteration (it == 0)
         VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = P->r; pu.v = P->v;
         pu.b = P->st->beta; pu.c = P->st->neg_omega; pu.guard_it = &P->st->it;
-        b.vec(V_BICG_P, pu, 4 * b.V(n));
-        double* ph = P->p;
-        if (pc) {
-            double e = 0; int k = 0;
-            ph = precond_into(P, skip, P->p, P->ph, P->zt, pg.body, e, k);
-            b.bytes += e; b.kernels += k;
-        }
-        b.spmv(A, ph, P->v, MRS_MODE_ASSIGN);                      // v = A ph
-        b.dot(P->r0, P->v, n, EPI_BICG_ALPHA);                     // alpha = rho / (r0, v)
+        Builder::set_seed(pu, pph.seed);
+        b.vec(V_BICG_P, pu, 4 * b.V(n) + b.seed_bytes(pph.seed, n));
+        const double* ph = pc_on ? pph.out : P->p;
+        append(pg.body, pph.ops);
+        b.bytes += pph.bytes; b.kernels += pph.kernels;
+        b.spmv(A, ph, P->v, MRS_MODE_ASSIGN, nullptr, EPI_BICG_ALPHA, P->r0);  // v = A ph; (r0, v)
         VArgs sa = Builder::v0(); sa.n = n; sa.y = P->s; sa.x = P->r; sa.v = P->v;
         sa.a = P->st->neg_alpha;
-        b.vec(V_BICG_S, sa, 3 * b.V(n));                           // s = r - alpha v
-        double* sh = P->s;
-        if (pc) {
-            double e = 0; int k = 0;
-            sh = precond_into(P, skip, P->s, P->sh, P->zt, pg.body, e, k);
-            b.bytes += e; b.kernels += k;
-        }
-        b.spmv(A, sh, P->t, MRS_MODE_ASSIGN);                      // t = A sh
+        Builder::set_seed(sa, psh.seed);
+        b.vec(V_BICG_S, sa, 3 * b.V(n) + b.seed_bytes(psh.seed, n));      // s = r - alpha v
+        const double* sh = pc_on ? psh.out : P->s;
+        append(pg.body, psh.ops);
+        b.bytes += psh.bytes; b.kernels += psh.kernels;
+        b.spmv(A, sh, P->t, MRS_MODE_ASSIGN);                              // t = A sh
         VArgs d3 = Builder::v0(); d3.n = n; d3.x = P->t; d3.s = P->s; d3.red = b.red(EPI_BICG_OMEGA);
-        b.vec(V_DOT3, d3, 2 * b.V(n));                             // (t,s),(t,t),(s,s) -> omega
+        b.vec(V_DOT3, d3, 2 * b.V(n));                                     // omega
         VArgs xr = Builder::v0(); xr.n = n; xr.y = P->X; xr.u = ph; xr.v = sh; xr.s = P->s;
         xr.w = P->t; xr.y2 = P->r; xr.z = P->r0;
         xr.a = P->st->alpha; xr.b = P->st->omega; xr.c = P->st->neg_omega;
         xr.red = b.red(EPI_BICG_RNORM);
-        b.vec(V_BICG_XR, xr, 8 * b.V(n));                          // X, r, (r0,r), (r,r)
+        b.vec(V_BICG_XR, xr, 8 * b.V(n));                                  // X, r, (r0,r), (r,r)
         pg.body_bytes = b.bytes;
         pg.body_kernels = b.kernels;
     }

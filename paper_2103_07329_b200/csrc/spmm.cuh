@@ -32,14 +32,13 @@ template <int M> struct Lay {
 
 // Kernel operation selector.
 enum SpOp : int {
-    OP_SPMV = 0,         // y op= A x by `mode`                         (csr_spmv)
-    OP_JAC_ZERO_RES,     // x1 = w*(b/d) (zero guess); r = b - A x1     (jacobi_sweep on zero x + residual)
-    OP_JAC_SWEEP,        // x' = x + w*((b - A x)/d)                    (jacobi_sweep)
-    OP_JAC_ZERO2,        // two sweeps from zero: x2 = x1 + w*((b - A x1)/d)
-    OP_CHEB_FIRST,       // r = b - A x; dv = r/(d*theta); x' = x + dv   (chebyshev_apply first step)
+    OP_SPMV = 0,         // y op= A x by `mode` (+ optional next-level seed)   (csr_spmv)
+    OP_JAC_SWEEP,        // x' = x + w*((b - A x)/d)                           (jacobi_sweep)
+    OP_CHEB_FIRST,       // r = b - A x; dv = r/(d*theta); x' = x + dv          (chebyshev first step)
     OP_CHEB_STEP,        // tmp = A dv; r -= tmp; dv' = dv*c1 + c2*(r/d); x += dv'
-    OP_CHEB_STEP_ZERO,   // same with dv = b/(d*theta), r = b, x = dv computed on the fly
 };
+// Zero-guess first steps never gather on-the-fly values: the producer of a
+// level's right-hand side emits the seed (see SpArgs::seed, VArgs::seed).
 
 struct SpArgs {
     const int32_t* rp;
@@ -59,28 +58,26 @@ struct SpArgs {
     double w, theta, c1, c2;
     int mode;
     const int* guard;       // non-null: skip the kernel when *guard != 0
-    int dot;                // OP_SPMV: fuse sum_j x_own * y_out per column
+    int dot;                // fused per-column dot: OP_SPMV x_own.y_out;
+                            // smoother ops b_own.x_new (PCG's (r, z))
+    int seed;               // OP_SPMV (restriction): also emit the next level's
+                            // zero-guess smoother seed from the row result:
+                            // 1: seed_out = w*(y/d)  2: seed_out = y/(d*theta)
+    double* seed_out;
     RedArgs red;
 };
+
+// Zero-guess smoother seed of a right-hand-side value v at a row with
+// diagonal d: Jacobi's first sweep x = 0 + w*(v/d) (blas2.py:181) or
+// Chebyshev's first step dv = v/(d*theta) (solvers.py:551).
+__device__ __forceinline__ double seed_value(int mode, double v, double d, double w_or_theta) {
+    return mode == 1 ? mul(w_or_theta, divd(v, d)) : divd(v, mul(d, w_or_theta));
+}
 
 // Value of the gathered operand at column `col` (CPL columns at cofs).
 template <int OP, int CPL>
 __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t ld, int cofs) {
-    if constexpr (OP == OP_JAC_ZERO_RES || OP == OP_JAC_ZERO2) {
-        Vec<CPL> bb = load_vec<CPL>(a.b + col * ld + cofs);
-        double dd = __ldg(a.d + col);
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) bb.v[i] = mul(a.w, divd(bb.v[i], dd));
-        return bb;
-    } else if constexpr (OP == OP_CHEB_STEP_ZERO) {
-        Vec<CPL> bb = load_vec<CPL>(a.b + col * ld + cofs);
-        double dt = mul(__ldg(a.d + col), a.theta);
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) bb.v[i] = divd(bb.v[i], dt);
-        return bb;
-    } else {
-        return load_vec<CPL>(a.x + col * ld + cofs);
-    }
+    return load_vec<CPL>(a.x + col * ld + cofs);
 }
 
 template <typename Ti>
@@ -160,66 +157,54 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
 #pragma unroll
         for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
         store_vec<CPL>(a.y + o, out);
-        if (a.dot) {
-            Vec<CPL> xo = load_vec<CPL>(a.x + o);
+        if (a.seed) {
+            const double dd = __ldg(a.d + row);
+            const double wt = a.seed == 1 ? a.w : a.theta;
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) out.v[i] = seed_value(a.seed, acc[i], dd, wt);
+            store_vec<CPL>(a.seed_out + o, out);
+        }
+        if (a.dot) {   // (x_in ? x_in : x)_own . y  (x_in: e.g. BiCGStab's r0)
+            Vec<CPL> xo = load_vec<CPL>((a.x_in ? a.x_in : a.x) + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
         }
-    } else if constexpr (OP == OP_JAC_ZERO_RES || OP == OP_JAC_SWEEP || OP == OP_JAC_ZERO2 ||
-                         OP == OP_CHEB_FIRST) {
+    } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
         // r = b - A x  (RSUB order: start at b, subtract in entry order)
         Vec<CPL> bb = load_vec<CPL>(a.b + o);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
         row_accumulate<OP, CPL, Tv, Ti, true>(a, lo, hi, ld, cofs, acc);
         const double dd = __ldg(a.d + row);
-        Vec<CPL> xo;
-        if constexpr (OP == OP_JAC_ZERO_RES || OP == OP_JAC_ZERO2) {
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) xo.v[i] = mul(a.w, divd(bb.v[i], dd));
-        } else {
-            xo = load_vec<CPL>(a.x + o);
-        }
-        Vec<CPL> out;
-        if constexpr (OP == OP_JAC_ZERO_RES) {
-            store_vec<CPL>(a.x_out + o, xo);
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
-            store_vec<CPL>(a.r_out + o, out);
-        } else if constexpr (OP == OP_CHEB_FIRST) {
+        Vec<CPL> xo = load_vec<CPL>(a.x + o);
+        if constexpr (OP == OP_CHEB_FIRST) {
             const double dt = mul(dd, a.theta);
-            Vec<CPL> dv;
+            Vec<CPL> r, dv;
 #pragma unroll
             for (int i = 0; i < CPL; ++i) {
-                out.v[i] = acc[i];
-                dv.v[i] = divd(acc[i], dt);
-                xo.v[i] = add(xo.v[i], dv.v[i]);
+                r.v[i] = acc[i];
+                dv.v[i] = divd(acc[i], dt);                 // dv = r / (d*theta)
+                xo.v[i] = add(xo.v[i], dv.v[i]);            // x + dv
             }
-            store_vec<CPL>(a.r_out + o, out);
-            store_vec<CPL>(a.dv_out + o, dv);
-            store_vec<CPL>(a.x_out + o, xo);
+            if (a.r_out) store_vec<CPL>(a.r_out + o, r);
+            if (a.dv_out) store_vec<CPL>(a.dv_out + o, dv);
         } else {
-            // x + w * (r / d)   (blas2.py:181)
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) out.v[i] = add(xo.v[i], mul(a.w, divd(acc[i], dd)));
-            store_vec<CPL>(a.x_out + o, out);
+            for (int i = 0; i < CPL; ++i) xo.v[i] = add(xo.v[i], mul(a.w, divd(acc[i], dd)));  // blas2.py:181
         }
-    } else {  // OP_CHEB_STEP / OP_CHEB_STEP_ZERO  (solvers.py:559-571)
+        store_vec<CPL>(a.x_out + o, xo);
+        if (a.dot) {
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+        }
+    } else {  // OP_CHEB_STEP  (solvers.py:559-571)
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
         row_accumulate<OP, CPL, Tv, Ti, false>(a, lo, hi, ld, cofs, acc);   // tmp = A dv
         const double dd = __ldg(a.d + row);
-        Vec<CPL> r, dv, xo;
-        if constexpr (OP == OP_CHEB_STEP_ZERO) {
-            r = load_vec<CPL>(a.b + o);
-            const double dt = mul(dd, a.theta);
-#pragma unroll
-            for (int i = 0; i < CPL; ++i) { dv.v[i] = divd(r.v[i], dt); xo.v[i] = dv.v[i]; }
-        } else {
-            r = load_vec<CPL>(a.r_in + o);
-            dv = load_vec<CPL>(a.x + o);
-            xo = load_vec_rw<CPL>(a.x_in + o);
-        }
+        Vec<CPL> r = load_vec<CPL>(a.r_in + o);
+        Vec<CPL> dv = load_vec<CPL>(a.x + o);
+        Vec<CPL> xo = load_vec_rw<CPL>(a.x_in + o);
         Vec<CPL> dvn;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
@@ -230,6 +215,11 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
         store_vec<CPL>(a.x_out + o, xo);
         if (a.r_out) store_vec<CPL>(a.r_out + o, r);
         if (a.dv_out) store_vec<CPL>(a.dv_out + o, dvn);
+        if (a.dot) {
+            Vec<CPL> bb = load_vec<CPL>(a.b + o);
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+        }
     }
 }
 
@@ -246,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     for (int64_t row = (int64_t)blockIdx.x * RPB + threadIdx.x / LPR; row < a.nrows;
          row += (int64_t)gridDim.x * RPB)
         do_row<OP, CPL, Tv, Ti>(a, row, M, cofs, dotp);
-    if constexpr (OP == OP_SPMV) {
+    {
         if (a.dot) {
             // warp tree over row groups (lanes with equal column slice), then CTA
             __shared__ double s_w[kThreads / 32][M];
@@ -286,7 +276,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
              row += (int64_t)gridDim.x * rpb)
             do_row<OP, 1, Tv, Ti>(a, row, m, c, dotp);
     }
-    if constexpr (OP == OP_SPMV) {
+    {
         if (a.dot) {
             __shared__ double s_t[kThreads];
             __shared__ double s_blk[kMaxM];

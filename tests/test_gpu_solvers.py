@@ -45,7 +45,7 @@ def test_golden_solves(golden_solves, name, mode):
         err = np.linalg.norm(X.data - Xr, axis=0) / np.linalg.norm(Xr, axis=0)
         assert err.max() < 1e-6, err
         h = np.array(st.residual_history)
-        np.testing.assert_allclose(h, g[f"{name}_hist"], rtol=1e-5, atol=1e-14)
+        np.testing.assert_allclose(h, g[f"{name}_hist"], rtol=1e-5, atol=0.1 * tol)
 
 
 def test_graph_and_eager_agree_bitwise():
