@@ -97,92 +97,139 @@ __device__ __forceinline__ void block_reduce_cols(double (&acc)[K], int m, doubl
     __syncthreads();
 }
 
-// Zero-guess smoother seed of a produced value v at row i (spmm.cuh seed_value).
-__device__ __forceinline__ double seed_of(const VArgs& A, double v, int64_t i) {
-    const double d = __ldg(A.seed_d + i);
+// Zero-guess smoother seed of a produced value v with row diagonal d
+// (spmm.cuh seed_value).
+__device__ __forceinline__ double seed_of(const VArgs& A, double v, double d) {
     return A.seed == 1 ? mul(A.seed_w, divd(v, d)) : divd(v, mul(d, A.seed_w));
 }
 
+// Operands of one element, loaded before any store of the unrolled group so
+// the loads of U rows overlap (outputs may alias inputs element-wise).
+struct Ld { double y, y2, x, u, v, w, z, s, d; };
+
+template <int OP> struct Uses {
+    static constexpr bool y = OP == V_AXPBY || OP == V_ADD2 || OP == V_PAIRED || OP == V_UPDATE_DOT ||
+                              OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_P_UPDATE ||
+                              OP == V_BICG_P || OP == V_BICG_XR;
+    static constexpr bool y2 = OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC;
+    static constexpr bool x = OP == V_AXPBY || OP == V_DOT || OP == V_UPDATE_DOT || OP == V_COPY ||
+                              OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_P_UPDATE ||
+                              OP == V_SEED || OP == V_BICG_P || OP == V_BICG_S || OP == V_DOT3 ||
+                              OP == V_DOT2;
+    static constexpr bool u = OP == V_ADD2 || OP == V_PAIRED || OP == V_UPDATE_DOT2 ||
+                              OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_BICG_XR ||
+                              OP == V_DOT2;
+    static constexpr bool v = OP == V_ADD2 || OP == V_BICG_P || OP == V_BICG_S || OP == V_BICG_XR ||
+                              OP == V_DOT2;
+    static constexpr bool w = OP == V_PAIRED || OP == V_UPDATE_DOT2 || OP == V_BICG_XR;
+    static constexpr bool z = OP == V_DOT || OP == V_UPDATE_DOT2 || OP == V_BICG_XR || OP == V_DOT2;
+    static constexpr bool s = OP == V_PAIRED || OP == V_DOT3 || OP == V_BICG_XR;
+    static constexpr bool d = OP == V_CG_UPDATE_JAC || OP == V_SEED;   // + any seeding op
+};
+
 template <int OP>
-__device__ __forceinline__ void vec_elem(const VArgs& A, int64_t i, int64_t e, int c,
-                                         double sa, double sb, double sc,
-                                         double (&acc)[VK<OP>::K > 0 ? VK<OP>::K : 1]) {
-    if constexpr (OP == V_AXPBY) {
-        A.y[e] = add(mul(sb, A.y[e]), mul(sa, __ldg(A.x + e)));
-    } else if constexpr (OP == V_ADD2) {
-        A.y[e] = add(add(A.y[e], mul(sa, __ldg(A.u + e))), mul(sb, __ldg(A.v + e)));
-    } else if constexpr (OP == V_PAIRED) {
-        double sv = __ldg(A.s + e);
-        A.y[e] = add(add(A.y[e], mul(sa, __ldg(A.u + e))), mul(sb, sv));
-        A.y2[e] = sub(sv, mul(sc, __ldg(A.w + e)));
-    } else if constexpr (OP == V_DOT) {
-        acc[0] = add(acc[0], mul(__ldg(A.x + e), __ldg(A.z + e)));
-    } else if constexpr (OP == V_UPDATE_DOT) {
-        double t = add(mul(sb, A.y[e]), mul(sa, __ldg(A.x + e)));
-        A.y[e] = t;
-        acc[0] = add(acc[0], mul(t, t));
-    } else if constexpr (OP == V_UPDATE_DOT2) {
-        double t = sub(A.u[e], mul(sc, A.w[e]));   // y may alias u or w: plain loads
-        A.y[e] = t;
-        acc[0] = add(acc[0], mul(__ldg(A.z + e), t));
-        acc[1] = add(acc[1], mul(t, t));
-    } else if constexpr (OP == V_COPY) {
-        const double v = __ldg(A.x + e);
-        A.y[e] = v;
-        if (A.seed) A.seed_out[e] = seed_of(A, v, i);
-    } else if constexpr (OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC) {
-        // X = 1*X + alpha*p ; r = 1*r + (-alpha)*q   (axpby, blas.py:144)
-        A.y[e] = add(A.y[e], mul(sa, __ldg(A.x + e)));
-        double r = add(A.y2[e], mul(sb, __ldg(A.u + e)));
-        A.y2[e] = r;
-        acc[0] = add(acc[0], mul(r, r));
-        if (A.seed) A.seed_out[e] = seed_of(A, r, i);
-        if constexpr (OP == V_CG_UPDATE_JAC) {
-            // z = 0 + w*(r/d) (jacobi_sweep from a zero guess, blas2.py:181)
-            double zz = mul(A.wt, divd(r, __ldg(A.d + i)));
-            A.y3[e] = zz;
-            acc[1] = add(acc[1], mul(r, zz));
-        }
-    } else if constexpr (OP == V_P_UPDATE) {
-        A.y[e] = add(mul(sb, A.y[e]), __ldg(A.x + e));
-    } else if constexpr (OP == V_SEED) {
-        A.y[e] = seed_of(A, __ldg(A.x + e), i);
-    } else if constexpr (OP == V_BICG_P) {
-        // p -= omega v ; p = r + beta p  (two axpby passes fused, same rounding)
-        double t = add(A.y[e], mul(sc, __ldg(A.v + e)));
-        double p = add(mul(sb, t), __ldg(A.x + e));
-        A.y[e] = p;
-        if (A.seed) A.seed_out[e] = seed_of(A, p, i);
-    } else if constexpr (OP == V_BICG_S) {
-        double s = add(__ldg(A.x + e), mul(sa, __ldg(A.v + e)));
-        A.y[e] = s;
-        if (A.seed) A.seed_out[e] = seed_of(A, s, i);
-    } else if constexpr (OP == V_DOT3) {
-        double t = __ldg(A.x + e), s = __ldg(A.s + e);
-        acc[0] = add(acc[0], mul(t, s));
-        acc[1] = add(acc[1], mul(t, t));
-        acc[2] = add(acc[2], mul(s, s));
-    } else if constexpr (OP == V_BICG_XR) {
-        // add2_scaled(X, alpha, ph, omega, sh); r = s ; axpby(-omega, t, 1, r)
-        A.y[e] = add(add(A.y[e], mul(sa, __ldg(A.u + e))), mul(sb, __ldg(A.v + e)));
-        double r = add(__ldg(A.s + e), mul(sc, __ldg(A.w + e)));
-        A.y2[e] = r;
-        acc[0] = add(acc[0], mul(__ldg(A.z + e), r));
-        acc[1] = add(acc[1], mul(r, r));
-    } else if constexpr (OP == V_DOT2) {
-        acc[0] = add(acc[0], mul(__ldg(A.x + e), __ldg(A.z + e)));
-        acc[1] = add(acc[1], mul(__ldg(A.u + e), __ldg(A.v + e)));
-    }
+__device__ __forceinline__ void vec_load(const VArgs& A, int64_t e, int64_t i, Ld& L) {
+    using Us = Uses<OP>;
+    if constexpr (Us::y) L.y = A.y[e];
+    if constexpr (Us::y2) L.y2 = A.y2[e];
+    if constexpr (Us::x) L.x = __ldg(A.x + e);
+    if constexpr (Us::u) L.u = A.u[e];
+    if constexpr (Us::v) L.v = __ldg(A.v + e);
+    if constexpr (Us::w) L.w = A.w[e];
+    if constexpr (Us::z) L.z = __ldg(A.z + e);
+    if constexpr (Us::s) L.s = __ldg(A.s + e);
+    if constexpr (Us::d) L.d = __ldg((OP == V_CG_UPDATE_JAC ? A.d : A.seed_d) + i);
+    else if (A.seed) L.d = __ldg(A.seed_d + i);
 }
 
 template <int OP>
-__global__ void __launch_bounds__(kThreads) vec_kernel(VArgs A) {
+__device__ __forceinline__ void vec_compute(const VArgs& A, int64_t e, const Ld& L,
+                                            double sa, double sb, double sc,
+                                            double (&acc)[VK<OP>::K > 0 ? VK<OP>::K : 1]) {
+    if constexpr (OP == V_AXPBY) {
+        A.y[e] = add(mul(sb, L.y), mul(sa, L.x));
+    } else if constexpr (OP == V_ADD2) {
+        A.y[e] = add(add(L.y, mul(sa, L.u)), mul(sb, L.v));
+    } else if constexpr (OP == V_PAIRED) {
+        A.y[e] = add(add(L.y, mul(sa, L.u)), mul(sb, L.s));
+        A.y2[e] = sub(L.s, mul(sc, L.w));
+    } else if constexpr (OP == V_DOT) {
+        acc[0] = add(acc[0], mul(L.x, L.z));
+    } else if constexpr (OP == V_UPDATE_DOT) {
+        const double t = add(mul(sb, L.y), mul(sa, L.x));
+        A.y[e] = t;
+        acc[0] = add(acc[0], mul(t, t));
+    } else if constexpr (OP == V_UPDATE_DOT2) {
+        const double t = sub(L.u, mul(sc, L.w));
+        A.y[e] = t;
+        acc[0] = add(acc[0], mul(L.z, t));
+        acc[1] = add(acc[1], mul(t, t));
+    } else if constexpr (OP == V_COPY) {
+        A.y[e] = L.x;
+        if (A.seed) A.seed_out[e] = seed_of(A, L.x, L.d);
+    } else if constexpr (OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC) {
+        // X = 1*X + alpha*p ; r = 1*r + (-alpha)*q   (axpby, blas.py:144)
+        A.y[e] = add(L.y, mul(sa, L.x));
+        const double r = add(L.y2, mul(sb, L.u));
+        A.y2[e] = r;
+        acc[0] = add(acc[0], mul(r, r));
+        if constexpr (OP == V_CG_UPDATE_JAC) {
+            // z = 0 + w*(r/d) (jacobi_sweep from a zero guess, blas2.py:181)
+            const double zz = mul(A.wt, divd(r, L.d));
+            A.y3[e] = zz;
+            acc[1] = add(acc[1], mul(r, zz));
+        } else {
+            if (A.seed) A.seed_out[e] = seed_of(A, r, L.d);
+        }
+    } else if constexpr (OP == V_P_UPDATE) {
+        A.y[e] = add(mul(sb, L.y), L.x);
+    } else if constexpr (OP == V_SEED) {
+        A.y[e] = seed_of(A, L.x, L.d);
+    } else if constexpr (OP == V_BICG_P) {
+        // p -= omega v ; p = r + beta p  (two axpby passes fused, same rounding)
+        const double t = add(L.y, mul(sc, L.v));
+        const double p = add(mul(sb, t), L.x);
+        A.y[e] = p;
+        if (A.seed) A.seed_out[e] = seed_of(A, p, L.d);
+    } else if constexpr (OP == V_BICG_S) {
+        const double s = add(L.x, mul(sa, L.v));
+        A.y[e] = s;
+        if (A.seed) A.seed_out[e] = seed_of(A, s, L.d);
+    } else if constexpr (OP == V_DOT3) {
+        acc[0] = add(acc[0], mul(L.x, L.s));
+        acc[1] = add(acc[1], mul(L.x, L.x));
+        acc[2] = add(acc[2], mul(L.s, L.s));
+    } else if constexpr (OP == V_BICG_XR) {
+        // add2_scaled(X, alpha, ph, omega, sh); r = s ; axpby(-omega, t, 1, r)
+        A.y[e] = add(add(L.y, mul(sa, L.u)), mul(sb, L.v));
+        const double r = add(L.s, mul(sc, L.w));
+        A.y2[e] = r;
+        acc[0] = add(acc[0], mul(L.z, r));
+        acc[1] = add(acc[1], mul(r, r));
+    } else if constexpr (OP == V_DOT2) {
+        acc[0] = add(acc[0], mul(L.x, L.z));
+        acc[1] = add(acc[1], mul(L.u, L.v));
+    }
+}
+
+constexpr int kVecUnroll = 4;
+// rows in flight per thread: fewer for the operand-heavy fused updates so
+// they stay spill-free under the 64-register cap (4 CTAs/SM)
+template <int OP> __host__ __device__ constexpr int vec_unroll() {
+    using Us = Uses<OP>;
+    return (Us::y + Us::y2 + Us::x + Us::u + Us::v + Us::w + Us::z + Us::s) >= 4 ? 2 : kVecUnroll;
+}
+
+// CTA b owns the contiguous row range [b*chunk, (b+1)*chunk) (chunk a multiple
+// of RPB*U); thread (rs, c) handles column c of rows rs, rs + RPB, ...
+template <int OP>
+__global__ void __launch_bounds__(kThreads, 4) vec_kernel(VArgs A, int64_t chunk) {
     if (A.guard && *A.guard) return;
     if constexpr (OP == V_BICG_P) {
         if (A.guard_it && *A.guard_it == 0) return;
     }
     constexpr int K = VK<OP>::K;
-    constexpr int U = 4;
+    constexpr int U = vec_unroll<OP>();
     const int m = (int)A.m;
     const int rpb = kThreads / m;
     const int c = threadIdx.x % m;
@@ -190,18 +237,23 @@ __global__ void __launch_bounds__(kThreads) vec_kernel(VArgs A) {
     double acc[K > 0 ? K : 1];
 #pragma unroll
     for (int k = 0; k < (K > 0 ? K : 1); ++k) acc[k] = 0.0;
-    double sa = 0.0, sb = 0.0, sc = 0.0;
     if (rs < rpb) {
-        if (A.a) sa = __ldg(A.a + c);
-        if (A.b) sb = __ldg(A.b + c);
-        if (A.c) sc = __ldg(A.c + c);
-        const int64_t chunk = (int64_t)rpb * U;
-        for (int64_t base = (int64_t)blockIdx.x * chunk; base < A.n;
-             base += (int64_t)gridDim.x * chunk) {
+        const double sa = A.a ? __ldg(A.a + c) : 0.0;
+        const double sb = A.b ? __ldg(A.b + c) : 0.0;
+        const double sc = A.c ? __ldg(A.c + c) : 0.0;
+        const int64_t r0 = (int64_t)blockIdx.x * chunk;
+        const int64_t r1 = min(r0 + chunk, A.n);
+        for (int64_t base = r0; base < r1; base += (int64_t)rpb * U) {
+            Ld L[U];
 #pragma unroll
             for (int j = 0; j < U; ++j) {
-                int64_t i = base + rs + (int64_t)j * rpb;
-                if (i < A.n) vec_elem<OP>(A, i, i * m + c, c, sa, sb, sc, acc);
+                const int64_t i = base + rs + (int64_t)j * rpb;
+                if (i < r1) vec_load<OP>(A, i * m + c, i, L[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < U; ++j) {
+                const int64_t i = base + rs + (int64_t)j * rpb;
+                if (i < r1) vec_compute<OP>(A, i * m + c, L[j], sa, sb, sc, acc);
             }
         }
     }

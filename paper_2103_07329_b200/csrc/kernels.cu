@@ -1,43 +1,68 @@
 // kernels.cu -- template instantiation and dispatch of the SpMM and vector
 // kernel families, and the dense coarse-level solve.
+#include <mutex>
+#include <unordered_map>
+
 #include "dispatch.h"
 
 namespace mrs {
 
 int max_grid() { return num_sms() * kMaxGridPerSM; }
 
-int spmm_grid(int64_t nrows, int64_t m) {
-    int rpb;
-    switch (m) {
-    case 1: rpb = Lay<1>::RPB; break;
-    case 2: rpb = Lay<2>::RPB; break;
-    case 4: rpb = Lay<4>::RPB; break;
-    case 8: rpb = Lay<8>::RPB; break;
-    case 16: rpb = Lay<16>::RPB; break;
-    case 32: rpb = Lay<32>::RPB; break;
-    case 64: rpb = Lay<64>::RPB; break;
-    default: rpb = kThreads / (int)m; break;
-    }
-    return grid_for(nrows, rpb);
+// Resident CTAs per SM of a kernel (cached per function).
+static int blocks_per_sm(const void* fn) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(fn);
+    if (it != cache.end()) return it->second;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, 0) != cudaSuccess || b < 1)
+        b = 1;
+    if (b > kMaxGridPerSM) b = kMaxGridPerSM;
+    cache[fn] = b;
+    return b;
+}
+
+// One wave: min(groups needed, resident CTAs); chunk = rows per CTA, a
+// multiple of `rows_per_pass`.
+static void wave_grid(const void* fn, int64_t nrows, int64_t rows_per_pass, int& grid,
+                      int64_t& chunk) {
+    const int64_t passes = (nrows + rows_per_pass - 1) / rows_per_pass;
+    int64_t g = (int64_t)blocks_per_sm(fn) * num_sms();
+    if (g > passes) g = passes;
+    if (g < 1) g = 1;
+    const int64_t per = (passes + g - 1) / g;
+    chunk = per * rows_per_pass;
+    grid = (int)((passes + per - 1) / per);
+}
+
+int spmm_grid(int64_t nrows, int64_t m) {   // upper bound (scratch sizing)
+    (void)nrows; (void)m;
+    return max_grid();
 }
 
 int vec_grid(int64_t n, int64_t m) {
-    int rpb = kThreads / (int)m;
-    return grid_for(n, rpb * 4);
+    (void)n; (void)m;
+    return max_grid();
 }
 
 template <int OP, typename Tv, typename Ti>
-static cudaError_t spmm_m(const SpArgs& a, int64_t m, cudaStream_t s, bool generic) {
-    int g = spmm_grid(a.nrows, generic ? 3 : m);
+static cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
+    int g;
+    auto go = [&](auto kern, int64_t rpp) {
+        wave_grid((const void*)kern, a.nrows, rpp, g, a.chunk);
+        kern<<<g, kThreads, 0, s>>>(a);
+    };
     switch (generic ? 0 : m) {
-    case 1: spmm_kernel<1, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    case 2: spmm_kernel<2, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    case 4: spmm_kernel<4, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    case 8: spmm_kernel<8, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    case 16: spmm_kernel<16, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    case 32: spmm_kernel<32, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    case 64: spmm_kernel<64, OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
-    default: spmm_kernel_generic<OP, Tv, Ti><<<g, kThreads, 0, s>>>(a); break;
+    case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
+    case 2: go(spmm_kernel<2, OP, Tv, Ti>, Lay<2>::RPB); break;
+    case 4: go(spmm_kernel<4, OP, Tv, Ti>, Lay<4>::RPB); break;
+    case 8: go(spmm_kernel<8, OP, Tv, Ti>, Lay<8>::RPB); break;
+    case 16: go(spmm_kernel<16, OP, Tv, Ti>, Lay<16>::RPB); break;
+    case 32: go(spmm_kernel<32, OP, Tv, Ti>, Lay<32>::RPB); break;
+    case 64: go(spmm_kernel<64, OP, Tv, Ti>, Lay<64>::RPB); break;
+    default: go(spmm_kernel_generic<OP, Tv, Ti>, kThreads / m); break;
     }
     return cudaGetLastError();
 }
@@ -73,8 +98,11 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
 
 template <int OP>
 static cudaError_t vec_op(const VArgs& a, cudaStream_t s) {
-    int g = vec_grid(a.n, a.m);
-    vec_kernel<OP><<<g, kThreads, 0, s>>>(a);
+    int g;
+    int64_t chunk;
+    wave_grid((const void*)vec_kernel<OP>, a.n, (int64_t)(kThreads / a.m) * vec_unroll<OP>(), g,
+              chunk);
+    vec_kernel<OP><<<g, kThreads, 0, s>>>(a, chunk);
     return cudaGetLastError();
 }
 

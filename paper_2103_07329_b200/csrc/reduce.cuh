@@ -244,34 +244,42 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
 static __device__ void finish_reduction(const RedArgs& ra, const double* blk, int Km, int m) {
     __shared__ bool s_last;
     __shared__ double s_out[3 * kMaxM];
+    const int G = gridDim.x;
+    // value-major partials [Km][G]: the last CTA reads each value's G partials
+    // with coalesced warp loads
     for (int i = threadIdx.x; i < Km; i += blockDim.x)
-        ra.partials[(size_t)blockIdx.x * Km + i] = blk[i];
+        ra.partials[(size_t)i * G + blockIdx.x] = blk[i];
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned t = atomicAdd(ra.ticket, 1u);
-        s_last = (t == gridDim.x - 1);
+        s_last = (t == (unsigned)G - 1);
     }
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // fold CTA partials in CTA order; S slices per value for parallelism,
-    // slices combined in slice order: fixed shape -> deterministic.
-    const int S = blockDim.x / Km >= 1 ? blockDim.x / Km : 1;
-    __shared__ double s_sl[kThreads];
-    const int val = threadIdx.x % Km, sl = threadIdx.x / Km;
-    if (sl < S && threadIdx.x < S * Km) {
+    // warp w folds values j = w, w + nw, ...: lane l sums partials
+    // b = l, l + 32, ... (loads batched 8 deep), then a fixed xor tree.
+    // Shape depends only on (Km, G): deterministic.
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int j = warp; j < Km; j += nw) {
+        const double* p = ra.partials + (size_t)j * G;
         double acc = 0.0;
-        for (int b = sl; b < (int)gridDim.x; b += S)
-            acc = add(acc, __ldcg(ra.partials + (size_t)b * Km + val));
-        s_sl[threadIdx.x] = acc;
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < Km; i += blockDim.x) {
-        double acc = s_sl[i];
-        for (int s = 1; s < S; ++s) acc = add(acc, s_sl[s * Km + i]);
-        s_out[i] = acc;
-        ra.out[i] = acc;
+        int b = lane;
+        for (; b + 7 * 32 < G; b += 8 * 32) {
+            double v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) v[u] = __ldcg(p + b + u * 32);
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc = add(acc, v[u]);
+        }
+        for (; b < G; b += 32) acc = add(acc, __ldcg(p + b));
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc = add(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+        if (lane == 0) {
+            s_out[j] = acc;
+            if (ra.out) ra.out[j] = acc;
+        }
     }
     if (threadIdx.x == 0) *ra.ticket = 0u;
     __syncthreads();

@@ -16,8 +16,10 @@
 //   CPL : 1  2  2  2   2   4   8
 //   LPR : 1  1  2  4   8   8   8
 //
-// Grid: persistent, min(rows/RPB, 8 * #SM) CTAs of 256 threads striding over
-// row groups (deterministic reduction shape for the fused dots).
+// Grid: one wave of resident CTAs (occupancy-sized, never more than the rows
+// need); CTA b owns a contiguous range of rows processed in passes of RPB
+// rows, so x rows shared by neighbouring passes are reused from L1, and the
+// reduction shape of the fused dots is fixed (deterministic).
 #pragma once
 
 #include "reduce.cuh"
@@ -64,6 +66,7 @@ struct SpArgs {
                             // zero-guess smoother seed from the row result:
                             // 1: seed_out = w*(y/d)  2: seed_out = y/(d*theta)
     double* seed_out;
+    int64_t chunk;          // rows per CTA (contiguous range, multiple of RPB)
     RedArgs red;
 };
 
@@ -233,9 +236,12 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     double dotp[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
-    for (int64_t row = (int64_t)blockIdx.x * RPB + threadIdx.x / LPR; row < a.nrows;
-         row += (int64_t)gridDim.x * RPB)
-        do_row<OP, CPL, Tv, Ti>(a, row, M, cofs, dotp);
+    {
+        const int64_t r0 = (int64_t)blockIdx.x * a.chunk;
+        const int64_t r1 = min(r0 + a.chunk, a.nrows);
+        for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
+            do_row<OP, CPL, Tv, Ti>(a, row, M, cofs, dotp);
+    }
     {
         if (a.dot) {
             // warp tree over row groups (lanes with equal column slice), then CTA
@@ -272,8 +278,9 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
     const int c = threadIdx.x % m;
     double dotp[1] = {0.0};
     if (threadIdx.x < rpb * m) {
-        for (int64_t row = (int64_t)blockIdx.x * rpb + threadIdx.x / m; row < a.nrows;
-             row += (int64_t)gridDim.x * rpb)
+        const int64_t r0 = (int64_t)blockIdx.x * a.chunk;
+        const int64_t r1 = min(r0 + a.chunk, a.nrows);
+        for (int64_t row = r0 + threadIdx.x / m; row < r1; row += rpb)
             do_row<OP, 1, Tv, Ti>(a, row, m, c, dotp);
     }
     {
