@@ -51,7 +51,17 @@ template <int OP, typename Tv, typename Ti>
 static cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     int g;
     auto go = [&](auto kern, int64_t rpp) {
-        wave_grid((const void*)kern, a.nrows, rpp, g, a.chunk);
+        // chunks of up to ~512 rows (fewer when that would idle SMs), strided
+        // over one wave of CTAs
+        const int64_t cap = (int64_t)blocks_per_sm((const void*)kern) * num_sms();
+        int64_t passes = a.nrows / (rpp * cap);
+        const int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
+        passes = passes < 1 ? 1 : (passes > pmax ? pmax : passes);
+        const int64_t chunk = rpp * passes;
+        const int64_t nchunks = (a.nrows + chunk - 1) / chunk;
+        g = (int)(nchunks < cap ? nchunks : cap);
+        if (g < 1) g = 1;
+        a.chunk = chunk;
         kern<<<g, kThreads, 0, s>>>(a);
     };
     switch (generic ? 0 : m) {

@@ -17,9 +17,11 @@
 //   LPR : 1  1  2  4   8   8   8
 //
 // Grid: one wave of resident CTAs (occupancy-sized, never more than the rows
-// need); CTA b owns a contiguous range of rows processed in passes of RPB
-// rows, so x rows shared by neighbouring passes are reused from L1, and the
-// reduction shape of the fused dots is fixed (deterministic).
+// need) striding over chunks of ~512 consecutive rows.  Inside a chunk the
+// CTA walks passes of RPB rows, so x rows shared by neighbouring passes are
+// reused from L1; across CTAs the active chunks form one narrow band of the
+// matrix, so the gathered x window of a banded matrix stays L2-resident.
+// The reduction shape of the fused dots is fixed by (n, grid): deterministic.
 #pragma once
 
 #include "reduce.cuh"
@@ -236,8 +238,8 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     double dotp[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
-    {
-        const int64_t r0 = (int64_t)blockIdx.x * a.chunk;
+    for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
+         r0 += (int64_t)gridDim.x * a.chunk) {
         const int64_t r1 = min(r0 + a.chunk, a.nrows);
         for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
             do_row<OP, CPL, Tv, Ti>(a, row, M, cofs, dotp);
@@ -278,10 +280,12 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
     const int c = threadIdx.x % m;
     double dotp[1] = {0.0};
     if (threadIdx.x < rpb * m) {
-        const int64_t r0 = (int64_t)blockIdx.x * a.chunk;
-        const int64_t r1 = min(r0 + a.chunk, a.nrows);
-        for (int64_t row = r0 + threadIdx.x / m; row < r1; row += rpb)
-            do_row<OP, 1, Tv, Ti>(a, row, m, c, dotp);
+        for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
+             r0 += (int64_t)gridDim.x * a.chunk) {
+            const int64_t r1 = min(r0 + a.chunk, a.nrows);
+            for (int64_t row = r0 + threadIdx.x / m; row < r1; row += rpb)
+                do_row<OP, 1, Tv, Ti>(a, row, m, c, dotp);
+        }
     }
     {
         if (a.dot) {
