@@ -34,13 +34,33 @@ sys.path.insert(0, ROOT)
 
 METRIC = "AMG-PCG RHS·iterations/sec; blocked SpMM HBM GB/s vs roofline"
 UNIT = "RHS*it/s"
-GRID, M, SEED, TOL = 64, 8, 0, 1e-8
-WORKLOAD = ("C2: 3D Poisson 7-pt 64^3 (n=262144), m=8 seeded uniform[-1,1] RHS, zero guess, "
-            "classical RS AMG V(1,1) weighted-Jacobi (w=0.8) + PCG, fp64, tol 1e-8")
-ROLES = {"solver": {"method": "CG", "rel_tolerance": str(TOL)},
-         "preconditioner": {"method": "MultiGrid"},
-         "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
-         "post_smoother": {"method": "Jacobi", "weight": "0.8"}}
+SEED, TOL = 0, 1e-8
+_JAC = {"method": "Jacobi", "weight": "0.8"}
+_CHEB = {"method": "Chebyshev", "polynomial_order": "2"}
+#: BASELINE.json configs on the reference generator (C4: builder-defined 27-pt)
+CONFIGS = {
+    "c1": dict(grid=32, m=4, workload=(
+        "C1: 3D Poisson 7-pt 32^3 (n=32768), m=4 seeded uniform[-1,1] RHS, zero guess, "
+        "Jacobi-preconditioned CG, fp64, tol 1e-8"),
+        roles={"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+               "preconditioner": {"method": "Jacobi"}}),
+    "c2": dict(grid=64, m=8, workload=(
+        "C2: 3D Poisson 7-pt 64^3 (n=262144), m=8 seeded uniform[-1,1] RHS, zero guess, "
+        "classical RS AMG V(1,1) weighted-Jacobi (w=0.8) + PCG, fp64, tol 1e-8"),
+        roles={"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+               "preconditioner": {"method": "MultiGrid"},
+               "pre_smoother": _JAC, "post_smoother": _JAC}),
+    "c3": dict(grid=128, m=16, workload=(
+        "C3: 3D Poisson 7-pt 128^3 (n=2097152), m=16 seeded uniform[-1,1] RHS, zero guess, "
+        "classical RS AMG V(1,1) Chebyshev-2 + BiCGStab, mixed precision (fp32 hierarchy "
+        "levels >= 1, fp64 vectors), tol 1e-8"),
+        roles={"solver": {"method": "BiCGStab", "rel_tolerance": "1e-8"},
+               "preconditioner": {"method": "MultiGrid", "mg_mixed_precision": "1"},
+               "pre_smoother": _CHEB, "post_smoother": _CHEB}),
+}
+CFG = CONFIGS["c2"]
+GRID, M = CFG["grid"], CFG["m"]
+WORKLOAD, ROLES = CFG["workload"], CFG["roles"]
 REF_SNIPPET = r"""
 import json, sys, time, numpy as np
 import mrsolve
@@ -78,6 +98,8 @@ def parse():
     ap.add_argument("--no-spmm", action="store_true", help="skip the config-5 SpMM sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--quick", action="store_true", help="small SpMM sweep (m=8 only)")
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
+                    help="workload (default c2, the BASELINE metric's configuration)")
     ap.add_argument("--exec", default="graph", choices=["graph", "eager"],
                     help="eager: per-kernel launches (ncu cannot profile kernels inside "
                          "graphs with conditional nodes)")
@@ -249,8 +271,16 @@ def spmm_sweep(torch, K, quick: bool):
     return {"n": A.nrows, "nnz": A.nnz, "gen_s": gen_s, "points": out}
 
 
+def select(name):
+    global CFG, GRID, M, WORKLOAD, ROLES
+    CFG = CONFIGS[name]
+    GRID, M = CFG["grid"], CFG["m"]
+    WORKLOAD, ROLES = CFG["workload"], CFG["roles"]
+
+
 def main():
     args = parse()
+    select(args.config)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -347,7 +377,7 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     kt = e0.elapsed_time(e1) * 1e-3 / reps
-    kbytes = A.nnz * 12 + (n + 1) * 4 + 3 * n * M * 8
+    kbytes = A.nnz * (A.values.itemsize + A.col_idx.itemsize) + (n + 1) * 4 + 3 * n * M * 8
     traffic = None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
@@ -357,7 +387,8 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": kbytes / kt / 1e9, "peak": peak, "unit": "GB/s",
             "frac": kbytes / kt / 1e9 / peak, "traffic": traffic,
-            "kernel": "spmm_kernel<8, OP_SPMV(RSUB), double, uint32> on A0 (C2 fine level)",
+            "kernel": f"spmm_kernel<{M}, OP_SPMV(RSUB), double, uint{8 * A.col_idx.itemsize}> "
+                      f"on the fine-level operator A0 ({args.config})",
             "algorithmic_bytes": kbytes, "us_per_launch": kt * 1e6, "peak_source": peak_src}
 
     sweep = None
@@ -386,7 +417,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: reference 7-pt Poisson generator + default_rng(0).uniform(-1,1) RHS",
             "config": {"workload": WORKLOAD, "n": n, "m": M, "iterations": iters,
-                       "levels": cs.hierarchy.nlevels,
+                       "levels": cs.hierarchy.nlevels if cs.hierarchy is not None else 1,
                        "kernels_per_iteration": plan.kernels_per_iteration,
                        "parallelism": "single GPU" if world == 1 else f"{world} replicas",
                        "l2": "flushed (256 MB write) between timed steps, outside the events",

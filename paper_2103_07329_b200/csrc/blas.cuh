@@ -224,6 +224,7 @@ template <int OP> __host__ __device__ constexpr int vec_unroll() {
 // of RPB*U); thread (rs, c) handles column c of rows rs, rs + RPB, ...
 template <int OP>
 __global__ void __launch_bounds__(kThreads, 4) vec_kernel(VArgs A, int64_t chunk) {
+    pdl_enter();
     if (A.guard && *A.guard) return;
     if constexpr (OP == V_BICG_P) {
         if (A.guard_it && *A.guard_it == 0) return;

@@ -74,6 +74,18 @@ __device__ __forceinline__ void store_vec(double* p, const Vec<CPL>& a) {
     }
 }
 
+// Programmatic dependent launch (PDL): every kernel waits for its stream
+// predecessor's memory before touching it, then lets its own successor start
+// launching.  Both are no-ops when the kernel was launched without the PDL
+// attribute.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Launch with the PDL attribute (see launch_ex in kernels.cu).
+bool pdl_enabled();
+
 inline int num_sms() {
     static int sms = 0;
     if (!sms) {

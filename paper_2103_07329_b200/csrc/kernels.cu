@@ -1,5 +1,6 @@
 // kernels.cu -- template instantiation and dispatch of the SpMM and vector
 // kernel families, and the dense coarse-level solve.
+#include <cstdlib>
 #include <mutex>
 #include <unordered_map>
 
@@ -8,6 +9,31 @@
 namespace mrs {
 
 int max_grid() { return num_sms() * kMaxGridPerSM; }
+
+bool pdl_enabled() {
+    static int on = -1;
+    if (on < 0) {
+        const char* e = getenv("MRS_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+
+// cudaLaunchKernelEx with programmatic stream serialization (PDL).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
 
 // Resident CTAs per SM of a kernel (cached per function).
 static int blocks_per_sm(const void* fn) {
@@ -62,7 +88,7 @@ static cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         g = (int)(nchunks < cap ? nchunks : cap);
         if (g < 1) g = 1;
         a.chunk = chunk;
-        kern<<<g, kThreads, 0, s>>>(a);
+        (void)launch_ex(kern, g, s, a);
     };
     switch (generic ? 0 : m) {
     case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
@@ -112,7 +138,7 @@ static cudaError_t vec_op(const VArgs& a, cudaStream_t s) {
     int64_t chunk;
     wave_grid((const void*)vec_kernel<OP>, a.n, (int64_t)(kThreads / a.m) * vec_unroll<OP>(), g,
               chunk);
-    vec_kernel<OP><<<g, kThreads, 0, s>>>(a, chunk);
+    (void)launch_ex(vec_kernel<OP>, g, s, a, chunk);
     return cudaGetLastError();
 }
 
@@ -147,6 +173,7 @@ __global__ void __launch_bounds__(kThreads) coarse_kernel(const double* __restri
                                                           const double* __restrict__ b,
                                                           double* __restrict__ x, int m,
                                                           const int* guard) {
+    pdl_enter();
     if (guard && *guard) return;
     __shared__ double s_t[kThreads];
     const int kpb = kThreads / m;
@@ -172,7 +199,7 @@ __global__ void __launch_bounds__(kThreads) coarse_kernel(const double* __restri
 cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
                           int64_t m, const int* guard, cudaStream_t s) {
     int g = (int)((nc + kCoarseRows - 1) / kCoarseRows);
-    coarse_kernel<<<g, kThreads, 0, s>>>(inv, nc, b, x, (int)m, guard);
+    (void)launch_ex(coarse_kernel, g, s, inv, nc, b, x, (int)m, guard);
     return cudaGetLastError();
 }
 

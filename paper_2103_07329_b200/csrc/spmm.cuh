@@ -230,6 +230,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
 
 template <int M, int OP, typename Tv, typename Ti>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
+    pdl_enter();
     if (a.guard && *a.guard) return;
     using L = Lay<M>;
     constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
@@ -274,6 +275,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
 // t of a CTA owns column t % m for RPB = 256 / m rows.
 template <int OP, typename Tv, typename Ti>
 __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
+    pdl_enter();
     if (a.guard && *a.guard) return;
     const int m = (int)a.m;
     const int rpb = kThreads / m;
