@@ -42,7 +42,7 @@ CONFIGS = {
     "c1": dict(grid=32, m=4, workload=(
         "C1: 3D Poisson 7-pt 32^3 (n=32768), m=4 seeded uniform[-1,1] RHS, zero guess, "
         "Jacobi-preconditioned CG, fp64, tol 1e-8"),
-        roles={"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+        roles={"solver": {"method": "CG", "rel_tolerance": "1e-8", "max_iters": "1000"},
                "preconditioner": {"method": "Jacobi"}}),
     "c2": dict(grid=64, m=8, workload=(
         "C2: 3D Poisson 7-pt 64^3 (n=262144), m=8 seeded uniform[-1,1] RHS, zero guess, "

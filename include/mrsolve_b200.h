@@ -203,6 +203,9 @@ int  mrs_eig_bounds(const mrs_host_csr* A, int32_t iterations, uint64_t seed_unu
 
 const char* mrs_status_string(int32_t status);
 int  mrs_version(void);
+/* Tuning knobs: "pdl" (0/1) -- programmatic dependent launch of the
+ * solve-path kernels.  Read when a plan captures its graph. */
+int  mrs_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus
 }

@@ -95,6 +95,7 @@ SIGNATURES = {
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "mrs_status_string": (C.c_char_p, [C.c_int32]),
     "mrs_version": (C.c_int, []),
+    "mrs_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
 }
 
 
@@ -115,6 +116,11 @@ def lib():
             f.argtypes = args
         _lib = L
     return _lib
+
+
+def set_option(key: str, value: int):
+    """Tuning knob (see mrs_set_option in include/mrsolve_b200.h)."""
+    check(lib().mrs_set_option(key.encode(), int(value)), f"set_option({key})")
 
 
 def status_string(code: int) -> str:

@@ -76,6 +76,15 @@ extern "C" {
 
 int mrs_version(void) { return 1; }
 
+// Tuning knobs.  "pdl": launch the solve-path kernels with programmatic
+// dependent launch (default 0; env MRS_PDL=1).  Plans capture their graph at
+// the first solve, so set options before preparing.
+int mrs_set_option(const char* key, int64_t value) {
+    if (!key) return MRS_ERR_ARG;
+    if (!strcmp(key, "pdl")) { set_pdl((int)value); return MRS_OK; }
+    return MRS_ERR_ARG;
+}
+
 const char* mrs_status_string(int32_t s) {
     switch (s) {
     case MRS_OK: return "ok";

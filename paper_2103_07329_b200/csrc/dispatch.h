@@ -35,5 +35,6 @@ cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double
 int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);
 int max_grid();
+void set_pdl(int on);
 
 }  // namespace mrs

@@ -10,14 +10,18 @@ namespace mrs {
 
 int max_grid() { return num_sms() * kMaxGridPerSM; }
 
+// Tuning knobs (mrs_set_option): read at launch / capture time.
+static int g_pdl = -1;
+
 bool pdl_enabled() {
-    static int on = -1;
-    if (on < 0) {
+    if (g_pdl < 0) {
         const char* e = getenv("MRS_PDL");
-        on = (e && e[0] == '0') ? 0 : 1;
+        g_pdl = (e && e[0] == '1') ? 1 : 0;
     }
-    return on == 1;
+    return g_pdl == 1;
 }
+
+void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
