@@ -12,6 +12,9 @@ int max_grid() { return num_sms() * kMaxGridPerSM; }
 
 // Tuning knobs (mrs_set_option): read at launch / capture time.
 static int g_pdl = -1;
+static int g_staged = 1;
+
+void set_staged(int on) { g_staged = on ? 1 : 0; }
 
 bool pdl_enabled() {
     if (g_pdl < 0) {
@@ -77,9 +80,69 @@ int vec_grid(int64_t n, int64_t m) {
     return max_grid();
 }
 
+// cudaLaunchKernelEx with dynamic shared memory (staged SpMM).
+template <typename... KArgs, typename... Args>
+static cudaError_t launch_ex_smem(void (*kern)(KArgs...), int grid, size_t smem, cudaStream_t s,
+                                  Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+static int staged_blocks_per_sm(const void* fn, size_t smem) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(fn);
+    if (it != cache.end()) return it->second;
+    cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, smem) != cudaSuccess || b < 1)
+        b = 1;
+    if (b > kMaxGridPerSM) b = kMaxGridPerSM;
+    cache[fn] = b;
+    return b;
+}
+
+template <int M, int OP, typename Tv, typename Ti>
+static void launch_staged(SpArgs a, cudaStream_t s) {
+    auto kern = spmm_staged_kernel<M, OP, Tv, Ti>;
+    constexpr size_t smem = stage_bytes<Tv, Ti>();
+    const int64_t rpp = Lay<M>::RPB;
+    const int64_t cap = (int64_t)staged_blocks_per_sm((const void*)kern, smem) * num_sms();
+    int64_t passes = a.nrows / (rpp * cap);
+    const int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
+    passes = passes < 1 ? 1 : (passes > pmax ? pmax : passes);
+    a.chunk = rpp * passes;
+    const int64_t nchunks = (a.nrows + a.chunk - 1) / a.chunk;
+    int g = (int)(nchunks < cap ? nchunks : cap);
+    if (g < 1) g = 1;
+    (void)launch_ex_smem(kern, g, smem, s, a);
+}
+
 template <int OP, typename Tv, typename Ti>
 static cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     int g;
+    if (g_staged && !generic) {
+        switch (m) {
+        case 1: launch_staged<1, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        case 2: launch_staged<2, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        case 4: launch_staged<4, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        case 8: launch_staged<8, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        case 16: launch_staged<16, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        case 32: launch_staged<32, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        case 64: launch_staged<64, OP, Tv, Ti>(a, s); return cudaGetLastError();
+        default: break;
+        }
+    }
     auto go = [&](auto kern, int64_t rpp) {
         // chunks of up to ~512 rows (fewer when that would idle SMs), strided
         // over one wave of CTAs

@@ -85,22 +85,32 @@ __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t
     return load_vec<CPL>(a.x + col * ld + cofs);
 }
 
-template <typename Ti>
-__device__ __forceinline__ int64_t colat(const void* ci, int64_t k) {
-    return (int64_t)__ldg(reinterpret_cast<const Ti*>(ci) + k);
-}
+// Where a row's (column, value) entries come from: global memory (read-only
+// path) or the CTA's shared-memory stage of its pass (see spmm_staged_kernel).
+template <typename Tv, typename Ti> struct GSrc {
+    const Ti* __restrict__ ci;
+    const Tv* __restrict__ v;
+    __device__ __forceinline__ int64_t col(int64_t k) const { return (int64_t)__ldg(ci + k); }
+    __device__ __forceinline__ double val(int64_t k) const { return widen(__ldg(v + k)); }
+};
+template <typename Tv, typename Ti> struct SSrc {
+    const Ti* ci;          // shared memory; entry k lives at ci[k - ci_off]
+    const Tv* v;
+    int64_t ci_off, v_off;
+    __device__ __forceinline__ int64_t col(int64_t k) const { return (int64_t)ci[k - ci_off]; }
+    __device__ __forceinline__ double val(int64_t k) const { return widen(v[k - v_off]); }
+};
 
-// Accumulate one row: acc op= sum_k v_k * g(col_k), entry order.
-template <int OP, int CPL, typename Tv, typename Ti, bool SUBTRACT>
-__device__ __forceinline__ void row_accumulate(const SpArgs& a, int64_t lo, int64_t hi,
-                                               int64_t ld, int cofs, double (&acc)[CPL]) {
-    const Tv* __restrict__ vals = reinterpret_cast<const Tv*>(a.vals);
+// Accumulate one row: acc op= sum_k v_k * g(col_k), entry order; loads of a
+// group of 4 entries are issued before their (ordered) accumulation.
+template <int OP, int CPL, bool SUBTRACT, class Src>
+__device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int64_t lo,
+                                               int64_t hi, int64_t ld, int cofs,
+                                               double (&acc)[CPL]) {
     int64_t k = lo;
     for (; k + 4 <= hi; k += 4) {
-        int64_t c0 = colat<Ti>(a.ci, k), c1 = colat<Ti>(a.ci, k + 1);
-        int64_t c2 = colat<Ti>(a.ci, k + 2), c3 = colat<Ti>(a.ci, k + 3);
-        double v0 = widen(__ldg(vals + k)), v1 = widen(__ldg(vals + k + 1));
-        double v2 = widen(__ldg(vals + k + 2)), v3 = widen(__ldg(vals + k + 3));
+        const int64_t c0 = src.col(k), c1 = src.col(k + 1), c2 = src.col(k + 2), c3 = src.col(k + 3);
+        const double v0 = src.val(k), v1 = src.val(k + 1), v2 = src.val(k + 2), v3 = src.val(k + 3);
         Vec<CPL> g0 = gather<OP, CPL>(a, c0, ld, cofs);
         Vec<CPL> g1 = gather<OP, CPL>(a, c1, ld, cofs);
         Vec<CPL> g2 = gather<OP, CPL>(a, c2, ld, cofs);
@@ -121,8 +131,8 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, int64_t lo, int6
         }
     }
     for (; k < hi; ++k) {
-        int64_t c0 = colat<Ti>(a.ci, k);
-        double v0 = widen(__ldg(vals + k));
+        const int64_t c0 = src.col(k);
+        const double v0 = src.val(k);
         Vec<CPL> g0 = gather<OP, CPL>(a, c0, ld, cofs);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
@@ -134,10 +144,9 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, int64_t lo, int6
 
 // One (row, column-slice) of work for every op.  `dotp` accumulates the fused
 // dot (OP_SPMV with a.dot: x_own . y).
-template <int OP, int CPL, typename Tv, typename Ti>
-__device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld, int cofs,
-                                       double (&dotp)[CPL]) {
-    const int64_t lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
+template <int OP, int CPL, class Src>
+__device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t row, int64_t lo,
+                                       int64_t hi, int64_t ld, int cofs, double (&dotp)[CPL]) {
     const int64_t o = row * ld + cofs;
     double acc[CPL];
     if constexpr (OP == OP_SPMV) {
@@ -155,9 +164,9 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         }
         if (mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD)
-            row_accumulate<OP, CPL, Tv, Ti, false>(a, lo, hi, ld, cofs, acc);
+            row_accumulate<OP, CPL, false>(a, src, lo, hi, ld, cofs, acc);
         else
-            row_accumulate<OP, CPL, Tv, Ti, true>(a, lo, hi, ld, cofs, acc);
+            row_accumulate<OP, CPL, true>(a, src, lo, hi, ld, cofs, acc);
         Vec<CPL> out;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
@@ -179,7 +188,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
         Vec<CPL> bb = load_vec<CPL>(a.b + o);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
-        row_accumulate<OP, CPL, Tv, Ti, true>(a, lo, hi, ld, cofs, acc);
+        row_accumulate<OP, CPL, true>(a, src, lo, hi, ld, cofs, acc);
         const double dd = __ldg(a.d + row);
         Vec<CPL> xo = load_vec<CPL>(a.x + o);
         if constexpr (OP == OP_CHEB_FIRST) {
@@ -205,7 +214,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-        row_accumulate<OP, CPL, Tv, Ti, false>(a, lo, hi, ld, cofs, acc);   // tmp = A dv
+        row_accumulate<OP, CPL, false>(a, src, lo, hi, ld, cofs, acc);   // tmp = A dv
         const double dd = __ldg(a.d + row);
         Vec<CPL> r = load_vec<CPL>(a.r_in + o);
         Vec<CPL> dv = load_vec<CPL>(a.x + o);
@@ -228,6 +237,32 @@ __device__ __forceinline__ void do_row(const SpArgs& a, int64_t row, int64_t ld,
     }
 }
 
+// CTA-level fixed-shape reduction of the fused-dot partials (warp xor tree
+// over row groups, then warps in order), finished by finish_reduction.
+template <int M>
+__device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[Lay<M>::CPL]) {
+    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR;
+    __shared__ double s_w[kThreads / 32][M];
+    __shared__ double s_blk[M];
+#pragma unroll
+    for (int off = LPR; off < 32; off <<= 1)
+#pragma unroll
+        for (int i = 0; i < CPL; ++i)
+            dotp[i] = add(dotp[i], __shfl_xor_sync(0xffffffffu, dotp[i], off));
+    const int warp = threadIdx.x / 32, wl = threadIdx.x % 32;
+    if (wl < LPR)
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) s_w[warp][wl * CPL + i] = dotp[i];
+    __syncthreads();
+    if (threadIdx.x < M) {
+        double acc = s_w[0][threadIdx.x];
+        for (int w = 1; w < kThreads / 32; ++w) acc = add(acc, s_w[w][threadIdx.x]);
+        s_blk[threadIdx.x] = acc;
+    }
+    __syncthreads();
+    finish_reduction(a.red, s_blk, M, M);
+}
+
 template <int M, int OP, typename Tv, typename Ti>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     pdl_enter();
@@ -236,6 +271,7 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
     const int lane = threadIdx.x % LPR;
     const int cofs = lane * CPL;
+    const GSrc<Tv, Ti> src{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
     double dotp[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
@@ -243,32 +279,9 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
          r0 += (int64_t)gridDim.x * a.chunk) {
         const int64_t r1 = min(r0 + a.chunk, a.nrows);
         for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
-            do_row<OP, CPL, Tv, Ti>(a, row, M, cofs, dotp);
+            do_row<OP, CPL>(a, src, row, __ldg(a.rp + row), __ldg(a.rp + row + 1), M, cofs, dotp);
     }
-    {
-        if (a.dot) {
-            // warp tree over row groups (lanes with equal column slice), then CTA
-            __shared__ double s_w[kThreads / 32][M];
-            __shared__ double s_blk[M];
-#pragma unroll
-            for (int off = LPR; off < 32; off <<= 1)
-#pragma unroll
-                for (int i = 0; i < CPL; ++i)
-                    dotp[i] = add(dotp[i], __shfl_xor_sync(0xffffffffu, dotp[i], off));
-            const int warp = threadIdx.x / 32, wl = threadIdx.x % 32;
-            if (wl < LPR)
-#pragma unroll
-                for (int i = 0; i < CPL; ++i) s_w[warp][wl * CPL + i] = dotp[i];
-            __syncthreads();
-            if (threadIdx.x < M) {
-                double acc = s_w[0][threadIdx.x];
-                for (int w = 1; w < kThreads / 32; ++w) acc = add(acc, s_w[w][threadIdx.x]);
-                s_blk[threadIdx.x] = acc;
-            }
-            __syncthreads();
-            finish_reduction(a.red, s_blk, M, M);
-        }
-    }
+    if (a.dot) spmm_block_dot<M>(a, dotp);
 }
 
 // Generic m (any value, any layout): one thread per (row, column), thread
@@ -280,13 +293,14 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
     const int m = (int)a.m;
     const int rpb = kThreads / m;
     const int c = threadIdx.x % m;
+    const GSrc<Tv, Ti> src{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
     double dotp[1] = {0.0};
     if (threadIdx.x < rpb * m) {
         for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
              r0 += (int64_t)gridDim.x * a.chunk) {
             const int64_t r1 = min(r0 + a.chunk, a.nrows);
             for (int64_t row = r0 + threadIdx.x / m; row < r1; row += rpb)
-                do_row<OP, 1, Tv, Ti>(a, row, m, c, dotp);
+                do_row<OP, 1>(a, src, row, __ldg(a.rp + row), __ldg(a.rp + row + 1), m, c, dotp);
         }
     }
     {
@@ -304,6 +318,132 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
             finish_reduction(a.red, s_blk, m, m);
         }
     }
+}
+
+
+// ---------------------------------------------------------------------------
+// Staged SpMM: the CSR segment of each pass (RPB rows: row pointers, column
+// indices, values -- one contiguous range) is copied into shared memory with
+// cp.async (16-byte chunks, L2-only), double-buffered so the next pass
+// streams in while this one computes.  Each thread then reads its row's
+// entries from shared memory and only the x gathers remain in its dependent
+// chain.  A pass whose segment exceeds the stage capacity is computed from
+// global memory (same arithmetic).  Bitwise identical to spmm_kernel.
+// ---------------------------------------------------------------------------
+
+constexpr int kStageCap = 2048;      // entries per buffer
+
+template <typename Tv, typename Ti>
+constexpr size_t stage_bytes() {
+    // two buffers of: row pointers (RPB_max+1 ints, padded), indices, values
+    return 2 * (sizeof(int32_t) * (kThreads + 8) + (kStageCap + 16) * (sizeof(Ti) + sizeof(Tv)));
+}
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
+    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N> __device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <typename Tv, typename Ti>
+struct Stage {
+    int32_t* rp;      // [kThreads + 8]
+    Ti* ci;           // [kStageCap + 16]
+    Tv* v;            // [kStageCap + 16]
+    int64_t r0, r1;   // rows of the pass
+    int64_t ci_off, v_off;
+    int ok;           // segment fits the stage
+};
+
+// Issue the copies of pass [r0, r1) into buffer `st` (all threads).
+template <typename Tv, typename Ti>
+__device__ __forceinline__ void stage_issue(const SpArgs& a, Stage<Tv, Ti>& st, int64_t r0,
+                                            int64_t r1) {
+    st.r0 = r0; st.r1 = r1;
+    const int64_t k0 = __ldg(a.rp + r0), k1 = __ldg(a.rp + r1);
+    constexpr int EI = 16 / sizeof(Ti), EV = 16 / sizeof(Tv);
+    const int64_t ki = k0 & ~(int64_t)(EI - 1), kv = k0 & ~(int64_t)(EV - 1);
+    st.ci_off = ki; st.v_off = kv;
+    st.ok = (k1 - ki <= kStageCap) && (k1 - kv <= kStageCap);
+    const int nrp = (int)(r1 - r0 + 1);
+    for (int t = threadIdx.x; t < nrp; t += kThreads) cp_async4(st.rp + t, a.rp + r0 + t);
+    if (st.ok) {
+        const Ti* gci = reinterpret_cast<const Ti*>(a.ci);
+        const Tv* gv = reinterpret_cast<const Tv*>(a.vals);
+        const int nci = (int)((k1 - ki + EI - 1) / EI), nv = (int)((k1 - kv + EV - 1) / EV);
+        for (int t = threadIdx.x; t < nci; t += kThreads) cp_async16(st.ci + t * EI, gci + ki + t * EI);
+        for (int t = threadIdx.x; t < nv; t += kThreads) cp_async16(st.v + t * EV, gv + kv + t * EV);
+    }
+}
+
+template <int M, int OP, typename Tv, typename Ti>
+__global__ void __launch_bounds__(kThreads) spmm_staged_kernel(SpArgs a) {
+    pdl_enter();
+    if (a.guard && *a.guard) return;
+    using L = Lay<M>;
+    constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
+    extern __shared__ __align__(16) unsigned char smem[];
+    Stage<Tv, Ti> st[2];
+    {
+        unsigned char* p = smem;
+        for (int b = 0; b < 2; ++b) {
+            st[b].ci = reinterpret_cast<Ti*>(p); p += (kStageCap + 16) * sizeof(Ti);
+            st[b].v = reinterpret_cast<Tv*>(p); p += (kStageCap + 16) * sizeof(Tv);
+            st[b].rp = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (kThreads + 8);
+        }
+    }
+    const int lane = threadIdx.x % LPR;
+    const int cofs = lane * CPL;
+    const GSrc<Tv, Ti> gsrc{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
+    double dotp[CPL];
+#pragma unroll
+    for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
+    // pass sequence of this CTA: chunks strided over the grid, RPB rows each
+    const int64_t stride = (int64_t)gridDim.x * a.chunk;
+    int64_t c0 = (int64_t)blockIdx.x * a.chunk;   // current chunk start
+    int64_t p0 = c0;                               // current pass start
+    auto next_pass = [&](int64_t& c, int64_t& p) {
+        p += RPB;
+        if (p >= min(c + a.chunk, a.nrows)) { c += stride; p = c; }
+    };
+    if (p0 < a.nrows) {
+    int cur = 0;
+    stage_issue(a, st[0], p0, min(p0 + RPB, min(c0 + a.chunk, a.nrows)));
+    cp_async_commit();
+    int64_t c1 = c0, p1 = p0;
+    next_pass(c1, p1);
+    while (true) {
+        const bool more = p1 < a.nrows;
+        if (more) stage_issue(a, st[cur ^ 1], p1, min(p1 + RPB, min(c1 + a.chunk, a.nrows)));
+        cp_async_commit();
+        cp_async_wait<1>();
+        __syncthreads();
+        const Stage<Tv, Ti>& S = st[cur];
+        const int64_t row = S.r0 + threadIdx.x / LPR;
+        if (row < S.r1) {
+            const int j = (int)(row - S.r0);
+            const int64_t lo = S.rp[j], hi = S.rp[j + 1];
+            if (S.ok) {
+                const SSrc<Tv, Ti> ssrc{S.ci, S.v, S.ci_off, S.v_off};
+                do_row<OP, CPL>(a, ssrc, row, lo, hi, M, cofs, dotp);
+            } else {
+                do_row<OP, CPL>(a, gsrc, row, lo, hi, M, cofs, dotp);
+            }
+        }
+        __syncthreads();           // buffer `cur` is refilled two passes later
+        if (!more) break;
+        cur ^= 1;
+        next_pass(c1, p1);
+    }
+    }
+    if (a.dot) spmm_block_dot<M>(a, dotp);
 }
 
 }  // namespace mrs

@@ -16,7 +16,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--knob", default="pdl")
+    ap.add_argument("--knob", default="spmm_staged")
     ap.add_argument("--values", type=int, nargs="+", default=[0, 1])
     ap.add_argument("--config", default="c2")
     ap.add_argument("--rounds", type=int, default=3)
