@@ -36,6 +36,5 @@ int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);
 int max_grid();
 void set_pdl(int on);
-void set_staged(int on);
 
 }  // namespace mrs

@@ -1,0 +1,102 @@
+// launch.cuh -- launch helpers shared by the kernel translation units
+// (occupancy-sized one-wave grids, PDL launch attribute).
+#pragma once
+
+#include <mutex>
+#include <unordered_map>
+
+#include "dispatch.h"
+
+namespace mrs {
+
+// cudaLaunchKernelEx with programmatic stream serialization (PDL).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+// Resident CTAs per SM of a kernel (cached per function).
+inline int blocks_per_sm(const void* fn) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, int> cache;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(fn);
+    if (it != cache.end()) return it->second;
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, fn, kThreads, 0) != cudaSuccess || b < 1)
+        b = 1;
+    if (b > kMaxGridPerSM) b = kMaxGridPerSM;
+    cache[fn] = b;
+    return b;
+}
+
+// One wave: min(groups needed, resident CTAs); chunk = rows per CTA, a
+// multiple of `rows_per_pass`.
+inline void wave_grid(const void* fn, int64_t nrows, int64_t rows_per_pass, int& grid,
+                      int64_t& chunk) {
+    const int64_t passes = (nrows + rows_per_pass - 1) / rows_per_pass;
+    int64_t g = (int64_t)blocks_per_sm(fn) * num_sms();
+    if (g > passes) g = passes;
+    if (g < 1) g = 1;
+    const int64_t per = (passes + g - 1) / g;
+    chunk = per * rows_per_pass;
+    grid = (int)((passes + per - 1) / per);
+}
+
+
+// SpMM family: chunk-strided one-wave grid (see spmm.cuh).
+template <int OP, typename Tv, typename Ti>
+inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
+    int g;
+    auto go = [&](auto kern, int64_t rpp) {
+        // chunks of up to ~512 rows (fewer when that would idle SMs), strided
+        // over one wave of CTAs
+        const int64_t cap = (int64_t)blocks_per_sm((const void*)kern) * num_sms();
+        int64_t passes = a.nrows / (rpp * cap);
+        const int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
+        passes = passes < 1 ? 1 : (passes > pmax ? pmax : passes);
+        const int64_t chunk = rpp * passes;
+        const int64_t nchunks = (a.nrows + chunk - 1) / chunk;
+        g = (int)(nchunks < cap ? nchunks : cap);
+        if (g < 1) g = 1;
+        a.chunk = chunk;
+        (void)launch_ex(kern, g, s, a);
+    };
+    switch (generic ? 0 : m) {
+    case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
+    case 2: go(spmm_kernel<2, OP, Tv, Ti>, Lay<2>::RPB); break;
+    case 4: go(spmm_kernel<4, OP, Tv, Ti>, Lay<4>::RPB); break;
+    case 8: go(spmm_kernel<8, OP, Tv, Ti>, Lay<8>::RPB); break;
+    case 16: go(spmm_kernel<16, OP, Tv, Ti>, Lay<16>::RPB); break;
+    case 32: go(spmm_kernel<32, OP, Tv, Ti>, Lay<32>::RPB); break;
+    case 64: go(spmm_kernel<64, OP, Tv, Ti>, Lay<64>::RPB); break;
+    default: go(spmm_kernel_generic<OP, Tv, Ti>, kThreads / m); break;
+    }
+    return cudaGetLastError();
+}
+
+template <int OP, typename Tv>
+inline cudaError_t spmm_op(const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s, bool g) {
+    if (A.ib == 4) return spmm_m<OP, Tv, uint32_t>(a, m, s, g);
+    if (A.ib == 2) return spmm_m<OP, Tv, uint16_t>(a, m, s, g);
+    if constexpr (OP == OP_SPMV)
+        if (A.ib == 1) return spmm_m<OP, Tv, uint8_t>(a, m, s, g);
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_spmm_f64(int op, const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s,
+                            bool generic);
+cudaError_t launch_spmm_f32(int op, const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s,
+                            bool generic);
+
+}  // namespace mrs

@@ -86,7 +86,7 @@ __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t
 }
 
 // Where a row's (column, value) entries come from: global memory (read-only
-// path) or the CTA's shared-memory stage of its pass (see spmm_staged_kernel).
+// path) or a shared-memory copy (tail kernel).
 template <typename Tv, typename Ti> struct GSrc {
     const Ti* __restrict__ ci;
     const Tv* __restrict__ v;
@@ -320,130 +320,5 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
     }
 }
 
-
-// ---------------------------------------------------------------------------
-// Staged SpMM: the CSR segment of each pass (RPB rows: row pointers, column
-// indices, values -- one contiguous range) is copied into shared memory with
-// cp.async (16-byte chunks, L2-only), double-buffered so the next pass
-// streams in while this one computes.  Each thread then reads its row's
-// entries from shared memory and only the x gathers remain in its dependent
-// chain.  A pass whose segment exceeds the stage capacity is computed from
-// global memory (same arithmetic).  Bitwise identical to spmm_kernel.
-// ---------------------------------------------------------------------------
-
-constexpr int kStageCap = 2048;      // entries per buffer
-
-template <typename Tv, typename Ti>
-constexpr size_t stage_bytes() {
-    // two buffers of: row pointers (RPB_max+1 ints, padded), indices, values
-    return 2 * (sizeof(int32_t) * (kThreads + 8) + (kStageCap + 16) * (sizeof(Ti) + sizeof(Tv)));
-}
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async4(void* smem, const void* gmem) {
-    const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N> __device__ __forceinline__ void cp_async_wait() {
-    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-template <typename Tv, typename Ti>
-struct Stage {
-    int32_t* rp;      // [kThreads + 8]
-    Ti* ci;           // [kStageCap + 16]
-    Tv* v;            // [kStageCap + 16]
-    int64_t r0, r1;   // rows of the pass
-    int64_t ci_off, v_off;
-    int ok;           // segment fits the stage
-};
-
-// Issue the copies of pass [r0, r1) into buffer `st` (all threads).
-template <typename Tv, typename Ti>
-__device__ __forceinline__ void stage_issue(const SpArgs& a, Stage<Tv, Ti>& st, int64_t r0,
-                                            int64_t r1) {
-    st.r0 = r0; st.r1 = r1;
-    const int64_t k0 = __ldg(a.rp + r0), k1 = __ldg(a.rp + r1);
-    constexpr int EI = 16 / sizeof(Ti), EV = 16 / sizeof(Tv);
-    const int64_t ki = k0 & ~(int64_t)(EI - 1), kv = k0 & ~(int64_t)(EV - 1);
-    st.ci_off = ki; st.v_off = kv;
-    st.ok = (k1 - ki <= kStageCap) && (k1 - kv <= kStageCap);
-    const int nrp = (int)(r1 - r0 + 1);
-    for (int t = threadIdx.x; t < nrp; t += kThreads) cp_async4(st.rp + t, a.rp + r0 + t);
-    if (st.ok) {
-        const Ti* gci = reinterpret_cast<const Ti*>(a.ci);
-        const Tv* gv = reinterpret_cast<const Tv*>(a.vals);
-        const int nci = (int)((k1 - ki + EI - 1) / EI), nv = (int)((k1 - kv + EV - 1) / EV);
-        for (int t = threadIdx.x; t < nci; t += kThreads) cp_async16(st.ci + t * EI, gci + ki + t * EI);
-        for (int t = threadIdx.x; t < nv; t += kThreads) cp_async16(st.v + t * EV, gv + kv + t * EV);
-    }
-}
-
-template <int M, int OP, typename Tv, typename Ti>
-__global__ void __launch_bounds__(kThreads) spmm_staged_kernel(SpArgs a) {
-    pdl_enter();
-    if (a.guard && *a.guard) return;
-    using L = Lay<M>;
-    constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
-    extern __shared__ __align__(16) unsigned char smem[];
-    Stage<Tv, Ti> st[2];
-    {
-        unsigned char* p = smem;
-        for (int b = 0; b < 2; ++b) {
-            st[b].ci = reinterpret_cast<Ti*>(p); p += (kStageCap + 16) * sizeof(Ti);
-            st[b].v = reinterpret_cast<Tv*>(p); p += (kStageCap + 16) * sizeof(Tv);
-            st[b].rp = reinterpret_cast<int32_t*>(p); p += sizeof(int32_t) * (kThreads + 8);
-        }
-    }
-    const int lane = threadIdx.x % LPR;
-    const int cofs = lane * CPL;
-    const GSrc<Tv, Ti> gsrc{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
-    double dotp[CPL];
-#pragma unroll
-    for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
-    // pass sequence of this CTA: chunks strided over the grid, RPB rows each
-    const int64_t stride = (int64_t)gridDim.x * a.chunk;
-    int64_t c0 = (int64_t)blockIdx.x * a.chunk;   // current chunk start
-    int64_t p0 = c0;                               // current pass start
-    auto next_pass = [&](int64_t& c, int64_t& p) {
-        p += RPB;
-        if (p >= min(c + a.chunk, a.nrows)) { c += stride; p = c; }
-    };
-    if (p0 < a.nrows) {
-    int cur = 0;
-    stage_issue(a, st[0], p0, min(p0 + RPB, min(c0 + a.chunk, a.nrows)));
-    cp_async_commit();
-    int64_t c1 = c0, p1 = p0;
-    next_pass(c1, p1);
-    while (true) {
-        const bool more = p1 < a.nrows;
-        if (more) stage_issue(a, st[cur ^ 1], p1, min(p1 + RPB, min(c1 + a.chunk, a.nrows)));
-        cp_async_commit();
-        cp_async_wait<1>();
-        __syncthreads();
-        const Stage<Tv, Ti>& S = st[cur];
-        const int64_t row = S.r0 + threadIdx.x / LPR;
-        if (row < S.r1) {
-            const int j = (int)(row - S.r0);
-            const int64_t lo = S.rp[j], hi = S.rp[j + 1];
-            if (S.ok) {
-                const SSrc<Tv, Ti> ssrc{S.ci, S.v, S.ci_off, S.v_off};
-                do_row<OP, CPL>(a, ssrc, row, lo, hi, M, cofs, dotp);
-            } else {
-                do_row<OP, CPL>(a, gsrc, row, lo, hi, M, cofs, dotp);
-            }
-        }
-        __syncthreads();           // buffer `cur` is refilled two passes later
-        if (!more) break;
-        cur ^= 1;
-        next_pass(c1, p1);
-    }
-    }
-    if (a.dot) spmm_block_dot<M>(a, dotp);
-}
 
 }  // namespace mrs
