@@ -135,7 +135,9 @@ typedef struct {
     mrs_smoother pre, post;
     int32_t nlevels;     /* MultiGrid: hierarchy depth (>= 1) */
     int32_t exec;        /* 0: CUDA graph with device-side while loop (default)
-                            1: eager launches, host checks convergence */
+                            1: eager launches, host checks convergence
+                            2: one captured body graph per iteration, host
+                               checks convergence (automatic fallback of 0) */
     int32_t merged;      /* BiCGStab merged=1 (solvers.py:258-283): ||s|| always
                             replaces rnorm in the omega breakdown test */
 } mrs_plan_desc;
@@ -170,6 +172,29 @@ int  mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
                     double* final_rel, double* history);
 /* Algorithmic HBM bytes of one outer iteration / of the setup residual
  * (the roofline model of SURVEY.md 8(d)). */
+/* ---- multi-GPU: one process per GPU, NCCL over NVLink --
+ * Every level is row-partitioned (local CSR blocks with columns renumbered
+ * [own rows | halo rows by (owner, global id)], so each row keeps its global
+ * entry order) until it is small enough to be agglomerated: its restriction
+ * is computed slice-wise and all-gathered, and the rest of the V-cycle runs
+ * replicated.  Dots: local partials -> ncclAllReduce -> device epilogue. */
+typedef struct mrs_comm mrs_comm;
+int  mrs_comm_unique_id(void* out128);                 /* ncclGetUniqueId */
+int  mrs_comm_create(const void* id128, int32_t rank, int32_t nranks, mrs_comm** out);
+void mrs_comm_destroy(mrs_comm* c);
+int  mrs_plan_set_comm(mrs_plan* p, mrs_comm* c);      /* before set_halo / finalize */
+/* Level layout: replicated (agglomerated) levels hold every row; the first
+ * replicated level after a partitioned one receives its restricted vector as
+ * equal slices [slice_row0, slice_row0 + slice_rows) all-gathered. */
+int  mrs_plan_set_layout(mrs_plan* p, int32_t l, int32_t replicated, int64_t slice_row0,
+                         int64_t slice_rows);
+/* Halo of the gathered operand of A_l (which 0), R_l (1) or P_l (2): the
+ * local rows to send, grouped by destination rank (counts per rank), and the
+ * rows received from each rank (they land after the operand's own rows). */
+int  mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend,
+                       const int32_t* send_idx, const int32_t* send_counts,
+                       const int32_t* recv_counts);
+
 double mrs_plan_iteration_bytes(const mrs_plan* p);
 int  mrs_plan_kernel_count(const mrs_plan* p);   /* kernels per outer iteration */
 int  mrs_plan_fixed_kernel_count(const mrs_plan* p); /* kernels outside the loop */

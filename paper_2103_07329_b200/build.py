@@ -80,7 +80,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 raise RuntimeError(f"compile failed: {os.path.basename(cmd[-3])}")
     objs = [j[-1] for j in jobs]
     tmp = LIB + ".tmp"
-    link = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-lpthread", "-ldl", "-lrt"]
+    link = [nvcc, *ARCH, "-shared", "-o", tmp, *objs, "-cudart", "static", "-lnccl", "-lpthread",
+            "-ldl", "-lrt"]
     r = subprocess.run(link, capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(" ".join(link) + "\n" + r.stdout + r.stderr)

@@ -12,8 +12,11 @@
 
 namespace mrs {
 
+struct Halo;
+
 struct DevCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0;
+    const Halo* halo = nullptr;   // multi-GPU: exchange of the gathered operand before use
     int32_t* rp = nullptr;
     void* ci = nullptr;
     void* v = nullptr;
@@ -36,5 +39,6 @@ int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);
 int max_grid();
 void set_pdl(int on);
+int vec_op_k(int op);   // reduced values per column of a vector op (0 = none)
 
 }  // namespace mrs

@@ -53,6 +53,20 @@ static cudaError_t vec_op(const VArgs& a, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+int vec_op_k(int op) {
+    switch (op) {
+    case V_DOT: return VK<V_DOT>::K;
+    case V_UPDATE_DOT: return VK<V_UPDATE_DOT>::K;
+    case V_UPDATE_DOT2: return VK<V_UPDATE_DOT2>::K;
+    case V_CG_UPDATE: return VK<V_CG_UPDATE>::K;
+    case V_CG_UPDATE_JAC: return VK<V_CG_UPDATE_JAC>::K;
+    case V_DOT3: return VK<V_DOT3>::K;
+    case V_BICG_XR: return VK<V_BICG_XR>::K;
+    case V_DOT2: return VK<V_DOT2>::K;
+    }
+    return 0;
+}
+
 cudaError_t launch_vec(int op, VArgs a, cudaStream_t s) {
     switch (op) {
     case V_AXPBY: return vec_op<V_AXPBY>(a, s);

@@ -15,12 +15,14 @@
 // whose iteration body sits under a conditional WHILE node that the
 // epilogues drive with cudaGraphSetConditional: one graph launch per solve,
 // no host round trip per iteration.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <functional>
 #include <vector>
 
+#include "comm.h"
 #include "dispatch.h"
 
 using namespace mrs;
@@ -30,8 +32,14 @@ namespace {
 using Launch = std::function<cudaError_t(cudaStream_t)>;
 
 struct LevelDev {
-    DevCsr A, P, R;          // P: n_l x n_{l+1}, R: n_{l+1} x n_l
+    DevCsr A, P, R;          // P: n_l x n_{l+1}, R: n_{l+1} x n_l (local blocks when distributed)
     double* d = nullptr;     // diagonal (full precision of stored values)
+    // multi-GPU layout; single GPU: nloc = rows, no halos
+    int64_t nloc = 0;        // rows this rank owns (replicated level: all rows)
+    int64_t vrows = 0;       // allocated rows of level vectors (own + largest halo; gather pad)
+    bool replicated = false; // agglomerated: every rank holds the whole level
+    int64_t slice_row0 = 0, slice_rows = 0;   // agglomeration: my restricted slice, allgather count
+    Halo hA, hR, hP;         // operand exchanges of A_l x, R_l r, P_l x_{l+1}
     double lmin = 0, lmax = 0;
     double* b = nullptr;     // rhs buffer (levels >= 1)
     double* xa = nullptr;
@@ -55,6 +63,8 @@ struct mrs_plan {
     mrs_plan_desc desc{};
     int64_t n = 0, m = 0;
     std::vector<LevelDev> L;
+    mrs_comm* comm = nullptr;  // multi-GPU: NCCL communicator (dist = set)
+    bool dist = false;
     double* inv = nullptr;
     int64_t nc = 0;
     std::vector<void*> owned;
@@ -72,6 +82,11 @@ struct mrs_plan {
     // graphs (index: x_is_zero)
     cudaGraph_t graph[2] = {nullptr, nullptr};
     cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    // exec mode 2: one captured body graph per iteration, host-checked stop
+    cudaGraph_t body_graph[2] = {nullptr, nullptr};
+    cudaGraphExec_t body_exec[2] = {nullptr, nullptr};
+    std::vector<std::function<cudaError_t(cudaStream_t)>> pro_list[2], epi_list[2];
+    int* stop_host = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     int body_kernels = 0;
     int fixed_kernels = 0;
@@ -80,7 +95,10 @@ struct mrs_plan {
         for (int i = 0; i < 2; ++i) {
             if (exec[i]) cudaGraphExecDestroy(exec[i]);
             if (graph[i]) cudaGraphDestroy(graph[i]);
+            if (body_exec[i]) cudaGraphExecDestroy(body_exec[i]);
+            if (body_graph[i]) cudaGraphDestroy(body_graph[i]);
         }
+        if (stop_host) cudaFreeHost(stop_host);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (void* p : owned) cudaFree(p);
@@ -121,17 +139,52 @@ struct Builder {
     static SpArgs sp0() { SpArgs a; memset(&a, 0, sizeof(a)); return a; }
     static VArgs v0() { VArgs a; memset(&a, 0, sizeof(a)); return a; }
 
+    // multi-GPU: exchange the halo rows of a gathered operand before its use
+    void exchange(const Halo* h, const double* x) {
+        if (!P->dist || !h || !h->active()) return;
+        const Halo* hh = h;
+        const mrs_comm* c = P->comm;
+        const int64_t m = P->m;
+        double* xx = const_cast<double*>(x);
+        const int* g = guard;
+        out->push_back([=](cudaStream_t s) { return halo_exchange(*hh, xx, m, c, g, s); });
+    }
+    // multi-GPU: a reduction finishes as local partials (kernel, EPI_NONE) ->
+    // ncclAllReduce -> epilogue kernel.  Returns the epilogue to run in-kernel.
+    int split_reduction(RedArgs& r) {
+        if (!P->dist || r.epi == EPI_NONE) return r.epi;
+        const int epi = r.epi;
+        r.epi = EPI_NONE;
+        return -epi - 1;   // marker: post-kernel allreduce + epilogue needed
+    }
+    void post_reduction(int marker, int Km) {
+        if (marker >= 0) return;
+        const int epi = -marker - 1;
+        double* buf = P->red_out;
+        const mrs_comm* c = P->comm;
+        SolveState* st = P->st;
+        const int m = (int)P->m;
+        const int* g = guard;
+        out->push_back([=](cudaStream_t s) { return allreduce_sum(buf, Km, c, s); });
+        out->push_back([=](cudaStream_t s) { return launch_epilogue(st, buf, Km, m, epi, g, s); });
+    }
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
         int64_t m = P->m;
+        exchange(A.halo, a.x);
+        const int mk = a.dot ? split_reduction(a.red) : 0;
         out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
+        if (a.dot) post_reduction(mk, (int)m);
         bytes += A.bytes() + extra_bytes;
         kernels++;
     }
     void vec(int op, VArgs a, double b) {
         a.guard = a.guard ? a.guard : guard;
         a.m = P->m;
+        const int K = vec_op_k(op);
+        const int mk = K ? split_reduction(a.red) : 0;
         out->push_back([=](cudaStream_t s) { return launch_vec(op, a, s); });
+        if (K) post_reduction(mk, K * (int)P->m);
         bytes += b;
         kernels++;
     }
@@ -309,9 +362,19 @@ struct Builder {
         LevelDev& lc = p.L[l + 1];
         spmv(lv.A, x.cur, lv.r, MRS_MODE_RSUB, b);                    // r = b - A x
         XB xc{lc.xa, lc.xb};
-        spmv(lv.R, lv.r, lc.b, MRS_MODE_ASSIGN, nullptr, -1, nullptr,
-             level_seed(l + 1, xc));                                  // rc = R r (+ seed)
-        vcycle(l + 1, lc.b, true, true, xc, -1);
+        if (p.dist && lc.replicated && !lv.replicated) {
+            // agglomeration: my slice of rc = R r, allgather, replicated below
+            spmv(lv.R, lv.r, lc.b + lc.slice_row0 * p.m, MRS_MODE_ASSIGN);
+            double* buf = lc.b;
+            const int64_t cnt = lc.slice_rows * p.m;
+            const mrs_comm* c = p.comm;
+            out->push_back([=](cudaStream_t s) { return allgather_inplace(buf, cnt, c, s); });
+            vcycle(l + 1, lc.b, true, false, xc, -1);
+        } else {
+            spmv(lv.R, lv.r, lc.b, MRS_MODE_ASSIGN, nullptr, -1, nullptr,
+                 level_seed(l + 1, xc));                              // rc = R r (+ seed)
+            vcycle(l + 1, lc.b, true, true, xc, -1);
+        }
         spmv(lv.P, xc.cur, x.cur, MRS_MODE_ADD);                      // x += P xc
         smooth_nonzero(lv, b, p.desc.post, x, dot_epi);
     }
@@ -671,6 +734,30 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     const int64_t n = p->n, m = p->m;
     auto& o = p->owned;
     if (!p->L[0].A.present() || p->L[0].A.nrows != n) return MRS_ERR_STATE;
+    // layout: rows owned, halo landing offsets, allocated vector rows
+    for (size_t l = 0; l < p->L.size(); ++l) {
+        LevelDev& lv = p->L[l];
+        lv.nloc = lv.A.nrows;
+        lv.hA.recv_row0 = lv.nloc;
+        lv.hR.recv_row0 = lv.nloc;
+    }
+    for (size_t l = 0; l < p->L.size(); ++l) {
+        LevelDev& lv = p->L[l];
+        if (l + 1 < p->L.size()) lv.hP.recv_row0 = p->L[l + 1].nloc;
+        int64_t halo = std::max(lv.hA.nrecv, lv.hR.nrecv);
+        if (l > 0) halo = std::max<int64_t>(halo, p->L[l - 1].hP.nrecv);
+        lv.vrows = lv.nloc + halo;
+        if (lv.replicated && lv.slice_rows && p->comm)
+            lv.vrows = std::max<int64_t>(lv.vrows, (int64_t)p->comm->nranks * lv.slice_rows);
+        for (Halo* h : {&lv.hA, &lv.hR, &lv.hP})
+            if (h->nsend) {
+                h->sendbuf = dalloc<double>((size_t)h->nsend * m, o);
+                if (!h->sendbuf) return MRS_ERR_ALLOC;
+            }
+        lv.A.halo = &lv.hA;
+        lv.R.halo = &lv.hR;
+        lv.P.halo = &lv.hP;
+    }
     if (p->desc.precond == MRS_PC_MG) {
         for (size_t l = 0; l + 1 < p->L.size(); ++l) {
             LevelDev& lv = p->L[l];
@@ -679,7 +766,7 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
         if (!p->inv || p->nc != p->L.back().A.nrows) return MRS_ERR_STATE;
         for (size_t l = 0; l < p->L.size(); ++l) {
             LevelDev& lv = p->L[l];
-            int64_t nl = lv.A.nrows;
+            int64_t nl = lv.vrows;
             if (l > 0) lv.b = dalloc<double>(nl * m, o);
             lv.xa = dalloc<double>(nl * m, o);
             lv.xb = dalloc<double>(nl * m, o);
@@ -696,7 +783,7 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     } else if (p->desc.precond == MRS_PC_JACOBI) {
         if (!p->L[0].d) return MRS_ERR_STATE;
     }
-    size_t V = (size_t)n * m;
+    size_t V = (size_t)p->L[0].vrows * m;   // level-0 Krylov vectors carry the A0 halo
     double** vecs[] = {&p->B, &p->X, &p->r, &p->r0, &p->p, &p->q, &p->v, &p->s,
                        &p->t, &p->ph, &p->sh, &p->z, &p->zt};
     for (double** v : vecs) {
@@ -744,15 +831,48 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
     MRS_CUDA_OK(cudaMemcpyAsync(p->B, B, bytes, in, s));
     if (x_is_zero) MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
     else MRS_CUDA_OK(cudaMemcpyAsync(p->X, X, bytes, in, s));
-    const bool eager = p->desc.exec == 1;
     MRS_CUDA_OK(cudaEventRecord(p->ev0, s));
-    if (!eager) {
-        int gi = x_is_zero ? 1 : 0;
-        if (!p->exec[gi]) {
-            int rc = capture_graph(p, x_is_zero != 0, s);
-            if (rc) return rc;
+    const int gi = x_is_zero ? 1 : 0;
+    if (p->desc.exec == 0 && !p->exec[gi]) {
+        if (capture_graph(p, x_is_zero != 0, s) != MRS_OK) {
+            // e.g. collectives that cannot live inside a conditional body:
+            // fall back to one captured body graph per iteration
+            cudaGetLastError();
+            p->desc.exec = 2;
         }
+    }
+    if (p->desc.exec == 0) {
         MRS_CUDA_OK(cudaGraphLaunch(p->exec[gi], s));
+    } else if (p->desc.exec == 2) {
+        if (!p->body_exec[gi]) {
+            Program pg;
+            if (p->desc.method == MRS_METHOD_CG) build_cg(p, x_is_zero != 0, pg);
+            else build_bicgstab(p, x_is_zero != 0, pg);
+            p->pro_list[gi] = pg.pro;
+            p->epi_list[gi] = pg.epi;
+            cudaStream_t cs;
+            MRS_CUDA_OK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+            MRS_CUDA_OK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+            cudaError_t e = run_list(pg.body, cs);
+            cudaGraph_t g = nullptr;
+            cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+            cudaStreamDestroy(cs);
+            if (e != cudaSuccess || e2 != cudaSuccess) return MRS_ERR_CUDA;
+            MRS_CUDA_OK(cudaGraphInstantiate(&p->body_exec[gi], g, 0));
+            p->body_graph[gi] = g;
+        }
+        if (!p->stop_host) MRS_CUDA_OK(cudaMallocHost(&p->stop_host, sizeof(int)));
+        set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);
+        MRS_CUDA_OK(cudaGetLastError());
+        MRS_CUDA_OK(run_list(p->pro_list[gi], s));
+        for (;;) {
+            MRS_CUDA_OK(cudaMemcpyAsync(p->stop_host, &p->st->stop, sizeof(int),
+                                        cudaMemcpyDeviceToHost, s));
+            MRS_CUDA_OK(cudaStreamSynchronize(s));
+            if (*p->stop_host) break;
+            MRS_CUDA_OK(cudaGraphLaunch(p->body_exec[gi], s));
+        }
+        MRS_CUDA_OK(run_list(p->epi_list[gi], s));
     } else {
         Program pg;
         // eager: no conditional handle; the host polls st->stop per iteration
@@ -790,6 +910,53 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
                                cudaMemcpyDeviceToHost));
     }
     return hs.err == MRS_OK ? MRS_OK : MRS_ERR_BREAKDOWN;
+}
+
+int mrs_plan_set_comm(mrs_plan* p, mrs_comm* c) {
+    if (!p || !c) return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    p->comm = c;
+    p->dist = true;     // also with one rank: exercises the split-reduction path
+    return MRS_OK;
+}
+
+int mrs_plan_set_layout(mrs_plan* p, int32_t l, int32_t replicated, int64_t slice_row0,
+                        int64_t slice_rows) {
+    if (!p || l < 0 || l >= (int)p->L.size()) return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    LevelDev& lv = p->L[l];
+    lv.replicated = replicated != 0;
+    lv.slice_row0 = slice_row0;
+    lv.slice_rows = slice_rows;
+    return MRS_OK;
+}
+
+int mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend, const int32_t* send_idx,
+                      const int32_t* send_counts, const int32_t* recv_counts) {
+    if (!p || !p->comm || l < 0 || l >= (int)p->L.size() || which < 0 || which > 2)
+        return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    LevelDev& lv = p->L[l];
+    Halo& h = which == 0 ? lv.hA : (which == 1 ? lv.hR : lv.hP);
+    const int R = p->comm->nranks;
+    h.scount.assign(send_counts, send_counts + R);
+    h.rcount.assign(recv_counts, recv_counts + R);
+    h.sdisp.assign(R, 0);
+    h.rdisp.assign(R, 0);
+    int64_t ns = 0, nr = 0;
+    for (int q = 0; q < R; ++q) {
+        h.sdisp[q] = (int)ns; ns += h.scount[q];
+        h.rdisp[q] = (int)nr; nr += h.rcount[q];
+    }
+    if (ns != nsend) return MRS_ERR_ARG;
+    h.nsend = (int)ns;
+    h.nrecv = (int)nr;
+    if (ns) {
+        h.send_idx = dalloc<int32_t>((size_t)ns, p->owned);
+        if (!h.send_idx) return MRS_ERR_ALLOC;
+        MRS_CUDA_OK(cudaMemcpy(h.send_idx, send_idx, (size_t)ns * 4, cudaMemcpyHostToDevice));
+    }
+    return MRS_OK;
 }
 
 double mrs_plan_iteration_bytes(const mrs_plan* p) { return p ? p->it_bytes : 0.0; }

@@ -85,7 +85,7 @@ def _smoother(plist) -> _lib.mrs_smoother:
 class DevicePlan:
     """One uploaded solver instance for a fixed RHS count m (owns a C plan)."""
 
-    def __init__(self, desc: _lib.mrs_plan_desc, levels, inv, method_name: str):
+    def __init__(self, desc: _lib.mrs_plan_desc, levels, inv, method_name: str, dist=None):
         self.L = _lib.lib()
         self.desc = desc
         self.method = method_name
@@ -93,6 +93,18 @@ class DevicePlan:
         _lib.check(self.L.mrs_plan_create(C.byref(desc), C.byref(h)), "plan create")
         self.h = h
         try:
+            if dist is not None:
+                team, lays = dist
+                _lib.check(self.L.mrs_plan_set_comm(h, team.comm), "plan set_comm")
+                for l, lay in enumerate(lays):
+                    _lib.check(self.L.mrs_plan_set_layout(h, l, int(lay.replicated),
+                                                          int(lay.slice[0]), int(lay.slice[1])),
+                               f"layout level {l}")
+                    for which, hp in lay.halos.items():
+                        _lib.check(self.L.mrs_plan_set_halo(
+                            h, l, which, hp.nsend, hp.send_idx.ctypes.data,
+                            hp.send_counts.ctypes.data, hp.recv_counts.ctypes.data),
+                            f"halo level {l}/{which}")
             for l, (A, P, R, bounds) in enumerate(levels):
                 keep: list = []
                 a = _lib.host_csr(A, keep)
@@ -195,14 +207,23 @@ def prepare(config: ParamTree, A, team=None, *, hierarchy=None, exec_mode: str =
     ``team``: a :class:`~paper_2103_07329_b200.team.GpuTeam` for the
     row-partitioned multi-GPU path (None = this process's current GPU).
     """
+    if team is not None and hasattr(team, "agg_rows_per_rank"):   # GpuTeam (a reference
+        from .team import prepare_distributed                      # WorkerTeam is ignored)
+        return prepare_distributed(config, A, team, hierarchy=hierarchy, exec_mode=exec_mode,
+                                   eig_bounds=eig_bounds)
+    desc, levels, inv, h, name, Ab = _configure(config, A, hierarchy, exec_mode, eig_bounds)
+    return _prepare_single(desc, levels, inv, h, name, Ab, config.role("solver").method)
+
+
+def _configure(config, A, hierarchy, exec_mode, eig_bounds):
+    """Validate the configuration and build everything that is uploaded:
+    plan descriptor, per-level (A, P, R, Chebyshev bounds), coarse inverse,
+    hierarchy, method name (solvers.py:864-953)."""
     if not config.finalized:
         config.set_defaults()
     violations = config.validate()
     if violations:
         raise ConfigurationError("; ".join(violations))
-    if team is not None and getattr(team, "world_size", 1) > 1:
-        from .team import prepare_distributed
-        return prepare_distributed(config, A, team, hierarchy=hierarchy, exec_mode=exec_mode)
     Ab = as_csr(A)
     if Ab.nrows != Ab.ncols:
         raise InvalidArgumentError("the system matrix must be square")
@@ -273,7 +294,10 @@ def prepare(config: ParamTree, A, team=None, *, hierarchy=None, exec_mode: str =
         desc.nlevels = h.nlevels
     else:
         raise ConfigurationError(f"preconditioner {pl.method!r} is not on the device path")
+    return desc, levels, inv, h, name, Ab
 
+
+def _prepare_single(desc, levels, inv, h, name, Ab, method):
     plans: dict = {}
 
     def plan_for(m: int) -> DevicePlan:

@@ -1,0 +1,281 @@
+"""Multi-GPU team: one process per GPU, row-partitioned hierarchy, NCCL.
+
+Replaces the reference's emulated worker team (src/parallel.py: WorkerTeam,
+ExchangePlan / halo_exchange, staged_sum) with real ranks:
+
+* every level is row-partitioned with the reference's rule (core.py:310-344,
+  :func:`make_partition`) until it has fewer than ``agg_rows_per_rank`` rows
+  per rank; from there on the hierarchy is **agglomerated** -- replicated on
+  every rank, fed by an all-gather of the restricted vector;
+* a rank's local block keeps each row's global entry order and renumbers its
+  columns as [own rows | halo rows ordered by (owner, global id)]: the SpMM
+  result of every row is bitwise the single-GPU one, and local column indices
+  shrink to 16 bits wherever the block allows (the reference's index
+  compression of segmented blocks, core.py:257-270, 364-404);
+* halo plans (:class:`HaloPlan`) play the reference's ExchangePlan
+  (parallel.py:259-300): import lists are the sorted unique referenced peer
+  rows; on the device a pack kernel + grouped ncclSend/ncclRecv fills the halo
+  segment before every SpMM whose operand has one;
+* dots: local partials -> ncclAllReduce -> the device epilogue (identical
+  scalars on every rank).
+
+The host logic here is pure numpy so it is testable on CPU (tests/test_team.py
+runs it on a gloo world of 2 and checks distributed SpMMs bitwise against
+global ones).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .core import CsrBlock, choose_width, make_partition
+from .errors import ConfigurationError, InvalidArgumentError
+
+__all__ = ["GpuTeam", "HaloPlan", "LevelLayout", "localize", "plan_levels", "equal_slices",
+           "prepare_distributed"]
+
+
+# ---------------------------------------------------------------------------
+# partitions and local blocks (host, numpy)
+# ---------------------------------------------------------------------------
+
+def equal_slices(n: int, nparts: int):
+    """Agglomeration slices: q = ceil(n/nparts) rows each (last one shorter),
+    so the all-gathered buffer of nparts*q rows holds the vector in order."""
+    q = -(-n // nparts)
+    return [(min(r * q, n), min((r + 1) * q, n)) for r in range(nparts)], q
+
+
+@dataclass
+class HaloPlan:
+    """Exchange of one gathered operand for one rank."""
+    send_idx: np.ndarray                 # int32 local rows, grouped by destination rank
+    send_counts: np.ndarray              # int32 [world]
+    recv_counts: np.ndarray              # int32 [world]
+
+    @property
+    def nrecv(self) -> int:
+        return int(self.recv_counts.sum())
+
+    @property
+    def nsend(self) -> int:
+        return int(self.send_counts.sum())
+
+
+def _halo_ids(blk: CsrBlock, rows: tuple, cols: tuple) -> np.ndarray:
+    lo, hi = rows
+    c = blk.col_idx[blk.row_ptr[lo]:blk.row_ptr[hi]].astype(np.int64)
+    return np.unique(c[(c < cols[0]) | (c >= cols[1])])
+
+
+def localize(blk: CsrBlock, rows: tuple, cols: tuple, col_ranges: list | None):
+    """Rows [rows) of `blk` with columns renumbered: own column range `cols`
+    first, then the halo (sorted global ids).  ``col_ranges`` = every rank's
+    column range (None: columns replicated -- no halo).
+    Returns (local CsrBlock, halo global ids, recv_counts per rank)."""
+    lo, hi = rows
+    k0, k1 = int(blk.row_ptr[lo]), int(blk.row_ptr[hi])
+    rp = (blk.row_ptr[lo:hi + 1] - k0).astype(np.int64)
+    c = blk.col_idx[k0:k1].astype(np.int64)
+    v = blk.values[k0:k1]
+    if col_ranges is None:
+        ncols = blk.ncols
+        new = c
+        halo = np.zeros(0, dtype=np.int64)
+        recv = None
+    else:
+        own = (c >= cols[0]) & (c < cols[1])
+        halo = np.unique(c[~own])
+        nloc = cols[1] - cols[0]
+        new = np.where(own, c - cols[0], nloc + np.searchsorted(halo, c))
+        ncols = nloc + len(halo)
+        recv = np.array([np.count_nonzero((halo >= a) & (halo < b)) for a, b in col_ranges],
+                        dtype=np.int32)
+    width = choose_width(max(ncols, 1))
+    local = CsrBlock(hi - lo, ncols, rp, new.astype(width.dtype), v, validate=False)
+    return local, halo, recv
+
+
+def halo_plan(blk: CsrBlock, row_ranges: list, col_ranges: list, rank: int) -> HaloPlan:
+    """My exchange for operand products of `blk`: rows each peer imports from
+    me (in its halo order) and my receive counts."""
+    world = len(row_ranges)
+    my_lo, my_hi = col_ranges[rank]
+    send, scount = [], np.zeros(world, dtype=np.int32)
+    for p in range(world):
+        if p == rank:
+            continue
+        h = _halo_ids(blk, row_ranges[p], col_ranges[p])
+        mine = h[(h >= my_lo) & (h < my_hi)] - my_lo
+        send.append(mine.astype(np.int32))
+        scount[p] = len(mine)
+    h = _halo_ids(blk, row_ranges[rank], col_ranges[rank])
+    recv = np.array([np.count_nonzero((h >= a) & (h < b)) for a, b in col_ranges], dtype=np.int32)
+    sidx = np.concatenate(send) if send else np.zeros(0, dtype=np.int32)
+    return HaloPlan(sidx.astype(np.int32), scount, recv)
+
+
+@dataclass
+class LevelLayout:
+    """One rank's view of one level."""
+    rows: tuple                    # owned rows (replicated: all)
+    replicated: bool
+    A: CsrBlock = None
+    P: CsrBlock | None = None
+    R: CsrBlock | None = None
+    halos: dict = field(default_factory=dict)      # 0: A, 1: R, 2: P -> HaloPlan
+    slice: tuple = (0, 0)          # agglomeration: (row0, rows) of my restricted slice
+
+
+def plan_levels(levels: list, rank: int, world: int, agg_rows_per_rank: int = 16384,
+                force_replicate_from: int | None = None) -> list:
+    """Row partition + local blocks + halo plans of every level for `rank`.
+
+    ``levels``: [(A, P, R)] global blocks (P, R None on the coarsest level).
+    Level l is partitioned while n_l / world >= agg_rows_per_rank (and the
+    level above is partitioned); ``force_replicate_from`` (tests) replicates
+    from that level on regardless.
+    """
+    n = [lv[0].nrows for lv in levels]
+    nl = len(levels)
+    repl = []
+    for l in range(nl):
+        r = (l > 0 and repl[l - 1]) or (l == nl - 1 and nl > 1) or n[l] < world or \
+            (l > 0 and n[l] / world < agg_rows_per_rank)
+        if force_replicate_from is not None and l >= force_replicate_from:
+            r = True
+        if l == 0:
+            r = False
+        repl.append(r)
+    ranges = [make_partition(n[l], world, allow_empty=True).ranges if not repl[l]
+              else [(0, n[l])] * world for l in range(nl)]
+    out = []
+    for l, (A, P, R) in enumerate(levels):
+        if repl[l]:
+            out.append(LevelLayout((0, n[l]), True, A, P, R))
+            continue
+        rr = ranges[l]
+        lay = LevelLayout(rr[rank], False)
+        lay.A, _, _ = localize(A, rr[rank], rr[rank], rr)
+        lay.halos[0] = halo_plan(A, rr, rr, rank)
+        if P is not None:
+            if repl[l + 1]:
+                # agglomeration: R restricts my slice of the (replicated) coarse
+                # rows; P reads the whole replicated coarse vector
+                sl, q = equal_slices(n[l + 1], world)
+                lay.R, _, _ = localize(R, sl[rank], rr[rank], rr)
+                lay.halos[1] = halo_plan(R, sl, rr, rank)
+                lay.P, _, _ = localize(P, rr[rank], (0, n[l + 1]), None)
+                out_slice = (sl[rank][0], q)
+            else:
+                rc = ranges[l + 1]
+                lay.R, _, _ = localize(R, rc[rank], rr[rank], rr)
+                lay.halos[1] = halo_plan(R, rc, rr, rank)
+                lay.P, _, _ = localize(P, rr[rank], rc[rank], rc)
+                lay.halos[2] = halo_plan(P, rr, rc, rank)
+                out_slice = None
+            lay._next_slice = out_slice
+        out.append(lay)
+    # the first replicated level records the slice it is gathered from
+    for l in range(1, nl):
+        if out[l].replicated and not out[l - 1].replicated:
+            row0, q = out[l - 1]._next_slice
+            out[l].slice = (row0, q)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the team
+# ---------------------------------------------------------------------------
+
+class GpuTeam:
+    """One rank per GPU over torch.distributed; owns an NCCL communicator for
+    the solve plans.  ``world_size == 1`` is valid (single GPU through the
+    distributed code path -- used by tests)."""
+
+    def __init__(self, agg_rows_per_rank: int = 16384, force_replicate_from: int | None = None):
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world_size = dist.get_rank(), dist.get_world_size()
+        else:
+            self.rank, self.world_size = 0, 1
+        self.agg_rows_per_rank = agg_rows_per_rank
+        self.force_replicate_from = force_replicate_from
+        self._comm = None
+
+    @property
+    def comm(self):
+        if self._comm is None:
+            import torch.distributed as dist
+            L = _lib.lib()
+            buf = (C.c_char * 128)()
+            if self.rank == 0:
+                _lib.check(L.mrs_comm_unique_id(buf), "nccl unique id")
+            uid = [bytes(buf)]
+            if self.world_size > 1:
+                dist.broadcast_object_list(uid, src=0)
+            h = C.c_void_p()
+            _lib.check(L.mrs_comm_create(uid[0], self.rank, self.world_size, C.byref(h)),
+                       "nccl communicator")
+            self._comm = h
+        return self._comm
+
+    def row_range(self, n: int) -> tuple:
+        return make_partition(n, self.world_size, allow_empty=True).ranges[self.rank]
+
+    def close(self):
+        if self._comm is not None:
+            _lib.lib().mrs_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: str = "graph",
+                        eig_bounds=None):
+    """``prepare`` on a team: every rank builds the (identical, deterministic)
+    global hierarchy, keeps its local blocks and uploads them.  ``run(B, X)``
+    takes THIS rank's rows of B and X (``team.row_range(n)``)."""
+    from .solvers import ConfiguredSolver, DevicePlan, _configure, _vector_args
+    from .errors import ShapeMismatchError
+    cfg = _configure(config, A, hierarchy, exec_mode, eig_bounds)
+    desc, levels, inv, h, name, Ab = cfg
+    glob = [(lv[0], lv[1], lv[2]) for lv in levels]
+    lays = plan_levels(glob, team.rank, team.world_size, team.agg_rows_per_rank,
+                       team.force_replicate_from)
+    local_levels = [(lay.A, lay.P, lay.R, levels[l][3]) for l, lay in enumerate(lays)]
+    lo, hi = lays[0].rows
+    desc.nrows = hi - lo
+    plans: dict = {}
+
+    def plan_for(m: int) -> DevicePlan:
+        if m not in plans:
+            d = _lib.mrs_plan_desc.from_buffer_copy(desc)
+            d.m = m
+            plans[m] = DevicePlan(d, local_levels, inv, name, dist=(team, lays))
+        return plans[m]
+
+    def run(B, X, x_is_zero=None):
+        shape, bp, xp, x_zero, host, stream, keep = _vector_args(B, X)
+        if x_is_zero is not None:
+            x_zero = bool(x_is_zero)
+        if shape[0] != hi - lo:
+            raise ShapeMismatchError(f"rank {team.rank} owns rows [{lo}, {hi}); got {shape[0]}")
+        st = plan_for(shape[1]).solve(bp, xp, x_zero, host, stream)
+        if host:
+            X.flags.zero = False
+            X.flags.initialized = True
+        return st
+
+    cs = ConfiguredSolver(name, run, h, plan_for)
+    cs.layouts = lays
+    cs.row_range = (lo, hi)
+    return cs

@@ -1,0 +1,52 @@
+"""The distributed (GpuTeam) device path on ONE GPU: an NCCL communicator of
+one rank drives the same schedule as N ranks -- local partial reductions ->
+ncclAllReduce -> device epilogue, and (forced) agglomeration with an
+ncclAllGather.  Halo exchanges are empty with one rank; their plans are
+checked bitwise on a gloo world of 2 in tests/test_team.py."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2103_07329_b200 import BlockVector, gen_poisson3d  # noqa: E402
+from paper_2103_07329_b200.params import tree  # noqa: E402
+from paper_2103_07329_b200.solvers import prepare  # noqa: E402
+from paper_2103_07329_b200.team import GpuTeam  # noqa: E402
+
+JAC = {"method": "Jacobi", "weight": "0.8"}
+CHEB = {"method": "Chebyshev", "polynomial_order": "2"}
+CASES = {
+    "amg_pcg": {"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"},
+                "pre_smoother": JAC, "post_smoother": JAC},
+    "amg_bicgstab_mixed": {"solver": {"method": "BiCGStab"},
+                           "preconditioner": {"method": "MultiGrid", "mg_mixed_precision": "1",
+                                              "mg_coarse_matrix_size": "100"},
+                           "pre_smoother": CHEB, "post_smoother": CHEB},
+    "jacobi_pcg": {"solver": {"method": "CG", "max_iters": "500"},
+                   "preconditioner": {"method": "Jacobi"}},
+}
+
+
+@pytest.mark.parametrize("name", list(CASES))
+@pytest.mark.parametrize("force", [None, 1, 2])
+def test_team_of_one_matches_single_gpu(name, force):
+    A, _ = gen_poisson3d(14, 13, 12)
+    B = np.random.default_rng(3).uniform(-1, 1, (A.nrows, 4))
+    roles = CASES[name]
+    Xs = BlockVector.zeros(A.nrows, 4)
+    ss = prepare(tree(roles), A).run(BlockVector.from_array(B), Xs)
+    team = GpuTeam(agg_rows_per_rank=1, force_replicate_from=force)
+    cs = prepare(tree(roles), A, team=team)
+    assert cs.row_range == (0, A.nrows)
+    Xd = BlockVector.zeros(A.nrows, 4)
+    sd = cs.run(BlockVector.from_array(B), Xd)
+    assert sd.iterations == ss.iterations and sd.all_converged
+    # one rank: identical arithmetic (NCCL sum of one partial is the partial)
+    np.testing.assert_array_equal(Xd.data, Xs.data)
+    np.testing.assert_array_equal(sd.final_rel_residual, ss.final_rel_residual)
+    team.close()
