@@ -196,6 +196,10 @@ int  mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend,
                        const int32_t* recv_counts);
 
 double mrs_plan_iteration_bytes(const mrs_plan* p);
+/* Warm per-launch device times (us) of one iteration body, each launch
+ * bracketed by CUDA events (diagnostics; call after one mrs_plan_solve). */
+int  mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32_t cap,
+                      int32_t* count);
 int  mrs_plan_kernel_count(const mrs_plan* p);   /* kernels per outer iteration */
 int  mrs_plan_fixed_kernel_count(const mrs_plan* p); /* kernels outside the loop */
 void mrs_plan_destroy(mrs_plan* p);

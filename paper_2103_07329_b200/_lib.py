@@ -83,6 +83,8 @@ SIGNATURES = {
     "mrs_plan_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                  C.c_void_p, C.POINTER(mrs_stats), C.c_void_p, C.c_void_p]),
     "mrs_plan_iteration_bytes": (C.c_double, [C.c_void_p]),
+    "mrs_plan_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+                                   C.POINTER(C.c_int32)]),
     "mrs_plan_kernel_count": (C.c_int, [C.c_void_p]),
     "mrs_plan_fixed_kernel_count": (C.c_int, [C.c_void_p]),
     "mrs_plan_destroy": (None, [C.c_void_p]),

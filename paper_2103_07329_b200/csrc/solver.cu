@@ -960,6 +960,40 @@ int mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend, cons
 }
 
 double mrs_plan_iteration_bytes(const mrs_plan* p) { return p ? p->it_bytes : 0.0; }
+
+// Warm per-launch timing of one iteration body: runs the prologue and `iters`
+// iterations eagerly (B already in the plan from a previous solve, X zero),
+// timing every launch of the last iteration with CUDA events.
+int mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32_t cap,
+                     int32_t* count) {
+    if (!p || !p->finalized || !us || !count || iters < 1) return MRS_ERR_ARG;
+    cudaStream_t s = (cudaStream_t)stream;
+    Program pg;
+    if (p->desc.method == MRS_METHOD_CG) build_cg(p, true, pg);
+    else build_bicgstab(p, true, pg);
+    const size_t bytes = (size_t)p->n * p->m * 8;
+    MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
+    set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);
+    MRS_CUDA_OK(run_list(pg.pro, s));
+    for (int it = 0; it + 1 < iters; ++it) MRS_CUDA_OK(run_list(pg.body, s));
+    const int n = (int)pg.body.size();
+    std::vector<cudaEvent_t> ev(n + 1);
+    for (auto& e : ev) MRS_CUDA_OK(cudaEventCreate(&e));
+    MRS_CUDA_OK(cudaEventRecord(ev[0], s));
+    for (int i = 0; i < n; ++i) {
+        MRS_CUDA_OK(pg.body[i](s));
+        MRS_CUDA_OK(cudaEventRecord(ev[i + 1], s));
+    }
+    MRS_CUDA_OK(cudaStreamSynchronize(s));
+    *count = n;
+    for (int i = 0; i < n && i < cap; ++i) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
+        us[i] = 1e3 * ms;
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    return MRS_OK;
+}
 int mrs_plan_kernel_count(const mrs_plan* p) { return p ? p->body_kernels : 0; }
 int mrs_plan_fixed_kernel_count(const mrs_plan* p) { return p ? p->fixed_kernels : 0; }
 

@@ -141,6 +141,15 @@ class DevicePlan:
     def kernels_per_iteration(self) -> int:
         return self.L.mrs_plan_kernel_count(self.h)
 
+    def profile(self, iters: int = 3) -> np.ndarray:
+        """Warm per-launch times (us) of one iteration body (diagnostics)."""
+        import torch
+        out = np.zeros(512)
+        n = C.c_int32()
+        _lib.check(self.L.mrs_plan_profile(self.h, iters, C.c_void_p(torch.cuda.current_stream().cuda_stream),
+                                           out.ctypes.data, 512, C.byref(n)), "profile")
+        return out[:n.value].copy()
+
     def kernel_launches(self, iterations: int) -> int:
         """Kernels one solve of `iterations` iterations launches."""
         return self.L.mrs_plan_fixed_kernel_count(self.h) + iterations * self.kernels_per_iteration

@@ -1,0 +1,40 @@
+#!/usr/bin/env python
+"""Warm per-launch device times of one solver iteration (CUDA events around
+each launch; no profiler).  Complements the cold ncu launch list.
+
+    python scripts/warm_profile.py --config c2
+"""
+import argparse
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="c2")
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+    import bench
+    from paper_2103_07329_b200 import gen_poisson3d
+    from paper_2103_07329_b200.params import tree
+    from paper_2103_07329_b200.solvers import prepare
+    bench.select(a.config)
+    A, _ = gen_poisson3d(bench.GRID, bench.GRID, bench.GRID)
+    B = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, (A.nrows, bench.M))).cuda()
+    X = torch.zeros_like(B)
+    cs = prepare(tree(bench.ROLES), A)
+    cs.run(B, X, x_is_zero=True)
+    plan = cs.plan_factory(bench.M)
+    t = plan.profile(3)
+    t = plan.profile(3)
+    print(f"{len(t)} launches/iteration, sum {t.sum():.1f} us")
+    for i, v in enumerate(t):
+        print(f"{i:3d} {v:8.2f}")
+
+
+if __name__ == "__main__":
+    main()
