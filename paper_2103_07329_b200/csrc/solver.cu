@@ -961,9 +961,10 @@ int mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend, cons
 
 double mrs_plan_iteration_bytes(const mrs_plan* p) { return p ? p->it_bytes : 0.0; }
 
-// Warm per-launch timing of one iteration body: runs the prologue and `iters`
-// iterations eagerly (B already in the plan from a previous solve, X zero),
-// timing every launch of the last iteration with CUDA events.
+// Warm per-launch timing of one iteration body: after `iters` eager
+// iterations (warm caches, realistic data), each launch of the body is
+// captured R times back-to-back into its own graph and timed with CUDA
+// events; us[i] = device time per launch (no host launch gaps).
 int mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32_t cap,
                      int32_t* count) {
     if (!p || !p->finalized || !us || !count || iters < 1) return MRS_ERR_ARG;
@@ -975,23 +976,37 @@ int mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32
     MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
     set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);
     MRS_CUDA_OK(run_list(pg.pro, s));
-    for (int it = 0; it + 1 < iters; ++it) MRS_CUDA_OK(run_list(pg.body, s));
-    const int n = (int)pg.body.size();
-    std::vector<cudaEvent_t> ev(n + 1);
-    for (auto& e : ev) MRS_CUDA_OK(cudaEventCreate(&e));
-    MRS_CUDA_OK(cudaEventRecord(ev[0], s));
-    for (int i = 0; i < n; ++i) {
-        MRS_CUDA_OK(pg.body[i](s));
-        MRS_CUDA_OK(cudaEventRecord(ev[i + 1], s));
-    }
+    for (int it = 0; it < iters; ++it) MRS_CUDA_OK(run_list(pg.body, s));
     MRS_CUDA_OK(cudaStreamSynchronize(s));
+    const int n = (int)pg.body.size();
+    const int R = 20;
+    cudaEvent_t e0, e1;
+    MRS_CUDA_OK(cudaEventCreate(&e0));
+    MRS_CUDA_OK(cudaEventCreate(&e1));
+    cudaStream_t cs;
+    MRS_CUDA_OK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     *count = n;
     for (int i = 0; i < n && i < cap; ++i) {
+        cudaGraph_t g;
+        MRS_CUDA_OK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+        for (int r = 0; r < R; ++r) pg.body[i](cs);
+        MRS_CUDA_OK(cudaStreamEndCapture(cs, &g));
+        cudaGraphExec_t ge;
+        MRS_CUDA_OK(cudaGraphInstantiate(&ge, g, 0));
+        MRS_CUDA_OK(cudaGraphLaunch(ge, s));
+        MRS_CUDA_OK(cudaEventRecord(e0, s));
+        MRS_CUDA_OK(cudaGraphLaunch(ge, s));
+        MRS_CUDA_OK(cudaEventRecord(e1, s));
+        MRS_CUDA_OK(cudaStreamSynchronize(s));
         float ms = 0.f;
-        cudaEventElapsedTime(&ms, ev[i], ev[i + 1]);
-        us[i] = 1e3 * ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        us[i] = 1e3 * ms / R;
+        cudaGraphExecDestroy(ge);
+        cudaGraphDestroy(g);
     }
-    for (auto& e : ev) cudaEventDestroy(e);
+    cudaStreamDestroy(cs);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
     return MRS_OK;
 }
 int mrs_plan_kernel_count(const mrs_plan* p) { return p ? p->body_kernels : 0; }
