@@ -232,8 +232,9 @@ int  mrs_eig_bounds(const mrs_host_csr* A, int32_t iterations, uint64_t seed_unu
 
 const char* mrs_status_string(int32_t status);
 int  mrs_version(void);
-/* Tuning knobs: "pdl" (0/1) -- programmatic dependent launch of the
- * solve-path kernels.  Read when a plan captures its graph. */
+/* Tuning knobs, read when a plan captures its graph:
+ *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
+ *   "spmm_wide" -1/0/1 long-row SpMM layout: auto (nnz/row >= 12), never, always */
 int  mrs_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

@@ -39,6 +39,7 @@ int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);
 int max_grid();
 void set_pdl(int on);
+void set_spmm_wide(int v);
 int vec_op_k(int op);   // reduced values per column of a vector op (0 = none)
 
 }  // namespace mrs

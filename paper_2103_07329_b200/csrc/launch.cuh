@@ -9,6 +9,8 @@
 
 namespace mrs {
 
+int spmm_wide_mode();   // -1 auto (by nnz/row), 0 never, 1 always (mrs_set_option)
+
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, Args... args) {
@@ -72,6 +74,20 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         a.chunk = chunk;
         (void)launch_ex(kern, g, s, a);
     };
+    // long rows (AMG coarse operators): the wide layout (spmm.cuh Lay)
+    const int wide_knob = spmm_wide_mode();
+    const bool wide = !generic && (m == 2 || m == 4 || m == 8 || m == 16) &&
+                      (wide_knob == 1 || (wide_knob < 0 && a.nrows > 0 &&
+                                          a.nnz_hint >= 12 * a.nrows));
+    if (wide) {
+        switch (m) {
+        case 2: go(spmm_kernel<2, OP, Tv, Ti, true>, Lay<2, true>::RPB); break;
+        case 4: go(spmm_kernel<4, OP, Tv, Ti, true>, Lay<4, true>::RPB); break;
+        case 8: go(spmm_kernel<8, OP, Tv, Ti, true>, Lay<8, true>::RPB); break;
+        case 16: go(spmm_kernel<16, OP, Tv, Ti, true>, Lay<16, true>::RPB); break;
+        }
+        return cudaGetLastError();
+    }
     switch (generic ? 0 : m) {
     case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
     case 2: go(spmm_kernel<2, OP, Tv, Ti>, Lay<2>::RPB); break;

@@ -28,10 +28,15 @@
 
 namespace mrs {
 
-template <int M> struct Lay {
-    static constexpr int CPL = (M == 1) ? 1 : (M <= 16 ? 2 : M / 8);
+// WIDE: long-row layout (AMG coarse operators, ~20-40 nnz/row): one column
+// per lane (LPR = M) and 8 entries in flight per lane, so a row's dependent
+// load chain is half as long; the default packs 2 columns per lane (16-byte
+// accesses) with 4 entries in flight.  Accumulation order is the same.
+template <int M, bool WIDE = false> struct Lay {
+    static constexpr int CPL = WIDE ? 1 : ((M == 1) ? 1 : (M <= 16 ? 2 : M / 8));
     static constexpr int LPR = M / CPL;
     static constexpr int RPB = kThreads / LPR;     // rows per CTA pass
+    static constexpr int UNR = WIDE ? 8 : 4;       // entries in flight per lane
 };
 
 // Kernel operation selector.
@@ -69,6 +74,7 @@ struct SpArgs {
                             // 1: seed_out = w*(y/d)  2: seed_out = y/(d*theta)
     double* seed_out;
     int64_t chunk;          // rows per CTA (contiguous range, multiple of RPB)
+    int64_t nnz_hint;       // matrix nnz (layout choice)
     RedArgs red;
 };
 
@@ -101,34 +107,28 @@ template <typename Tv, typename Ti> struct SSrc {
     __device__ __forceinline__ double val(int64_t k) const { return widen(v[k - v_off]); }
 };
 
-// Accumulate one row: acc op= sum_k v_k * g(col_k), entry order; loads of a
-// group of 4 entries are issued before their (ordered) accumulation.
-template <int OP, int CPL, bool SUBTRACT, class Src>
+// Accumulate one row: acc op= sum_k v_k * g(col_k), entry order; the loads
+// of a group of UNR entries are issued before their (ordered) accumulation.
+template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4>
 __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int64_t lo,
                                                int64_t hi, int64_t ld, int cofs,
                                                double (&acc)[CPL]) {
     int64_t k = lo;
-    for (; k + 4 <= hi; k += 4) {
-        const int64_t c0 = src.col(k), c1 = src.col(k + 1), c2 = src.col(k + 2), c3 = src.col(k + 3);
-        const double v0 = src.val(k), v1 = src.val(k + 1), v2 = src.val(k + 2), v3 = src.val(k + 3);
-        Vec<CPL> g0 = gather<OP, CPL>(a, c0, ld, cofs);
-        Vec<CPL> g1 = gather<OP, CPL>(a, c1, ld, cofs);
-        Vec<CPL> g2 = gather<OP, CPL>(a, c2, ld, cofs);
-        Vec<CPL> g3 = gather<OP, CPL>(a, c3, ld, cofs);
+    for (; k + UNR <= hi; k += UNR) {
+        int64_t c[UNR];
+        double v[UNR];
+        Vec<CPL> g[UNR];
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            if constexpr (SUBTRACT) {
-                acc[i] = sub(acc[i], mul(v0, g0.v[i]));
-                acc[i] = sub(acc[i], mul(v1, g1.v[i]));
-                acc[i] = sub(acc[i], mul(v2, g2.v[i]));
-                acc[i] = sub(acc[i], mul(v3, g3.v[i]));
-            } else {
-                acc[i] = add(acc[i], mul(v0, g0.v[i]));
-                acc[i] = add(acc[i], mul(v1, g1.v[i]));
-                acc[i] = add(acc[i], mul(v2, g2.v[i]));
-                acc[i] = add(acc[i], mul(v3, g3.v[i]));
+        for (int u = 0; u < UNR; ++u) { c[u] = src.col(k + u); v[u] = src.val(k + u); }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL>(a, c[u], ld, cofs);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v[u], g[u].v[i]));
+                else acc[i] = add(acc[i], mul(v[u], g[u].v[i]));
             }
-        }
     }
     for (; k < hi; ++k) {
         const int64_t c0 = src.col(k);
@@ -144,7 +144,7 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
 
 // One (row, column-slice) of work for every op.  `dotp` accumulates the fused
 // dot (OP_SPMV with a.dot: x_own . y).
-template <int OP, int CPL, class Src>
+template <int OP, int CPL, class Src, int UNR = 4>
 __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t row, int64_t lo,
                                        int64_t hi, int64_t ld, int cofs, double (&dotp)[CPL]) {
     const int64_t o = row * ld + cofs;
@@ -164,9 +164,9 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         }
         if (mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD)
-            row_accumulate<OP, CPL, false>(a, src, lo, hi, ld, cofs, acc);
+            row_accumulate<OP, CPL, false, Src, UNR>(a, src, lo, hi, ld, cofs, acc);
         else
-            row_accumulate<OP, CPL, true>(a, src, lo, hi, ld, cofs, acc);
+            row_accumulate<OP, CPL, true, Src, UNR>(a, src, lo, hi, ld, cofs, acc);
         Vec<CPL> out;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
@@ -188,7 +188,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
         Vec<CPL> bb = load_vec<CPL>(a.b + o);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
-        row_accumulate<OP, CPL, true>(a, src, lo, hi, ld, cofs, acc);
+        row_accumulate<OP, CPL, true, Src, UNR>(a, src, lo, hi, ld, cofs, acc);
         const double dd = __ldg(a.d + row);
         Vec<CPL> xo = load_vec<CPL>(a.x + o);
         if constexpr (OP == OP_CHEB_FIRST) {
@@ -214,7 +214,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-        row_accumulate<OP, CPL, false>(a, src, lo, hi, ld, cofs, acc);   // tmp = A dv
+        row_accumulate<OP, CPL, false, Src, UNR>(a, src, lo, hi, ld, cofs, acc);   // tmp = A dv
         const double dd = __ldg(a.d + row);
         Vec<CPL> r = load_vec<CPL>(a.r_in + o);
         Vec<CPL> dv = load_vec<CPL>(a.x + o);
@@ -239,9 +239,9 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
 
 // CTA-level fixed-shape reduction of the fused-dot partials (warp xor tree
 // over row groups, then warps in order), finished by finish_reduction.
-template <int M>
-__device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[Lay<M>::CPL]) {
-    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR;
+template <int M, bool WIDE>
+__device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[Lay<M, WIDE>::CPL]) {
+    constexpr int CPL = Lay<M, WIDE>::CPL, LPR = Lay<M, WIDE>::LPR;
     __shared__ double s_w[kThreads / 32][M];
     __shared__ double s_blk[M];
 #pragma unroll
@@ -263,11 +263,11 @@ __device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[L
     finish_reduction(a.red, s_blk, M, M);
 }
 
-template <int M, int OP, typename Tv, typename Ti>
+template <int M, int OP, typename Tv, typename Ti, bool WIDE = false>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
-    using L = Lay<M>;
+    using L = Lay<M, WIDE>;
     constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
     const int lane = threadIdx.x % LPR;
     const int cofs = lane * CPL;
@@ -279,9 +279,10 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
          r0 += (int64_t)gridDim.x * a.chunk) {
         const int64_t r1 = min(r0 + a.chunk, a.nrows);
         for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
-            do_row<OP, CPL>(a, src, row, __ldg(a.rp + row), __ldg(a.rp + row + 1), M, cofs, dotp);
+            do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src, row, __ldg(a.rp + row),
+                                                  __ldg(a.rp + row + 1), M, cofs, dotp);
     }
-    if (a.dot) spmm_block_dot<M>(a, dotp);
+    if (a.dot) spmm_block_dot<M, WIDE>(a, dotp);
 }
 
 // Generic m (any value, any layout): one thread per (row, column), thread
