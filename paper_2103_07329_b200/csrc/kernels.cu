@@ -24,7 +24,7 @@ bool pdl_enabled() {
 
 void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
-static int g_wide = -1;
+static int g_wide = 0;   // wide layout measured slower on C2/C3 (profiles/r01_ab_experiments.txt)
 int spmm_wide_mode() { return g_wide; }
 void set_spmm_wide(int v) { g_wide = v < 0 ? -1 : (v ? 1 : 0); }
 
