@@ -61,17 +61,19 @@ template <int OP, typename Tv, typename Ti>
 inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     int g;
     auto go = [&](auto kern, int64_t rpp) {
-        // chunks of up to ~512 rows (fewer when that would idle SMs), strided
-        // over one wave of CTAs
+        // Balanced one wave: every CTA gets the same number of passes (the
+        // slowest CTA sets the kernel time), in chunks of <= ~512 rows strided
+        // over the grid (L1 reuse inside a chunk, L2-resident band across).
         const int64_t cap = (int64_t)blocks_per_sm((const void*)kern) * num_sms();
-        int64_t passes = a.nrows / (rpp * cap);
+        const int64_t P = (a.nrows + rpp - 1) / rpp;             // passes in total
+        const int64_t ppc = (P + cap - 1) / cap;                  // passes per CTA
         const int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
-        passes = passes < 1 ? 1 : (passes > pmax ? pmax : passes);
-        const int64_t chunk = rpp * passes;
-        const int64_t nchunks = (a.nrows + chunk - 1) / chunk;
-        g = (int)(nchunks < cap ? nchunks : cap);
+        const int64_t sp = ppc < pmax ? ppc : pmax;               // passes per chunk
+        const int64_t nchunks = (P + sp - 1) / sp;
+        const int64_t cpc = (nchunks + cap - 1) / cap;            // chunks per CTA
+        g = (int)((nchunks + cpc - 1) / cpc);
         if (g < 1) g = 1;
-        a.chunk = chunk;
+        a.chunk = rpp * sp;
         (void)launch_ex(kern, g, s, a);
     };
     // long rows (AMG coarse operators): the wide layout (spmm.cuh Lay)

@@ -36,10 +36,11 @@ def main():
     b = torch.rand(A.nrows, a.m, dtype=torch.float64, device="cuda")
     y = torch.empty_like(b)
     mode = K.MODE_RSUB if a.mode == "rsub" else K.MODE_ASSIGN
-    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    flush = torch.ones(32 << 20, dtype=torch.float64, device="cuda")
+    sink = torch.empty((), dtype=torch.float64, device="cuda")
     ts = []
     for r in range(a.reps):
-        flush.add_(1)
+        torch.sum(flush, out=sink)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         K.csr_spmv(D, None, None, x, y, mode, b)
