@@ -9,7 +9,7 @@ uniform[-1,1] right-hand sides, zero initial guess, classical RS AMG V(1,1)
 with weighted Jacobi (w = 0.8) preconditioning CG, fp64, tol 1e-8.  A step
 is one whole solve with B, X resident in HBM; setup (prepare) is excluded,
 like the reference's bench (src/cli.py:111-146).  L2 is flushed (256 MB read
-write) between timed steps, outside the per-step CUDA events.
+) between timed steps, outside the per-step CUDA events.
 
 N > 1 (torchrun): the one global system is row-partitioned over the ranks
 (team.py: halo exchange + m-wide dot allreduce over NCCL, coarse levels
@@ -257,7 +257,7 @@ def spmm_sweep(torch, K, quick: bool):
                 K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
             times = []
             for _ in range(10):
-                torch.sum(flush_buf, out=flush_sink)
+                torch.sum(flush_buf, dim=0, out=flush_sink)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record()
                 K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
@@ -325,7 +325,7 @@ def main():
     flush_sink = torch.empty((), dtype=torch.float64, device="cuda")
 
     def flush_l2():
-        torch.sum(flush_buf, out=flush_sink)
+        torch.sum(flush_buf, dim=0, out=flush_sink)
 
     for _ in range(max(args.warmup, 3)):
         st = cs.run(Bd, Xd, x_is_zero=True)

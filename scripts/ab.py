@@ -45,7 +45,7 @@ def main():
                 cs.run(B, X, x_is_zero=True)
             ts = []
             for _ in range(a.steps):
-                torch.sum(flush, out=sink)
+                torch.sum(flush, dim=0, out=sink)
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(); st = cs.run(B, X, x_is_zero=True); e1.record(); e1.synchronize()
                 ts.append(e0.elapsed_time(e1))
