@@ -40,6 +40,8 @@ int spmm_grid(int64_t nrows, int64_t m);
 int max_grid();
 void set_pdl(int on);
 void set_spmm_wide(int v);
+void set_spmm_prefetch(int v);
+int spmm_prefetch_mode();
 int vec_op_k(int op);   // reduced values per column of a vector op (0 = none)
 
 }  // namespace mrs

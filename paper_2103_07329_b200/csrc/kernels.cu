@@ -24,6 +24,9 @@ bool pdl_enabled() {
 
 void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
+static int g_prefetch = 1;
+int spmm_prefetch_mode() { return g_prefetch; }
+void set_spmm_prefetch(int v) { g_prefetch = v ? 1 : 0; }
 static int g_wide = 0;   // wide layout measured slower on C2/C3 (profiles/r01_ab_experiments.txt)
 int spmm_wide_mode() { return g_wide; }
 void set_spmm_wide(int v) { g_wide = v < 0 ? -1 : (v ? 1 : 0); }
@@ -41,6 +44,8 @@ int vec_grid(int64_t n, int64_t m) {
 cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream_t s,
                         bool generic) {
     a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.nrows = A.nrows; a.m = m; a.nnz_hint = A.nnz;
+    a.ncols_hint = A.ncols;
+    a.prefetch = spmm_prefetch_mode();
     if (A.nrows == 0) return cudaSuccess;
     if (A.vb == 8) return launch_spmm_f64(op, A, a, m, s, generic);
     if (A.vb == 4) return launch_spmm_f32(op, A, a, m, s, generic);

@@ -75,6 +75,8 @@ struct SpArgs {
     double* seed_out;
     int64_t chunk;          // rows per CTA (contiguous range, multiple of RPB)
     int64_t nnz_hint;       // matrix nnz (layout choice)
+    int64_t ncols_hint;     // matrix columns (square: own x rows are prefetchable)
+    int prefetch;           // bulk-prefetch each chunk's streams into L2
     RedArgs red;
 };
 
@@ -89,6 +91,37 @@ __device__ __forceinline__ double seed_value(int mode, double v, double d, doubl
 template <int OP, int CPL>
 __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t ld, int cofs) {
     return load_vec<CPL>(a.x + col * ld + cofs);
+}
+
+// cp.async.bulk.prefetch.L2: one instruction pulls a contiguous byte range
+// into L2 (16-byte aligned, size a multiple of 16).
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, size_t bytes) {
+    uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
+    uintptr_t a1 = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
+    while (a1 > a0) {
+        const uint32_t n = (uint32_t)min((uintptr_t)(1u << 20), a1 - a0);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
+        a0 += n;
+    }
+}
+
+// Prefetch the streams of rows [r0, r1): row pointers, CSR entries, and the
+// row-indexed vector operands (b / y / own x rows).  Lanes 0..3 of warp 0
+// split the work.
+template <typename Tv, typename Ti>
+__device__ __forceinline__ void prefetch_chunk(const SpArgs& a, int64_t r0, int64_t r1, int64_t ld) {
+    const int lane = threadIdx.x;
+    if (lane == 0) bulk_prefetch_l2(a.rp + r0, (size_t)(r1 - r0 + 1) * sizeof(int32_t));
+    if (lane == 1 || lane == 2) {
+        const int64_t k0 = __ldg(a.rp + r0), k1 = __ldg(a.rp + r1);
+        if (lane == 1) bulk_prefetch_l2(reinterpret_cast<const Ti*>(a.ci) + k0, (size_t)(k1 - k0) * sizeof(Ti));
+        else bulk_prefetch_l2(reinterpret_cast<const Tv*>(a.vals) + k0, (size_t)(k1 - k0) * sizeof(Tv));
+    }
+    const size_t vb = (size_t)(r1 - r0) * ld * sizeof(double);
+    if (lane == 3 && a.b) bulk_prefetch_l2(a.b + r0 * ld, vb);
+    if (lane == 4 && a.x && a.nrows == a.ncols_hint) bulk_prefetch_l2(a.x + r0 * ld, vb);
+    if (lane == 5 && a.mode != 0 && a.y && (a.mode == MRS_MODE_ADD || a.mode == MRS_MODE_SUB))
+        bulk_prefetch_l2(a.y + r0 * ld, vb);
 }
 
 // Where a row's (column, value) entries come from: global memory (read-only
@@ -278,6 +311,11 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
          r0 += (int64_t)gridDim.x * a.chunk) {
         const int64_t r1 = min(r0 + a.chunk, a.nrows);
+        if (a.prefetch) {
+            // TMA bulk L2 prefetch of this chunk's streams (this chunk is
+            // first touched now; the next chunk of this CTA is stride away)
+            if (threadIdx.x < 32) prefetch_chunk<Tv, Ti>(a, r0, r1, M);
+        }
         for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
             do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src, row, __ldg(a.rp + row),
                                                   __ldg(a.rp + row + 1), M, cofs, dotp);
