@@ -235,7 +235,8 @@ int  mrs_version(void);
 /* Tuning knobs, read when a plan captures its graph:
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
  *   "spmm_wide" -1/0/1 long-row SpMM layout: auto (nnz/row >= 12), never, always
- *   "spmm_prefetch" 0/1 TMA bulk L2 prefetch of each SpMM chunk's streams */
+ *   "spmm_prefetch" 0/1 TMA bulk L2 prefetch of each SpMM chunk's streams
+ *   "tail_rows" N  V-cycle levels with <= N rows run as one cluster kernel (0: off) */
 int  mrs_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

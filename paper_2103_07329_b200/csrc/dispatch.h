@@ -34,6 +34,13 @@ cudaError_t launch_vec(int op, VArgs a, cudaStream_t s);
 // Dense coarse solve x = Ainv b for (nc, m) blocks.
 cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
                           int64_t m, const int* guard, cudaStream_t s);
+// V-cycle tail on one thread-block cluster (tail.cu)
+struct TailStep;
+cudaError_t launch_tail(const TailStep* steps, int nsteps, int64_t m, const int* guard, int csize,
+                        cudaStream_t s);
+int tail_cluster_size(int64_t m);
+int tail_rows_threshold();
+void set_tail_rows(int64_t v);
 // Grid the reduction kernels use (partials buffer sizing).
 int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);

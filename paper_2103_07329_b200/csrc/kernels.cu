@@ -24,7 +24,10 @@ bool pdl_enabled() {
 
 void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
-static int g_prefetch = 1;
+static int64_t g_tail_rows = 4096;
+int tail_rows_threshold() { return (int)g_tail_rows; }
+void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
+static int g_prefetch = 0;   // measured slower (profiles/r01_ab_experiments.txt)
 int spmm_prefetch_mode() { return g_prefetch; }
 void set_spmm_prefetch(int v) { g_prefetch = v ? 1 : 0; }
 static int g_wide = 0;   // wide layout measured slower on C2/C3 (profiles/r01_ab_experiments.txt)

@@ -20,9 +20,12 @@
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <string>
 #include <vector>
 
 #include "comm.h"
+#include "tail.cuh"
 #include "dispatch.h"
 
 using namespace mrs;
@@ -65,6 +68,9 @@ struct mrs_plan {
     std::vector<LevelDev> L;
     mrs_comm* comm = nullptr;  // multi-GPU: NCCL communicator (dist = set)
     bool dist = false;
+    int tail_from = -1;        // first level run by the cluster tail kernel (-1: none)
+    int tail_csize = 0;
+    std::map<std::string, TailStep*> tail_cache;   // uploaded step lists
     double* inv = nullptr;
     int64_t nc = 0;
     std::vector<void*> owned;
@@ -128,6 +134,8 @@ struct Builder {
     const int* guard = nullptr;       // body kernels: &st->skip
     double bytes = 0;                 // algorithmic bytes accumulated
     int kernels = 0;
+    std::vector<TailStep>* rec = nullptr;   // recording a tail sub-V-cycle
+    bool rec_fail = false;
     double V(int64_t rows) const { return (double)rows * P->m * 8.0; }
 
     RedArgs red(int epi) const {
@@ -138,6 +146,18 @@ struct Builder {
     }
     static SpArgs sp0() { SpArgs a; memset(&a, 0, sizeof(a)); return a; }
     static VArgs v0() { VArgs a; memset(&a, 0, sizeof(a)); return a; }
+
+    // device copy of a recorded tail step list (memoized by content)
+    const TailStep* upload_tail(const std::vector<TailStep>& steps) {
+        std::string key(reinterpret_cast<const char*>(steps.data()), steps.size() * sizeof(TailStep));
+        auto it = P->tail_cache.find(key);
+        if (it != P->tail_cache.end()) return it->second;
+        TailStep* d = dalloc<TailStep>(steps.size(), P->owned);
+        if (!d) return nullptr;
+        if (cudaMemcpy(d, steps.data(), key.size(), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+        P->tail_cache[key] = d;
+        return d;
+    }
 
     // multi-GPU: exchange the halo rows of a gathered operand before its use
     void exchange(const Halo* h, const double* x) {
@@ -171,6 +191,18 @@ struct Builder {
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
         int64_t m = P->m;
+        if (rec) {
+            if (a.dot) rec_fail = true;
+            TailStep t;
+            memset(&t, 0, sizeof(t));
+            t.kind = TK_SPMM; t.op = op; t.vb = A.vb; t.ib = A.ib;
+            a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.nrows = A.nrows; a.m = m;
+            a.nnz_hint = A.nnz; a.ncols_hint = A.ncols;
+            t.a = a;
+            rec->push_back(t);
+            bytes += A.bytes() + extra_bytes;
+            return;
+        }
         exchange(A.halo, a.x);
         const int mk = a.dot ? split_reduction(a.red) : 0;
         out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
@@ -179,6 +211,7 @@ struct Builder {
         kernels++;
     }
     void vec(int op, VArgs a, double b) {
+        if (rec) { rec_fail = true; return; }
         a.guard = a.guard ? a.guard : guard;
         a.m = P->m;
         const int K = vec_op_k(op);
@@ -340,12 +373,45 @@ struct Builder {
     void vcycle(int l, const double* b, bool zero, bool seeded, XB& x, int dot_epi) {
         mrs_plan& p = *P;
         LevelDev& lv = p.L[l];
+        if (!rec && l == p.tail_from && zero && seeded && dot_epi < 0) {
+            // the whole sub-V-cycle below (and at) level l: one cluster launch
+            std::vector<TailStep> steps;
+            Builder child{P, nullptr, guard};
+            child.rec = &steps;
+            XB xr = x;
+            child.vcycle(l, b, true, true, xr, -1);
+            if (!child.rec_fail && !steps.empty()) {
+                const TailStep* dsteps = upload_tail(steps);
+                if (dsteps) {
+                    x = xr;
+                    const int nsteps = (int)steps.size();
+                    const int64_t m = p.m;
+                    const int* g = guard;
+                    const int cs = p.tail_csize;
+                    out->push_back([=](cudaStream_t s) {
+                        return launch_tail(dsteps, nsteps, m, g, cs, s);
+                    });
+                    bytes += child.bytes;
+                    kernels++;
+                    return;
+                }
+            }
+        }
         if (coarsest(p, l)) {
             // x = A_c^{-1} b (replaces the LU solve, solvers.py:644-649)
             int64_t m = p.m, nc = p.nc;
             const double* inv = p.inv;
             double* xo = x.cur;
             const int* g = guard;
+            if (rec) {
+                TailStep t;
+                memset(&t, 0, sizeof(t));
+                t.kind = TK_COARSE; t.inv = inv; t.nc = nc; t.cb = b; t.cx = xo;
+                rec->push_back(t);
+                bytes += (double)nc * nc * 8.0 + 2 * V(nc);
+                if (dot_epi >= 0) rec_fail = true;
+                return;
+            }
             out->push_back([=](cudaStream_t s) { return launch_coarse(inv, nc, b, xo, m, g, s); });
             bytes += (double)nc * nc * 8.0 + 2 * V(nc);
             kernels++;
@@ -808,6 +874,22 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     MRS_CUDA_OK(cudaMemcpy(p->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     MRS_CUDA_OK(cudaEventCreate(&p->ev0));
     MRS_CUDA_OK(cudaEventCreate(&p->ev1));
+    // cluster tail: the deepest levels with <= tail_rows rows each (never
+    // level 0; distributed: only replicated levels)
+    if (p->desc.precond == MRS_PC_MG && tail_rows_threshold() > 0 && p->L.size() >= 3) {
+        const int cs = tail_cluster_size(m);
+        int from = -1;
+        for (int l = (int)p->L.size() - 2; l >= 1; --l) {
+            const LevelDev& lv = p->L[l];
+            if (lv.A.nrows > tail_rows_threshold()) break;
+            if (p->dist && !lv.replicated) break;
+            from = l;
+        }
+        if (cs > 0 && from >= 1) {
+            p->tail_from = from;
+            p->tail_csize = cs;
+        }
+    }
     p->finalized = true;
     // estimate the per-iteration byte model / kernel count once
     Program pg;

@@ -87,10 +87,39 @@ __device__ __forceinline__ double seed_value(int mode, double v, double d, doubl
     return mode == 1 ? mul(w_or_theta, divd(v, d)) : divd(v, mul(d, w_or_theta));
 }
 
+// Vector-operand loads: NC = through the read-only path (normal kernels: a
+// buffer is never written by the kernel that reads it); !NC = coherent loads
+// for the tail kernel, whose steps read what earlier steps wrote.
+template <int CPL>
+__device__ __forceinline__ Vec<CPL> load_vec_cg(const double* p) {
+    Vec<CPL> r;
+    if constexpr (CPL == 1) {
+        r.v[0] = __ldcg(p);
+    } else {
+#pragma unroll
+        for (int i = 0; i < CPL; i += 2) {
+            double2 t = __ldcg(reinterpret_cast<const double2*>(p + i));
+            r.v[i] = t.x; r.v[i + 1] = t.y;
+        }
+    }
+    return r;
+}
+template <int CPL, bool NC>
+__device__ __forceinline__ Vec<CPL> ldv(const double* p) {
+    if constexpr (NC) return load_vec<CPL>(p);
+    else return load_vec_cg<CPL>(p);          // L2 (coherent across the cluster)
+}
+// read-modify-write operands of a row (the thread that reads also writes)
+template <int CPL, bool NC>
+__device__ __forceinline__ Vec<CPL> ldv_rw(const double* p) {
+    if constexpr (NC) return load_vec_rw<CPL>(p);
+    else return load_vec_cg<CPL>(p);
+}
+
 // Value of the gathered operand at column `col` (CPL columns at cofs).
-template <int OP, int CPL>
+template <int OP, int CPL, bool NC = true>
 __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t ld, int cofs) {
-    return load_vec<CPL>(a.x + col * ld + cofs);
+    return ldv<CPL, NC>(a.x + col * ld + cofs);
 }
 
 // cp.async.bulk.prefetch.L2: one instruction pulls a contiguous byte range
@@ -142,7 +171,7 @@ template <typename Tv, typename Ti> struct SSrc {
 
 // Accumulate one row: acc op= sum_k v_k * g(col_k), entry order; the loads
 // of a group of UNR entries are issued before their (ordered) accumulation.
-template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4>
+template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4, bool NC = true>
 __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int64_t lo,
                                                int64_t hi, int64_t ld, int cofs,
                                                double (&acc)[CPL]) {
@@ -154,7 +183,7 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
 #pragma unroll
         for (int u = 0; u < UNR; ++u) { c[u] = src.col(k + u); v[u] = src.val(k + u); }
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL>(a, c[u], ld, cofs);
+        for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL, NC>(a, c[u], ld, cofs);
 #pragma unroll
         for (int u = 0; u < UNR; ++u)
 #pragma unroll
@@ -166,7 +195,7 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
     for (; k < hi; ++k) {
         const int64_t c0 = src.col(k);
         const double v0 = src.val(k);
-        Vec<CPL> g0 = gather<OP, CPL>(a, c0, ld, cofs);
+        Vec<CPL> g0 = gather<OP, CPL, NC>(a, c0, ld, cofs);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
             if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v0, g0.v[i]));
@@ -177,7 +206,7 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
 
 // One (row, column-slice) of work for every op.  `dotp` accumulates the fused
 // dot (OP_SPMV with a.dot: x_own . y).
-template <int OP, int CPL, class Src, int UNR = 4>
+template <int OP, int CPL, class Src, int UNR = 4, bool NC = true>
 __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t row, int64_t lo,
                                        int64_t hi, int64_t ld, int cofs, double (&dotp)[CPL]) {
     const int64_t o = row * ld + cofs;
@@ -188,18 +217,18 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
         } else if (mode == MRS_MODE_RSUB) {
-            Vec<CPL> t = load_vec<CPL>(a.b + o);
+            Vec<CPL> t = ldv<CPL, NC>(a.b + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         } else {
-            Vec<CPL> t = load_vec_rw<CPL>(a.y + o);
+            Vec<CPL> t = ldv_rw<CPL, NC>(a.y + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         }
         if (mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD)
-            row_accumulate<OP, CPL, false, Src, UNR>(a, src, lo, hi, ld, cofs, acc);
+            row_accumulate<OP, CPL, false, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
         else
-            row_accumulate<OP, CPL, true, Src, UNR>(a, src, lo, hi, ld, cofs, acc);
+            row_accumulate<OP, CPL, true, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
         Vec<CPL> out;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
@@ -212,18 +241,18 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
             store_vec<CPL>(a.seed_out + o, out);
         }
         if (a.dot) {   // (x_in ? x_in : x)_own . y  (x_in: e.g. BiCGStab's r0)
-            Vec<CPL> xo = load_vec<CPL>((a.x_in ? a.x_in : a.x) + o);
+            Vec<CPL> xo = ldv<CPL, NC>((a.x_in ? a.x_in : a.x) + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
         }
     } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
         // r = b - A x  (RSUB order: start at b, subtract in entry order)
-        Vec<CPL> bb = load_vec<CPL>(a.b + o);
+        Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
-        row_accumulate<OP, CPL, true, Src, UNR>(a, src, lo, hi, ld, cofs, acc);
+        row_accumulate<OP, CPL, true, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
         const double dd = __ldg(a.d + row);
-        Vec<CPL> xo = load_vec<CPL>(a.x + o);
+        Vec<CPL> xo = ldv<CPL, NC>(a.x + o);
         if constexpr (OP == OP_CHEB_FIRST) {
             const double dt = mul(dd, a.theta);
             Vec<CPL> r, dv;
@@ -247,11 +276,11 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-        row_accumulate<OP, CPL, false, Src, UNR>(a, src, lo, hi, ld, cofs, acc);   // tmp = A dv
+        row_accumulate<OP, CPL, false, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);   // tmp = A dv
         const double dd = __ldg(a.d + row);
-        Vec<CPL> r = load_vec<CPL>(a.r_in + o);
-        Vec<CPL> dv = load_vec<CPL>(a.x + o);
-        Vec<CPL> xo = load_vec_rw<CPL>(a.x_in + o);
+        Vec<CPL> r = ldv<CPL, NC>(a.r_in + o);
+        Vec<CPL> dv = ldv<CPL, NC>(a.x + o);
+        Vec<CPL> xo = ldv_rw<CPL, NC>(a.x_in + o);
         Vec<CPL> dvn;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
@@ -263,7 +292,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
         if (a.r_out) store_vec<CPL>(a.r_out + o, r);
         if (a.dv_out) store_vec<CPL>(a.dv_out + o, dvn);
         if (a.dot) {
-            Vec<CPL> bb = load_vec<CPL>(a.b + o);
+            Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
         }
