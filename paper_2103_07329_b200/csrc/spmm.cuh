@@ -104,16 +104,17 @@ __device__ __forceinline__ Vec<CPL> load_vec_cg(const double* p) {
     }
     return r;
 }
+// !NC: plain (L1-cached) loads -- coherent in the tail kernel because its
+// cluster barrier carries MEMBAR.GPU + CCTL.IVALL (L1 invalidate) in SASS.
 template <int CPL, bool NC>
 __device__ __forceinline__ Vec<CPL> ldv(const double* p) {
     if constexpr (NC) return load_vec<CPL>(p);
-    else return load_vec_cg<CPL>(p);          // L2 (coherent across the cluster)
+    else return load_vec_rw<CPL>(p);
 }
 // read-modify-write operands of a row (the thread that reads also writes)
 template <int CPL, bool NC>
 __device__ __forceinline__ Vec<CPL> ldv_rw(const double* p) {
-    if constexpr (NC) return load_vec_rw<CPL>(p);
-    else return load_vec_cg<CPL>(p);
+    return load_vec_rw<CPL>(p);
 }
 
 // Value of the gathered operand at column `col` (CPL columns at cofs).

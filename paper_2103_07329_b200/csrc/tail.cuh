@@ -7,8 +7,8 @@
 // same steps, same arithmetic, recorded from the schedule builder) on one
 // thread-block CLUSTER: the cluster's CTAs split each step's rows and meet at
 // a hardware cluster barrier (barrier.cluster arrive.release / wait.acquire)
-// between steps.  Vector operands are read with ld.global.cg so data written
-// by another CTA of the cluster in an earlier step is seen.
+// between steps.  The barrier's acquire invalidates L1 (CCTL.IVALL in SASS),
+// so plain loads see what other CTAs of the cluster wrote in earlier steps.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -64,7 +64,7 @@ __device__ __forceinline__ void tail_coarse(const TailStep& st, int m, int crank
         double acc = 0.0;
         if (ks < kpb)
             for (int64_t k = ks; k < st.nc; k += kpb)
-                acc = add(acc, mul(__ldg(st.inv + i * st.nc + k), __ldcg(st.cb + k * m + c)));
+                acc = add(acc, mul(__ldg(st.inv + i * st.nc + k), st.cb[k * m + c]));
         s_t[threadIdx.x] = acc;
         __syncthreads();
         if (threadIdx.x < m) {
