@@ -24,7 +24,7 @@ bool pdl_enabled() {
 
 void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 
-static int64_t g_tail_rows = 4096;
+static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
 static int g_prefetch = 0;   // measured slower (profiles/r01_ab_experiments.txt)
