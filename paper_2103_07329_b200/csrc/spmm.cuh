@@ -176,30 +176,32 @@ template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4, bool NC = true
 __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int64_t lo,
                                                int64_t hi, int64_t ld, int cofs,
                                                double (&acc)[CPL]) {
-    // Groups of UNR entries: all loads of a group (including a partial last
-    // group, predicated) are issued before the group is accumulated in entry
-    // order -- a 7-entry row costs two load rounds, not 1 + 3.
-    for (int64_t k = lo; k < hi; k += UNR) {
+    int64_t k = lo;
+    for (; k + UNR <= hi; k += UNR) {
         int64_t c[UNR];
         double v[UNR];
         Vec<CPL> g[UNR];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-            const bool on = k + u < hi;
-            c[u] = on ? src.col(k + u) : 0;
-            v[u] = on ? src.val(k + u) : 0.0;
+        for (int u = 0; u < UNR; ++u) { c[u] = src.col(k + u); v[u] = src.val(k + u); }
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL, NC>(a, c[u], ld, cofs);
+#pragma unroll
+        for (int u = 0; u < UNR; ++u)
+#pragma unroll
+            for (int i = 0; i < CPL; ++i) {
+                if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v[u], g[u].v[i]));
+                else acc[i] = add(acc[i], mul(v[u], g[u].v[i]));
+            }
+    }
+    for (; k < hi; ++k) {
+        const int64_t c0 = src.col(k);
+        const double v0 = src.val(k);
+        Vec<CPL> g0 = gather<OP, CPL, NC>(a, c0, ld, cofs);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v0, g0.v[i]));
+            else acc[i] = add(acc[i], mul(v0, g0.v[i]));
         }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
-            if (k + u < hi) g[u] = gather<OP, CPL, NC>(a, c[u], ld, cofs);
-#pragma unroll
-        for (int u = 0; u < UNR; ++u)
-            if (k + u < hi)
-#pragma unroll
-                for (int i = 0; i < CPL; ++i) {
-                    if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v[u], g[u].v[i]));
-                    else acc[i] = add(acc[i], mul(v[u], g[u].v[i]));
-                }
     }
 }
 
