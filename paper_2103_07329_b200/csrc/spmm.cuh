@@ -176,31 +176,33 @@ template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4, bool NC = true
 __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int64_t lo,
                                                int64_t hi, int64_t ld, int cofs,
                                                double (&acc)[CPL]) {
-    int64_t k = lo;
-    for (; k + UNR <= hi; k += UNR) {
-        int64_t c[UNR];
+    // Entries in groups of UNR: all loads of a group are issued before the
+    // group is accumulated in entry order.  The last, partial group loads
+    // entry `lo` in its empty slots (valid addresses, no branches) and only
+    // accumulates its live entries: a 7-entry row costs two dependent load
+    // rounds instead of 1 + 3.
+    const int klo = (int)lo, khi = (int)hi;
+    for (int k = klo; k < khi; k += UNR) {
+        int c[UNR];
         double v[UNR];
         Vec<CPL> g[UNR];
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) { c[u] = src.col(k + u); v[u] = src.val(k + u); }
+        for (int u = 0; u < UNR; ++u) {
+            const int kk = (k + u < khi) ? k + u : klo;
+            c[u] = (int)src.col(kk);
+            v[u] = src.val(kk);
+        }
 #pragma unroll
         for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL, NC>(a, c[u], ld, cofs);
 #pragma unroll
-        for (int u = 0; u < UNR; ++u)
+        for (int u = 0; u < UNR; ++u) {
+            if (k + u < khi) {
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) {
-                if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v[u], g[u].v[i]));
-                else acc[i] = add(acc[i], mul(v[u], g[u].v[i]));
+                for (int i = 0; i < CPL; ++i) {
+                    if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v[u], g[u].v[i]));
+                    else acc[i] = add(acc[i], mul(v[u], g[u].v[i]));
+                }
             }
-    }
-    for (; k < hi; ++k) {
-        const int64_t c0 = src.col(k);
-        const double v0 = src.val(k);
-        Vec<CPL> g0 = gather<OP, CPL, NC>(a, c0, ld, cofs);
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) {
-            if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v0, g0.v[i]));
-            else acc[i] = add(acc[i], mul(v0, g0.v[i]));
         }
     }
 }
