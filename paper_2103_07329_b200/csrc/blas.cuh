@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(kThreads, 4) vec_kernel(VArgs A, int64_t chunk
                 const int64_t i = base + rs + (int64_t)j * rpb;
                 if (i < r1) vec_load<OP>(A, i * m + c, i, L[j]);
             }
+            compiler_fence();
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 const int64_t i = base + rs + (int64_t)j * rpb;

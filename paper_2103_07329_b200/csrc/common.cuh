@@ -74,6 +74,10 @@ __device__ __forceinline__ void store_vec(double* p, const Vec<CPL>& a) {
     }
 }
 
+// Compiler-only memory fence: loads before it are issued before loads/uses
+// after it (keeps batches of independent loads together in SASS).
+__device__ __forceinline__ void compiler_fence() { asm volatile("" ::: "memory"); }
+
 // Programmatic dependent launch (PDL): every kernel waits for its stream
 // predecessor's memory before touching it, then lets its own successor start
 // launching.  Both are no-ops when the kernel was launched without the PDL

@@ -192,8 +192,11 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
             c[u] = (int)src.col(kk);
             v[u] = src.val(kk);
         }
+        compiler_fence();   // keep the group's loads issued together (the
+                            // scheduler otherwise interleaves them with uses)
 #pragma unroll
         for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL, NC>(a, c[u], ld, cofs);
+        compiler_fence();
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
             if (k + u < khi) {
