@@ -236,7 +236,8 @@ int  mrs_version(void);
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
  *   "spmm_wide" -1/0/1 long-row SpMM layout: auto (nnz/row >= 12), never, always
  *   "spmm_prefetch" 0/1 TMA bulk L2 prefetch of each SpMM chunk's streams
- *   "tail_rows" N  V-cycle levels with <= N rows run as one cluster kernel (0: off) */
+ *   "tail_rows" N  V-cycle levels with <= N rows run as one cluster kernel (0: off)
+ *   "spmm_stage" 0/1 chunk-staged SpMM (CSR segment copied to shared memory) */
 int  mrs_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

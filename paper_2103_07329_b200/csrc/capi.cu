@@ -85,6 +85,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_wide")) { set_spmm_wide((int)value); return MRS_OK; }
     if (!strcmp(key, "spmm_prefetch")) { set_spmm_prefetch((int)value); return MRS_OK; }
     if (!strcmp(key, "tail_rows")) { set_tail_rows(value); return MRS_OK; }
+    if (!strcmp(key, "spmm_stage")) { set_spmm_stage((int)value); return MRS_OK; }
     return MRS_ERR_ARG;
 }
 

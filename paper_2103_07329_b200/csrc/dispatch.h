@@ -48,6 +48,7 @@ int max_grid();
 void set_pdl(int on);
 void set_spmm_wide(int v);
 void set_spmm_prefetch(int v);
+void set_spmm_stage(int v);
 int spmm_prefetch_mode();
 int vec_op_k(int op);   // reduced values per column of a vector op (0 = none)
 

@@ -331,7 +331,35 @@ __device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[L
     finish_reduction(a.red, s_blk, M, M);
 }
 
-template <int M, int OP, typename Tv, typename Ti, bool WIDE = false>
+// Chunk staging (STAGE): a CTA copies its whole chunk's CSR segment (row
+// pointers, column indices, values: one contiguous range) into shared memory
+// with coalesced 16-byte loads issued as one batch, then computes the chunk's
+// rows from shared memory -- per chunk the dependent chain is bounds -> one
+// coalesced copy -> x gathers, instead of rp -> entries -> x per row pass.
+constexpr int kStageCap = 4096;      // entries per chunk stage
+
+template <typename Tv, typename Ti>
+__host__ __device__ constexpr size_t stage_smem_bytes() {
+    return (size_t)(kStageCap + 16) * (sizeof(Ti) + sizeof(Tv)) + 16 + (512 + 8) * sizeof(int32_t);
+}
+
+template <typename T>
+__device__ __forceinline__ void stage_copy(T* dst, const T* src, int64_t n_elems) {
+    // 16-byte chunks; `src` 16-byte aligned (caller aligns down)
+    constexpr int E = 16 / sizeof(T);
+    const int nch = (int)((n_elems + E - 1) / E);
+    const uint4* s = reinterpret_cast<const uint4*>(src);
+    uint4* d = reinterpret_cast<uint4*>(dst);
+    int t = threadIdx.x;
+    for (; t + 3 * kThreads < nch; t += 4 * kThreads) {
+        uint4 a0 = __ldg(s + t), a1 = __ldg(s + t + kThreads), a2 = __ldg(s + t + 2 * kThreads),
+              a3 = __ldg(s + t + 3 * kThreads);
+        d[t] = a0; d[t + kThreads] = a1; d[t + 2 * kThreads] = a2; d[t + 3 * kThreads] = a3;
+    }
+    for (; t < nch; t += kThreads) d[t] = __ldg(s + t);
+}
+
+template <int M, int OP, typename Tv, typename Ti, bool WIDE = false, bool STAGE = false>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
@@ -350,6 +378,30 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
             // TMA bulk L2 prefetch of this chunk's streams (this chunk is
             // first touched now; the next chunk of this CTA is stride away)
             if (threadIdx.x < 32) prefetch_chunk<Tv, Ti>(a, r0, r1, M);
+        }
+        if constexpr (STAGE) {
+            extern __shared__ __align__(16) unsigned char smem[];
+            const int64_t k0 = __ldg(a.rp + r0), k1 = __ldg(a.rp + r1);
+            constexpr int EI = 16 / sizeof(Ti), EV = 16 / sizeof(Tv);
+            const int64_t ki = k0 & ~(int64_t)(EI - 1), kv = k0 & ~(int64_t)(EV - 1);
+            if (k1 - ki <= kStageCap && k1 - kv <= kStageCap) {
+                Ti* s_ci = reinterpret_cast<Ti*>(smem);
+                Tv* s_v = reinterpret_cast<Tv*>(smem + (size_t)(kStageCap + 16) * sizeof(Ti));
+                int32_t* s_rp = reinterpret_cast<int32_t*>(smem + (size_t)(kStageCap + 16) *
+                                                                  (sizeof(Ti) + sizeof(Tv)) + 16);
+                stage_copy(s_ci, reinterpret_cast<const Ti*>(a.ci) + ki, k1 - ki);
+                stage_copy(s_v, reinterpret_cast<const Tv*>(a.vals) + kv, k1 - kv);
+                for (int t = threadIdx.x; t <= (int)(r1 - r0); t += kThreads) s_rp[t] = __ldg(a.rp + r0 + t);
+                __syncthreads();
+                const SSrc<Tv, Ti> ss{s_ci, s_v, ki, kv};
+                for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB) {
+                    const int j = (int)(row - r0);
+                    do_row<OP, CPL, SSrc<Tv, Ti>, L::UNR>(a, ss, row, s_rp[j], s_rp[j + 1], M, cofs,
+                                                         dotp);
+                }
+                __syncthreads();
+                continue;
+            }
         }
         for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
             do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src, row, __ldg(a.rp + row),

@@ -18,9 +18,14 @@ def main():
     ap.add_argument("--mode", default="rsub", choices=["assign", "rsub"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--f32", action="store_true")
+    ap.add_argument("--knob", action="append", default=[], help="name=value (mrs_set_option)")
     a = ap.parse_args()
     import numpy as np
     import torch
+    from paper_2103_07329_b200 import _lib
+    for kv in a.knob:
+        k, v = kv.split("=")
+        _lib.set_option(k, int(v))
     from paper_2103_07329_b200 import gen_poisson3d, gen_random_sdd, kernels as K
     if a.matrix == "c5":
         A = gen_random_sdd()
