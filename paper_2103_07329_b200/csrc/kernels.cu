@@ -27,7 +27,7 @@ void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
-static int g_stage = 1;
+static int g_stage = 0;   // no gain measured (profiles/r01_ab_experiments.txt)
 int spmm_stage_mode() { return g_stage; }
 void set_spmm_stage(int v) { g_stage = v ? 1 : 0; }
 static int g_prefetch = 0;   // measured slower (profiles/r01_ab_experiments.txt)

@@ -113,8 +113,6 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB, sm); return cudaGetLastError();
         case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB, sm); return cudaGetLastError();
         case 16: go(spmm_kernel<16, OP, Tv, Ti, false, true>, Lay<16>::RPB, sm); return cudaGetLastError();
-        case 32: go(spmm_kernel<32, OP, Tv, Ti, false, true>, Lay<32>::RPB, sm); return cudaGetLastError();
-        case 64: go(spmm_kernel<64, OP, Tv, Ti, false, true>, Lay<64>::RPB, sm); return cudaGetLastError();
         default: break;
         }
     }
