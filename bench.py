@@ -249,28 +249,32 @@ def spmm_sweep(torch, K, quick: bool):
     flush_sink = torch.empty((), dtype=torch.float64, device="cuda")
     for vdt in ("f64", "f32"):
         vals = A.values if vdt == "f64" else A.values.astype("float32")
-        D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols)
-        for m in ms_list:
-            x = torch.rand(A.ncols, m, dtype=torch.float64, device="cuda")
-            y = torch.empty(A.nrows, m, dtype=torch.float64, device="cuda")
-            for _ in range(3):
-                K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
-            times = []
-            for _ in range(10):
-                torch.sum(flush_buf, dim=0, out=flush_sink)
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
-                e1.record()
-                torch.cuda.synchronize()
-                times.append(e0.elapsed_time(e1) * 1e-3)
-            t = sorted(times)[len(times) // 2]
-            vb = 8 if vdt == "f64" else 4
-            byts = A.nnz * (vb + 4) + (A.nrows + 1) * 4 + 2 * A.nrows * m * 8
-            out.append({"m": m, "values": vdt, "idx": "u32", "us": t * 1e6,
-                        "GBps": byts / t / 1e9, "frac": byts / t / 1e9 / peak})
-            del x, y
-        del D
+        for idx in ("u32", "u16slab"):
+            D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols, slab=idx == "u16slab")
+            ib = D.col_idx.element_size()
+            nslab = 0 if D.slab_base is None else D.slab_base.numel()
+            for m in ms_list:
+                x = torch.rand(A.ncols, m, dtype=torch.float64, device="cuda")
+                y = torch.empty(A.nrows, m, dtype=torch.float64, device="cuda")
+                for _ in range(3):
+                    K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
+                times = []
+                for _ in range(10):
+                    torch.sum(flush_buf, dim=0, out=flush_sink)
+                    e0 = torch.cuda.Event(enable_timing=True)
+                    e1 = torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
+                    e1.record()
+                    torch.cuda.synchronize()
+                    times.append(e0.elapsed_time(e1) * 1e-3)
+                t = sorted(times)[len(times) // 2]
+                vb = 8 if vdt == "f64" else 4
+                byts = A.nnz * (vb + ib) + (A.nrows + 1) * 4 + 4 * nslab + 2 * A.nrows * m * 8
+                out.append({"m": m, "values": vdt, "idx": idx, "us": t * 1e6,
+                            "GBps": byts / t / 1e9, "frac": byts / t / 1e9 / peak})
+                del x, y
+            del D
     return {"n": A.nrows, "nnz": A.nnz, "gen_s": gen_s, "points": out}
 
 

@@ -63,6 +63,11 @@ typedef struct {
     const void* values;       /* nnz entries of val_bytes */
     int32_t idx_bytes;        /* 1, 2 or 4 */
     int32_t val_bytes;        /* 4 or 8 */
+    /* Slab-compressed 16-bit indices (optional, idx_bytes == 2): the column of
+     * an entry in row i is slab_base[i >> slab_shift] + col_idx[k]. */
+    const int32_t* slab_base; /* NULL: plain indices */
+    int32_t slab_shift;
+    int32_t pad_;
 } mrs_csr;
 
 /* Host CSR (the reference CsrBlock layout, core.py:146-254). */
@@ -73,6 +78,9 @@ typedef struct {
     const void* values;
     int32_t idx_bytes;
     int32_t val_bytes;
+    const int32_t* slab_base; /* optional slab-relative 16-bit indices (see mrs_csr) */
+    int32_t slab_shift;
+    int32_t pad_;
 } mrs_host_csr;
 
 /* ---- 1. kernel plugin (src/kernels/__init__.py:27-41) ------------------ */
@@ -234,10 +242,8 @@ const char* mrs_status_string(int32_t status);
 int  mrs_version(void);
 /* Tuning knobs, read when a plan captures its graph:
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
- *   "spmm_wide" -1/0/1 long-row SpMM layout: auto (nnz/row >= 12), never, always
- *   "spmm_prefetch" 0/1 TMA bulk L2 prefetch of each SpMM chunk's streams
  *   "tail_rows" N  V-cycle levels with <= N rows run as one cluster kernel (0: off)
- *   "spmm_stage" 0/1 chunk-staged SpMM (CSR segment copied to shared memory) */
+ * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

@@ -26,13 +26,15 @@ SMOOTH_JACOBI, SMOOTH_CHEBYSHEV = 0, 1
 class mrs_csr(C.Structure):
     _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
-                ("idx_bytes", C.c_int32), ("val_bytes", C.c_int32)]
+                ("idx_bytes", C.c_int32), ("val_bytes", C.c_int32),
+                ("slab_base", C.c_void_p), ("slab_shift", C.c_int32), ("pad_", C.c_int32)]
 
 
 class mrs_host_csr(C.Structure):
     _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
-                ("idx_bytes", C.c_int32), ("val_bytes", C.c_int32)]
+                ("idx_bytes", C.c_int32), ("val_bytes", C.c_int32),
+                ("slab_base", C.c_void_p), ("slab_shift", C.c_int32), ("pad_", C.c_int32)]
 
 
 class mrs_smoother(C.Structure):
@@ -154,8 +156,10 @@ def check(code: int, what: str = "mrsolve_b200 call"):
     raise DeviceError(msg, code)
 
 
-def host_csr(blk, keep: list) -> mrs_host_csr:
-    """mrs_host_csr view of a CsrBlock-like object (arrays kept alive in `keep`)."""
+def host_csr(blk, keep: list, slab=False) -> mrs_host_csr:
+    """mrs_host_csr view of a CsrBlock-like object (arrays kept alive in `keep`).
+    ``slab=True``: store 32-bit column indices as slab-relative 16-bit ones
+    when every slab's column span fits (core.slab_compress)."""
     import numpy as np
     rp = np.ascontiguousarray(blk.row_ptr, dtype=np.int64)
     ci = np.ascontiguousarray(blk.col_idx)
@@ -164,6 +168,15 @@ def host_csr(blk, keep: list) -> mrs_host_csr:
     v = np.ascontiguousarray(blk.values)
     if v.dtype not in (np.float32, np.float64):
         v = v.astype(np.float64)
+    base_p, shift = None, 0
+    if slab and ci.dtype == np.uint32:
+        from .core import slab_compress
+        sc = slab_compress(rp, ci)
+        if sc is not None:
+            ci, base, shift = sc
+            keep.append(base)
+            base_p = base.ctypes.data
     keep.extend([rp, ci, v])
     return mrs_host_csr(int(blk.nrows), int(blk.ncols), int(rp[-1]), rp.ctypes.data,
-                        ci.ctypes.data, v.ctypes.data, ci.dtype.itemsize, v.dtype.itemsize)
+                        ci.ctypes.data, v.ctypes.data, ci.dtype.itemsize, v.dtype.itemsize,
+                        base_p, shift, 0)

@@ -82,10 +82,7 @@ int mrs_version(void) { return 1; }
 int mrs_set_option(const char* key, int64_t value) {
     if (!key) return MRS_ERR_ARG;
     if (!strcmp(key, "pdl")) { set_pdl((int)value); return MRS_OK; }
-    if (!strcmp(key, "spmm_wide")) { set_spmm_wide((int)value); return MRS_OK; }
-    if (!strcmp(key, "spmm_prefetch")) { set_spmm_prefetch((int)value); return MRS_OK; }
     if (!strcmp(key, "tail_rows")) { set_tail_rows(value); return MRS_OK; }
-    if (!strcmp(key, "spmm_stage")) { set_spmm_stage((int)value); return MRS_OK; }
     return MRS_ERR_ARG;
 }
 
@@ -120,6 +117,11 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_
     D.ci = const_cast<void*>(A->col_idx);
     D.v = const_cast<void*>(A->values);
     D.ib = A->idx_bytes; D.vb = A->val_bytes;
+    if (A->slab_base) {
+        if (A->idx_bytes != 2 || A->slab_shift < 0 || A->slab_shift > 30) return MRS_ERR_ARG;
+        D.slab_base = const_cast<int32_t*>(A->slab_base);
+        D.slab_shift = A->slab_shift;
+    }
     SpArgs a;
     memset(&a, 0, sizeof(a));
     a.x = x; a.y = y; a.b = b; a.mode = mode;

@@ -17,13 +17,18 @@ struct Halo;
 struct DevCsr {
     int64_t nrows = 0, ncols = 0, nnz = 0;
     const Halo* halo = nullptr;   // multi-GPU: exchange of the gathered operand before use
+    int32_t* slab_base = nullptr; // slab-relative 16-bit column indices (optional)
+    int slab_shift = 0;
     int32_t* rp = nullptr;
     void* ci = nullptr;
     void* v = nullptr;
     int ib = 4, vb = 8;
     bool present() const { return rp != nullptr; }
     // algorithmic bytes of one pass over the CSR arrays
-    double bytes() const { return (double)nnz * (ib + vb) + (double)(nrows + 1) * 4.0; }
+    double bytes() const {
+        double sb = slab_base ? (double)(((nrows - 1) >> slab_shift) + 1) * 4.0 : 0.0;
+        return (double)nnz * (ib + vb) + (double)(nrows + 1) * 4.0 + sb;
+    }
 };
 
 // SpMM-family launch (OP = SpOp).  a.rp/ci/vals/nrows are filled from A.
@@ -46,10 +51,6 @@ int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);
 int max_grid();
 void set_pdl(int on);
-void set_spmm_wide(int v);
-void set_spmm_prefetch(int v);
-void set_spmm_stage(int v);
-int spmm_prefetch_mode();
 int vec_op_k(int op);   // reduced values per column of a vector op (0 = none)
 
 }  // namespace mrs

@@ -27,15 +27,6 @@ void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
-static int g_stage = 0;   // no gain measured (profiles/r01_ab_experiments.txt)
-int spmm_stage_mode() { return g_stage; }
-void set_spmm_stage(int v) { g_stage = v ? 1 : 0; }
-static int g_prefetch = 0;   // measured slower (profiles/r01_ab_experiments.txt)
-int spmm_prefetch_mode() { return g_prefetch; }
-void set_spmm_prefetch(int v) { g_prefetch = v ? 1 : 0; }
-static int g_wide = 0;   // wide layout measured slower on C2/C3 (profiles/r01_ab_experiments.txt)
-int spmm_wide_mode() { return g_wide; }
-void set_spmm_wide(int v) { g_wide = v < 0 ? -1 : (v ? 1 : 0); }
 
 int spmm_grid(int64_t nrows, int64_t m) {   // upper bound (scratch sizing)
     (void)nrows; (void)m;
@@ -51,7 +42,8 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
                         bool generic) {
     a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.nrows = A.nrows; a.m = m; a.nnz_hint = A.nnz;
     a.ncols_hint = A.ncols;
-    a.prefetch = spmm_prefetch_mode();
+    a.slab_base = A.slab_base;
+    a.slab_shift = A.slab_shift;
     if (A.nrows == 0) return cudaSuccess;
     if (A.vb == 8) return launch_spmm_f64(op, A, a, m, s, generic);
     if (A.vb == 4) return launch_spmm_f32(op, A, a, m, s, generic);

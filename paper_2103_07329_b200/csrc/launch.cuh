@@ -9,11 +9,6 @@
 
 namespace mrs {
 
-int spmm_wide_mode();   // -1 auto (by nnz/row), 0 never, 1 always (mrs_set_option)
-int spmm_stage_mode();  // 1: chunk-staged SpMM (shared-memory CSR segments)
-
-// dynamic shared memory of the next launch_ex (set around staged launches)
-inline thread_local size_t g_launch_smem = 0;
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
@@ -21,7 +16,7 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, A
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = g_launch_smem;
+    cfg.dynamicSmemBytes = 0;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -66,56 +61,22 @@ inline void wave_grid(const void* fn, int64_t nrows, int64_t rows_per_pass, int&
 template <int OP, typename Tv, typename Ti>
 inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     int g;
-    auto go = [&](auto kern, int64_t rpp, size_t smem = 0) {
+    auto go = [&](auto kern, int64_t rpp) {
         // Balanced one wave: every CTA gets the same number of passes (the
         // slowest CTA sets the kernel time), in chunks of <= ~512 rows strided
         // over the grid (L1 reuse inside a chunk, L2-resident band across).
-        const int64_t cap = (int64_t)blocks_per_sm((const void*)kern, smem) * num_sms();
+        const int64_t cap = (int64_t)blocks_per_sm((const void*)kern) * num_sms();
         const int64_t P = (a.nrows + rpp - 1) / rpp;             // passes in total
         const int64_t ppc = (P + cap - 1) / cap;                  // passes per CTA
-        int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
-        if (smem) {
-            // staged: a chunk's entries must fit the stage (25% headroom)
-            const double avg = a.nrows ? (double)a.nnz_hint / (double)a.nrows : 1.0;
-            int64_t fit = (int64_t)(kStageCap / (rpp * (avg > 1.0 ? avg : 1.0) * 1.25));
-            if (fit < 1) fit = 1;
-            if (fit < pmax) pmax = fit;
-        }
+        const int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
         const int64_t sp = ppc < pmax ? ppc : pmax;               // passes per chunk
         const int64_t nchunks = (P + sp - 1) / sp;
         const int64_t cpc = (nchunks + cap - 1) / cap;            // chunks per CTA
         g = (int)((nchunks + cpc - 1) / cpc);
         if (g < 1) g = 1;
         a.chunk = rpp * sp;
-        g_launch_smem = smem;
         (void)launch_ex(kern, g, s, a);
-        g_launch_smem = 0;
     };
-    // long rows (AMG coarse operators): the wide layout (spmm.cuh Lay)
-    const int wide_knob = spmm_wide_mode();
-    const bool wide = !generic && (m == 2 || m == 4 || m == 8 || m == 16) &&
-                      (wide_knob == 1 || (wide_knob < 0 && a.nrows > 0 &&
-                                          a.nnz_hint >= 12 * a.nrows));
-    if (wide) {
-        switch (m) {
-        case 2: go(spmm_kernel<2, OP, Tv, Ti, true>, Lay<2, true>::RPB); break;
-        case 4: go(spmm_kernel<4, OP, Tv, Ti, true>, Lay<4, true>::RPB); break;
-        case 8: go(spmm_kernel<8, OP, Tv, Ti, true>, Lay<8, true>::RPB); break;
-        case 16: go(spmm_kernel<16, OP, Tv, Ti, true>, Lay<16, true>::RPB); break;
-        }
-        return cudaGetLastError();
-    }
-    if (!generic && spmm_stage_mode()) {
-        constexpr size_t sm = stage_smem_bytes<Tv, Ti>();
-        switch (m) {
-        case 1: go(spmm_kernel<1, OP, Tv, Ti, false, true>, Lay<1>::RPB, sm); return cudaGetLastError();
-        case 2: go(spmm_kernel<2, OP, Tv, Ti, false, true>, Lay<2>::RPB, sm); return cudaGetLastError();
-        case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB, sm); return cudaGetLastError();
-        case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB, sm); return cudaGetLastError();
-        case 16: go(spmm_kernel<16, OP, Tv, Ti, false, true>, Lay<16>::RPB, sm); return cudaGetLastError();
-        default: break;
-        }
-    }
     switch (generic ? 0 : m) {
     case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
     case 2: go(spmm_kernel<2, OP, Tv, Ti>, Lay<2>::RPB); break;

@@ -715,6 +715,14 @@ int upload_csr(const mrs_host_csr* h, DevCsr& d, std::vector<void*>& owned) {
         MRS_CUDA_OK(cudaMemcpy(d.ci, h->col_idx, (size_t)h->nnz * d.ib, cudaMemcpyHostToDevice));
     }
     MRS_CUDA_OK(cudaMemcpy(d.v, h->values, (size_t)h->nnz * d.vb, cudaMemcpyHostToDevice));
+    if (h->slab_base) {
+        if (h->idx_bytes != 2 || h->slab_shift < 0 || h->slab_shift > 30) return MRS_ERR_ARG;
+        const int64_t ns = ((h->nrows - 1) >> h->slab_shift) + 1;
+        d.slab_base = dalloc<int32_t>((size_t)ns, owned);
+        if (!d.slab_base) return MRS_ERR_ALLOC;
+        d.slab_shift = h->slab_shift;
+        MRS_CUDA_OK(cudaMemcpy(d.slab_base, h->slab_base, (size_t)ns * 4, cudaMemcpyHostToDevice));
+    }
     return MRS_OK;
 }
 
@@ -728,6 +736,7 @@ int host_diag(const mrs_host_csr* h, std::vector<double>& d) {
             int64_t c = h->idx_bytes == 4 ? ((const uint32_t*)h->col_idx)[k]
                       : h->idx_bytes == 2 ? ((const uint16_t*)h->col_idx)[k]
                                           : ((const uint8_t*)h->col_idx)[k];
+            if (h->slab_base) c += h->slab_base[i >> h->slab_shift];
             if (c == i) {
                 d[i] = h->val_bytes == 8 ? ((const double*)h->values)[k]
                                          : (double)((const float*)h->values)[k];

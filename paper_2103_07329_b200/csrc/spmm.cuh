@@ -28,15 +28,11 @@
 
 namespace mrs {
 
-// WIDE: long-row layout (AMG coarse operators, ~20-40 nnz/row): one column
-// per lane (LPR = M) and 8 entries in flight per lane, so a row's dependent
-// load chain is half as long; the default packs 2 columns per lane (16-byte
-// accesses) with 4 entries in flight.  Accumulation order is the same.
-template <int M, bool WIDE = false> struct Lay {
-    static constexpr int CPL = WIDE ? 1 : ((M == 1) ? 1 : (M <= 16 ? 2 : M / 8));
+template <int M> struct Lay {
+    static constexpr int CPL = (M == 1) ? 1 : (M <= 16 ? 2 : M / 8);
     static constexpr int LPR = M / CPL;
     static constexpr int RPB = kThreads / LPR;     // rows per CTA pass
-    static constexpr int UNR = WIDE ? 8 : 4;       // entries in flight per lane
+    static constexpr int UNR = 4;                  // entries in flight per lane
 };
 
 // Kernel operation selector.
@@ -75,8 +71,9 @@ struct SpArgs {
     double* seed_out;
     int64_t chunk;          // rows per CTA (contiguous range, multiple of RPB)
     int64_t nnz_hint;       // matrix nnz (layout choice)
-    int64_t ncols_hint;     // matrix columns (square: own x rows are prefetchable)
-    int prefetch;           // bulk-prefetch each chunk's streams into L2
+    const int32_t* slab_base;  // non-null: column = slab_base[row >> slab_shift] + col16
+    int slab_shift;
+    int64_t ncols_hint;     // matrix columns
     RedArgs red;
 };
 
@@ -123,44 +120,20 @@ __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t
     return ldv<CPL, NC>(a.x + col * ld + cofs);
 }
 
-// cp.async.bulk.prefetch.L2: one instruction pulls a contiguous byte range
-// into L2 (16-byte aligned, size a multiple of 16).
-__device__ __forceinline__ void bulk_prefetch_l2(const void* p, size_t bytes) {
-    uintptr_t a0 = (uintptr_t)p & ~(uintptr_t)15;
-    uintptr_t a1 = ((uintptr_t)p + bytes + 15) & ~(uintptr_t)15;
-    while (a1 > a0) {
-        const uint32_t n = (uint32_t)min((uintptr_t)(1u << 20), a1 - a0);
-        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(n) : "memory");
-        a0 += n;
-    }
-}
-
-// Prefetch the streams of rows [r0, r1): row pointers, CSR entries, and the
-// row-indexed vector operands (b / y / own x rows).  Lanes 0..3 of warp 0
-// split the work.
-template <typename Tv, typename Ti>
-__device__ __forceinline__ void prefetch_chunk(const SpArgs& a, int64_t r0, int64_t r1, int64_t ld) {
-    const int lane = threadIdx.x;
-    if (lane == 0) bulk_prefetch_l2(a.rp + r0, (size_t)(r1 - r0 + 1) * sizeof(int32_t));
-    if (lane == 1 || lane == 2) {
-        const int64_t k0 = __ldg(a.rp + r0), k1 = __ldg(a.rp + r1);
-        if (lane == 1) bulk_prefetch_l2(reinterpret_cast<const Ti*>(a.ci) + k0, (size_t)(k1 - k0) * sizeof(Ti));
-        else bulk_prefetch_l2(reinterpret_cast<const Tv*>(a.vals) + k0, (size_t)(k1 - k0) * sizeof(Tv));
-    }
-    const size_t vb = (size_t)(r1 - r0) * ld * sizeof(double);
-    if (lane == 3 && a.b) bulk_prefetch_l2(a.b + r0 * ld, vb);
-    if (lane == 4 && a.x && a.nrows == a.ncols_hint) bulk_prefetch_l2(a.x + r0 * ld, vb);
-    if (lane == 5 && a.mode != 0 && a.y && (a.mode == MRS_MODE_ADD || a.mode == MRS_MODE_SUB))
-        bulk_prefetch_l2(a.y + r0 * ld, vb);
-}
-
 // Where a row's (column, value) entries come from: global memory (read-only
 // path) or a shared-memory copy (tail kernel).
 template <typename Tv, typename Ti> struct GSrc {
     const Ti* __restrict__ ci;
     const Tv* __restrict__ v;
-    __device__ __forceinline__ int64_t col(int64_t k) const { return (int64_t)__ldg(ci + k); }
+    int64_t base = 0;      // slab-compressed indices: column = base(row) + ci
+    __device__ __forceinline__ int64_t col(int64_t k) const { return base + (int64_t)__ldg(ci + k); }
     __device__ __forceinline__ double val(int64_t k) const { return widen(__ldg(v + k)); }
+    // the row's view: slab base of `row` (16-bit slab-relative columns)
+    __device__ __forceinline__ GSrc at_row(const SpArgs& a, int64_t row) const {
+        GSrc r = *this;
+        if (a.slab_base) r.base = __ldg(a.slab_base + (row >> a.slab_shift));
+        return r;
+    }
 };
 template <typename Tv, typename Ti> struct SSrc {
     const Ti* ci;          // shared memory; entry k lives at ci[k - ci_off]
@@ -307,9 +280,9 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t 
 
 // CTA-level fixed-shape reduction of the fused-dot partials (warp xor tree
 // over row groups, then warps in order), finished by finish_reduction.
-template <int M, bool WIDE>
-__device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[Lay<M, WIDE>::CPL]) {
-    constexpr int CPL = Lay<M, WIDE>::CPL, LPR = Lay<M, WIDE>::LPR;
+template <int M>
+__device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[Lay<M>::CPL]) {
+    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR;
     __shared__ double s_w[kThreads / 32][M];
     __shared__ double s_blk[M];
 #pragma unroll
@@ -331,39 +304,11 @@ __device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[L
     finish_reduction(a.red, s_blk, M, M);
 }
 
-// Chunk staging (STAGE): a CTA copies its whole chunk's CSR segment (row
-// pointers, column indices, values: one contiguous range) into shared memory
-// with coalesced 16-byte loads issued as one batch, then computes the chunk's
-// rows from shared memory -- per chunk the dependent chain is bounds -> one
-// coalesced copy -> x gathers, instead of rp -> entries -> x per row pass.
-constexpr int kStageCap = 4096;      // entries per chunk stage
-
-template <typename Tv, typename Ti>
-__host__ __device__ constexpr size_t stage_smem_bytes() {
-    return (size_t)(kStageCap + 16) * (sizeof(Ti) + sizeof(Tv)) + 16 + (512 + 8) * sizeof(int32_t);
-}
-
-template <typename T>
-__device__ __forceinline__ void stage_copy(T* dst, const T* src, int64_t n_elems) {
-    // 16-byte chunks; `src` 16-byte aligned (caller aligns down)
-    constexpr int E = 16 / sizeof(T);
-    const int nch = (int)((n_elems + E - 1) / E);
-    const uint4* s = reinterpret_cast<const uint4*>(src);
-    uint4* d = reinterpret_cast<uint4*>(dst);
-    int t = threadIdx.x;
-    for (; t + 3 * kThreads < nch; t += 4 * kThreads) {
-        uint4 a0 = __ldg(s + t), a1 = __ldg(s + t + kThreads), a2 = __ldg(s + t + 2 * kThreads),
-              a3 = __ldg(s + t + 3 * kThreads);
-        d[t] = a0; d[t + kThreads] = a1; d[t + 2 * kThreads] = a2; d[t + 3 * kThreads] = a3;
-    }
-    for (; t < nch; t += kThreads) d[t] = __ldg(s + t);
-}
-
-template <int M, int OP, typename Tv, typename Ti, bool WIDE = false, bool STAGE = false>
+template <int M, int OP, typename Tv, typename Ti>
 __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
-    using L = Lay<M, WIDE>;
+    using L = Lay<M>;
     constexpr int CPL = L::CPL, LPR = L::LPR, RPB = L::RPB;
     const int lane = threadIdx.x % LPR;
     const int cofs = lane * CPL;
@@ -374,40 +319,11 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
          r0 += (int64_t)gridDim.x * a.chunk) {
         const int64_t r1 = min(r0 + a.chunk, a.nrows);
-        if (a.prefetch) {
-            // TMA bulk L2 prefetch of this chunk's streams (this chunk is
-            // first touched now; the next chunk of this CTA is stride away)
-            if (threadIdx.x < 32) prefetch_chunk<Tv, Ti>(a, r0, r1, M);
-        }
-        if constexpr (STAGE) {
-            extern __shared__ __align__(16) unsigned char smem[];
-            const int64_t k0 = __ldg(a.rp + r0), k1 = __ldg(a.rp + r1);
-            constexpr int EI = 16 / sizeof(Ti), EV = 16 / sizeof(Tv);
-            const int64_t ki = k0 & ~(int64_t)(EI - 1), kv = k0 & ~(int64_t)(EV - 1);
-            if (k1 - ki <= kStageCap && k1 - kv <= kStageCap) {
-                Ti* s_ci = reinterpret_cast<Ti*>(smem);
-                Tv* s_v = reinterpret_cast<Tv*>(smem + (size_t)(kStageCap + 16) * sizeof(Ti));
-                int32_t* s_rp = reinterpret_cast<int32_t*>(smem + (size_t)(kStageCap + 16) *
-                                                                  (sizeof(Ti) + sizeof(Tv)) + 16);
-                stage_copy(s_ci, reinterpret_cast<const Ti*>(a.ci) + ki, k1 - ki);
-                stage_copy(s_v, reinterpret_cast<const Tv*>(a.vals) + kv, k1 - kv);
-                for (int t = threadIdx.x; t <= (int)(r1 - r0); t += kThreads) s_rp[t] = __ldg(a.rp + r0 + t);
-                __syncthreads();
-                const SSrc<Tv, Ti> ss{s_ci, s_v, ki, kv};
-                for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB) {
-                    const int j = (int)(row - r0);
-                    do_row<OP, CPL, SSrc<Tv, Ti>, L::UNR>(a, ss, row, s_rp[j], s_rp[j + 1], M, cofs,
-                                                         dotp);
-                }
-                __syncthreads();
-                continue;
-            }
-        }
         for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
-            do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src, row, __ldg(a.rp + row),
+            do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src.at_row(a, row), row, __ldg(a.rp + row),
                                                   __ldg(a.rp + row + 1), M, cofs, dotp);
     }
-    if (a.dot) spmm_block_dot<M, WIDE>(a, dotp);
+    if (a.dot) spmm_block_dot<M>(a, dotp);
 }
 
 // Generic m (any value, any layout): one thread per (row, column), thread
@@ -426,7 +342,8 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
              r0 += (int64_t)gridDim.x * a.chunk) {
             const int64_t r1 = min(r0 + a.chunk, a.nrows);
             for (int64_t row = r0 + threadIdx.x / m; row < r1; row += rpb)
-                do_row<OP, 1>(a, src, row, __ldg(a.rp + row), __ldg(a.rp + row + 1), m, c, dotp);
+                do_row<OP, 1>(a, src.at_row(a, row), row, __ldg(a.rp + row), __ldg(a.rp + row + 1), m,
+                              c, dotp);
         }
     }
     {

@@ -39,7 +39,7 @@ __device__ __forceinline__ void tail_rows(const SpArgs& a, int crank, int csize)
     double dotp[CPL];
     for (int64_t row = (int64_t)crank * RPB + threadIdx.x / LPR; row < a.nrows;
          row += (int64_t)csize * RPB)
-        do_row<OP, CPL, GSrc<Tv, Ti>, 4, false>(a, src, row, __ldg(a.rp + row),
+        do_row<OP, CPL, GSrc<Tv, Ti>, 4, false>(a, src.at_row(a, row), row, __ldg(a.rp + row),
                                                 __ldg(a.rp + row + 1), M, cofs, dotp);
 }
 

@@ -68,23 +68,36 @@ def _ck(code, what):
 class DeviceCsr:
     """A CSR block resident on the GPU (int32 row pointers)."""
 
-    def __init__(self, row_ptr, col_idx, values, nrows, ncols, device=None):
+    def __init__(self, row_ptr, col_idx, values, nrows, ncols, device=None, slab=False):
+        """``slab=True``: 32-bit columns stored as slab-relative 16-bit ones
+        when they fit (core.slab_compress) -- 2 bytes less per nonzero."""
         dev = device or torch.device("cuda", torch.cuda.current_device())
         self.row_ptr = torch.as_tensor(np.asarray(row_ptr, dtype=np.int64)).to(torch.int32).to(dev)
         ci = np.asarray(col_idx)
         if ci.dtype not in (np.uint8, np.uint16, np.uint32):
             ci = ci.astype(np.uint32)
+        self.slab_base, self.slab_shift = None, 0
+        if slab and ci.dtype == np.uint32:
+            from .core import slab_compress
+            sc = slab_compress(row_ptr, ci)
+            if sc is not None:
+                ci, base, self.slab_shift = sc
+                self.slab_base = torch.from_numpy(base).to(dev)
         self.col_idx = torch.from_numpy(ci.copy()).to(dev)
         self.values = torch.as_tensor(np.asarray(values)).to(dev)
         self.nrows, self.ncols = int(nrows), int(ncols)
         self.nnz = int(self.col_idx.numel())
 
     @classmethod
-    def from_block(cls, blk, device=None):
-        return cls(blk.row_ptr, blk.col_idx, blk.values, blk.nrows, blk.ncols, device)
+    def from_block(cls, blk, device=None, slab=False):
+        return cls(blk.row_ptr, blk.col_idx, blk.values, blk.nrows, blk.ncols, device, slab)
 
     def view(self) -> _lib.mrs_csr:
-        return _csr_view(self.row_ptr, self.col_idx, self.values, self.nrows, self.ncols)
+        v = _csr_view(self.row_ptr, self.col_idx, self.values, self.nrows, self.ncols)
+        if self.slab_base is not None:
+            v.slab_base = self.slab_base.data_ptr()
+            v.slab_shift = self.slab_shift
+        return v
 
 
 def _csr_view(row_ptr, col_idx, values, nrows, ncols):

@@ -85,6 +85,9 @@ def _smoother(plist) -> _lib.mrs_smoother:
 class DevicePlan:
     """One uploaded solver instance for a fixed RHS count m (owns a C plan)."""
 
+    #: store 32-bit level indices as slab-relative 16-bit ones where they fit
+    compress_indices = True
+
     def __init__(self, desc: _lib.mrs_plan_desc, levels, inv, method_name: str, dist=None):
         self.L = _lib.lib()
         self.desc = desc
@@ -107,9 +110,10 @@ class DevicePlan:
                             f"halo level {l}/{which}")
             for l, (A, P, R, bounds) in enumerate(levels):
                 keep: list = []
-                a = _lib.host_csr(A, keep)
-                p = _lib.host_csr(P, keep) if P is not None else None
-                r = _lib.host_csr(R, keep) if R is not None else None
+                sl = DevicePlan.compress_indices
+                a = _lib.host_csr(A, keep, sl)
+                p = _lib.host_csr(P, keep, sl) if P is not None else None
+                r = _lib.host_csr(R, keep, sl) if R is not None else None
                 lo, hi = bounds if bounds is not None else (0.0, 0.0)
                 _lib.check(self.L.mrs_plan_set_level(h, l, C.byref(a),
                                                      C.byref(p) if p is not None else None,

@@ -152,3 +152,20 @@ def test_local_blocks_use_compressed_indices():
     lays = plan_levels([(A, None, None)], 0, 4)
     assert lays[0].A.col_idx.dtype == np.uint16
     assert lays[0].A.ncols < 65536
+
+
+def test_slab_compress_roundtrip_and_bandwidth_limit():
+    from paper_2103_07329_b200.core import slab_compress
+    from paper_2103_07329_b200.io import gen_random_sdd
+    A = gen_random_sdd(n=200_000, band=4096, seed=5)
+    assert A.col_idx.dtype == np.uint32
+    col16, base, shift = slab_compress(A.row_ptr, A.col_idx)
+    assert col16.dtype == np.uint16 and (1 << shift) >= 64
+    rows = np.repeat(np.arange(A.nrows), np.diff(A.row_ptr))
+    np.testing.assert_array_equal(base[rows >> shift].astype(np.int64) + col16,
+                                  A.col_idx.astype(np.int64))
+    # a full-width random matrix cannot be slab-compressed
+    rng = np.random.default_rng(0)
+    from mrs_testutil import random_csr
+    R = random_csr(70001, 70001, 8.0, rng)
+    assert slab_compress(R.row_ptr, R.col_idx.astype(np.uint32)) is None
