@@ -411,7 +411,7 @@ def main():
 
     # roofline: the dominant kernel (fine-level SpMM, residual form b - A x, m=8)
     peak, peak_src = peak_hbm()
-    A0 = cs.layouts[0].A if world > 1 else A          # this rank's block
+    A0 = cs.layouts[0].A if partitioned else A          # this rank's block
     D0 = K.DeviceCsr.from_block(A0)
     Xr = torch.rand(A0.ncols, M, dtype=torch.float64, device="cuda")
     Rd = torch.empty_like(Bd)
