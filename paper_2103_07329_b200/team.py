@@ -248,6 +248,11 @@ def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: 
     from .errors import ShapeMismatchError
     cfg = _configure(config, A, hierarchy, exec_mode, eig_bounds)
     desc, levels, inv, h, name, Ab = cfg
+    if exec_mode == "graph":
+        # NCCL p2p/collectives are captured into one ordinary graph per
+        # iteration (host checks convergence between launches) rather than
+        # into a conditional-node body
+        desc.exec = 2
     glob = [(lv[0], lv[1], lv[2]) for lv in levels]
     lays = plan_levels(glob, team.rank, team.world_size, team.agg_rows_per_rank,
                        team.force_replicate_from)
