@@ -412,7 +412,7 @@ def main():
     # roofline: the dominant kernel (fine-level SpMM, residual form b - A x, m=8)
     peak, peak_src = peak_hbm()
     A0 = cs.layouts[0].A if partitioned else A          # this rank's block
-    D0 = K.DeviceCsr.from_block(A0)
+    D0 = K.DeviceCsr.from_block(A0, slab=True)     # as uploaded by the solver
     Xr = torch.rand(A0.ncols, M, dtype=torch.float64, device="cuda")
     Rd = torch.empty_like(Bd)
     for _ in range(5):
@@ -426,7 +426,8 @@ def main():
     e1.record()
     torch.cuda.synchronize()
     kt = e0.elapsed_time(e1) * 1e-3 / reps
-    kbytes = (A0.nnz * (A0.values.itemsize + A0.col_idx.itemsize) + (n + 1) * 4
+    nslab = 0 if D0.slab_base is None else D0.slab_base.numel()
+    kbytes = (A0.nnz * (A0.values.itemsize + D0.col_idx.element_size()) + (n + 1) * 4 + 4 * nslab
               + (A0.ncols + 2 * n) * M * 8)
     traffic = None
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
@@ -437,7 +438,8 @@ def main():
             traffic = None
     roof = {"bound": "hbm", "achieved": kbytes / kt / 1e9, "peak": peak, "unit": "GB/s",
             "frac": kbytes / kt / 1e9 / peak, "traffic": traffic,
-            "kernel": f"spmm_kernel<{M}, OP_SPMV(RSUB), double, uint{8 * A0.col_idx.itemsize}> "
+            "kernel": f"spmm_kernel<{M}, OP_SPMV(RSUB), double, uint{8 * D0.col_idx.element_size()}"
+                      f"{'(slab)' if nslab else ''}> "
                       f"on the fine-level operator A0 ({args.config})",
             "algorithmic_bytes": kbytes, "us_per_launch": kt * 1e6, "peak_source": peak_src}
 
