@@ -45,6 +45,10 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
     a.slab_base = A.slab_base;
     a.slab_shift = A.slab_shift;
     if (A.nrows == 0) return cudaSuccess;
+    // the SpMM engine indexes with 32 bits (rows, entries, element offsets)
+    if ((A.nrows + 1) * m >= (int64_t)INT32_MAX || (A.ncols + 1) * m >= (int64_t)INT32_MAX ||
+        A.nnz >= (int64_t)INT32_MAX)
+        return cudaErrorInvalidValue;
     if (A.vb == 8) return launch_spmm_f64(op, A, a, m, s, generic);
     if (A.vb == 4) return launch_spmm_f32(op, A, a, m, s, generic);
     return cudaErrorInvalidValue;

@@ -116,7 +116,7 @@ __device__ __forceinline__ Vec<CPL> ldv_rw(const double* p) {
 
 // Value of the gathered operand at column `col` (CPL columns at cofs).
 template <int OP, int CPL, bool NC = true>
-__device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t ld, int cofs) {
+__device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int col, int ld, int cofs) {
     return ldv<CPL, NC>(a.x + col * ld + cofs);
 }
 
@@ -125,11 +125,11 @@ __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int64_t col, int64_t
 template <typename Tv, typename Ti> struct GSrc {
     const Ti* __restrict__ ci;
     const Tv* __restrict__ v;
-    int64_t base = 0;      // slab-compressed indices: column = base(row) + ci
-    __device__ __forceinline__ int64_t col(int64_t k) const { return base + (int64_t)__ldg(ci + k); }
-    __device__ __forceinline__ double val(int64_t k) const { return widen(__ldg(v + k)); }
+    int base = 0;          // slab-compressed indices: column = base(row) + ci
+    __device__ __forceinline__ int col(int k) const { return base + (int)__ldg(ci + k); }
+    __device__ __forceinline__ double val(int k) const { return widen(__ldg(v + k)); }
     // the row's view: slab base of `row` (16-bit slab-relative columns)
-    __device__ __forceinline__ GSrc at_row(const SpArgs& a, int64_t row) const {
+    __device__ __forceinline__ GSrc at_row(const SpArgs& a, int row) const {
         GSrc r = *this;
         if (a.slab_base) r.base = __ldg(a.slab_base + (row >> a.slab_shift));
         return r;
@@ -138,16 +138,16 @@ template <typename Tv, typename Ti> struct GSrc {
 template <typename Tv, typename Ti> struct SSrc {
     const Ti* ci;          // shared memory; entry k lives at ci[k - ci_off]
     const Tv* v;
-    int64_t ci_off, v_off;
-    __device__ __forceinline__ int64_t col(int64_t k) const { return (int64_t)ci[k - ci_off]; }
-    __device__ __forceinline__ double val(int64_t k) const { return widen(v[k - v_off]); }
+    int ci_off, v_off;
+    __device__ __forceinline__ int col(int k) const { return (int)ci[k - ci_off]; }
+    __device__ __forceinline__ double val(int k) const { return widen(v[k - v_off]); }
 };
 
 // Accumulate one row: acc op= sum_k v_k * g(col_k), entry order; the loads
 // of a group of UNR entries are issued before their (ordered) accumulation.
 template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4, bool NC = true>
-__device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int64_t lo,
-                                               int64_t hi, int64_t ld, int cofs,
+__device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int lo,
+                                               int hi, int ld, int cofs,
                                                double (&acc)[CPL]) {
     // Entries in groups of UNR: all loads of a group are issued before the
     // group is accumulated in entry order.  The last, partial group loads
@@ -186,9 +186,10 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
 // One (row, column-slice) of work for every op.  `dotp` accumulates the fused
 // dot (OP_SPMV with a.dot: x_own . y).
 template <int OP, int CPL, class Src, int UNR = 4, bool NC = true>
-__device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int64_t row, int64_t lo,
-                                       int64_t hi, int64_t ld, int cofs, double (&dotp)[CPL]) {
-    const int64_t o = row * ld + cofs;
+__device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row, int lo,
+                                       int hi, int ld, int cofs, double (&dotp)[CPL]) {
+    // 32-bit indices: rows, entries and element offsets < 2^31 (launch checks)
+    const int o = row * ld + cofs;
     double acc[CPL];
     if constexpr (OP == OP_SPMV) {
         const int mode = a.mode;
@@ -304,8 +305,13 @@ __device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[L
     finish_reduction(a.red, s_blk, M, M);
 }
 
+// 6 CTAs/SM (<= 40 registers) where that compiles spill-free
+template <int M, int OP> constexpr int spmm_min_blocks() {
+    return (M <= 16 && (OP == OP_SPMV || OP == OP_JAC_SWEEP)) ? 6 : 1;
+}
+
 template <int M, int OP, typename Tv, typename Ti>
-__global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
+__global__ void __launch_bounds__(kThreads, spmm_min_blocks<M, OP>()) spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
     using L = Lay<M>;
@@ -316,10 +322,10 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel(SpArgs a) {
     double dotp[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
-    for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
-         r0 += (int64_t)gridDim.x * a.chunk) {
-        const int64_t r1 = min(r0 + a.chunk, a.nrows);
-        for (int64_t row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
+    const int nrows = (int)a.nrows, chunk = (int)a.chunk;
+    for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gridDim.x * chunk) {
+        const int r1 = min(r0 + chunk, nrows);
+        for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
             do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src.at_row(a, row), row, __ldg(a.rp + row),
                                                   __ldg(a.rp + row + 1), M, cofs, dotp);
     }
@@ -338,10 +344,10 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
     const GSrc<Tv, Ti> src{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
     double dotp[1] = {0.0};
     if (threadIdx.x < rpb * m) {
-        for (int64_t r0 = (int64_t)blockIdx.x * a.chunk; r0 < a.nrows;
-             r0 += (int64_t)gridDim.x * a.chunk) {
-            const int64_t r1 = min(r0 + a.chunk, a.nrows);
-            for (int64_t row = r0 + threadIdx.x / m; row < r1; row += rpb)
+        const int nrows = (int)a.nrows, chunk = (int)a.chunk;
+        for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gridDim.x * chunk) {
+            const int r1 = min(r0 + chunk, nrows);
+            for (int row = r0 + threadIdx.x / m; row < r1; row += rpb)
                 do_row<OP, 1>(a, src.at_row(a, row), row, __ldg(a.rp + row), __ldg(a.rp + row + 1), m,
                               c, dotp);
         }

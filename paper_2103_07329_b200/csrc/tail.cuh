@@ -37,8 +37,7 @@ __device__ __forceinline__ void tail_rows(const SpArgs& a, int crank, int csize)
     const int cofs = (threadIdx.x % LPR) * CPL;
     const GSrc<Tv, Ti> src{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
     double dotp[CPL];
-    for (int64_t row = (int64_t)crank * RPB + threadIdx.x / LPR; row < a.nrows;
-         row += (int64_t)csize * RPB)
+    for (int row = crank * RPB + threadIdx.x / LPR; row < (int)a.nrows; row += csize * RPB)
         do_row<OP, CPL, GSrc<Tv, Ti>, 4, false>(a, src.at_row(a, row), row, __ldg(a.rp + row),
                                                 __ldg(a.rp + row + 1), M, cofs, dotp);
 }
