@@ -305,9 +305,11 @@ __device__ __forceinline__ void spmm_block_dot(const SpArgs& a, double (&dotp)[L
     finish_reduction(a.red, s_blk, M, M);
 }
 
-// 6 CTAs/SM (<= 40 registers) where that compiles spill-free
+// Occupancy floor per op: 6 CTAs/SM (<= 40 registers) for SpMV / Jacobi,
+// 5 (<= 48) for the Chebyshev steps -- the largest that compile spill-free.
 template <int M, int OP> constexpr int spmm_min_blocks() {
-    return (M <= 16 && (OP == OP_SPMV || OP == OP_JAC_SWEEP)) ? 6 : 1;
+    if (M > 16) return 1;
+    return (OP == OP_SPMV || OP == OP_JAC_SWEEP) ? 6 : 5;
 }
 
 template <int M, int OP, typename Tv, typename Ti>
