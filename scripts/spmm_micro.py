@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--mode", default="rsub", choices=["assign", "rsub"])
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--f32", action="store_true")
+    ap.add_argument("--no-slab", action="store_true", help="plain 32-bit columns")
     ap.add_argument("--knob", action="append", default=[], help="name=value (mrs_set_option)")
     a = ap.parse_args()
     import numpy as np
@@ -36,7 +37,7 @@ def main():
         g = 64 if a.matrix == "c2" else 128
         A = gen_poisson3d(g, g, g)[0]
     vals = A.values.astype(np.float32) if a.f32 else A.values
-    D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols)
+    D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols, slab=not a.no_slab)
     x = torch.rand(A.ncols, a.m, dtype=torch.float64, device="cuda")
     b = torch.rand(A.nrows, a.m, dtype=torch.float64, device="cuda")
     y = torch.empty_like(b)
@@ -54,8 +55,10 @@ def main():
         ts.append(e0.elapsed_time(e1) * 1e3)
     t = sorted(ts)[len(ts) // 2]
     vb = vals.itemsize
-    byts = A.nnz * (vb + A.col_idx.itemsize) + (A.nrows + 1) * 4 + (A.ncols + A.nrows * (2 if mode else 1)) * a.m * 8
-    print(f"{a.matrix} n={A.nrows} nnz={A.nnz} m={a.m} {a.mode}: {t:.2f} us (L2 flushed), "
+    nslab = 0 if D.slab_base is None else D.slab_base.numel()
+    byts = (A.nnz * (vb + D.col_idx.element_size()) + (A.nrows + 1) * 4 + 4 * nslab
+            + (A.ncols + A.nrows * (2 if mode else 1)) * a.m * 8)
+    print(f"{a.matrix} n={A.nrows} nnz={A.nnz} m={a.m} {a.mode} idx={'u16slab' if nslab else 'u' + str(8 * D.col_idx.element_size())}: {t:.2f} us (L2 flushed), "
           f"{byts / t / 1e3:.0f} GB/s algorithmic")
 
 
