@@ -114,6 +114,10 @@ def lib():
     """Load the library, building it first when it is missing or stale."""
     global _lib
     if _lib is None:
+        # torch first: its CUDA libraries bring their own libnccl.so.2, which
+        # then also serves this library (same soname).  Loading ours first
+        # would bind the system NCCL and break torch's newer NCCL symbols.
+        import torch  # noqa: F401
         from . import build as _build
         if _build.needs_build():
             _build.build()

@@ -65,3 +65,45 @@ def test_plan_rejects_bad_descriptors_without_gpu():
     d.m = 4
     d.method = 7
     assert L.mrs_plan_create(ctypes.byref(d), ctypes.byref(h)) == _lib.MRS_ERR_UNSUPPORTED
+
+
+def test_product_path_fails_loudly_without_the_extension(monkeypatch):
+    """No CPU fallback: a missing library is an ImportError, not a slow path."""
+    import pytest
+    from paper_2103_07329_b200 import build
+    monkeypatch.setattr(_lib, "_lib", None)
+    monkeypatch.setattr(_lib, "LIBPATH", "/nonexistent/libmrsolve_b200.so")
+    monkeypatch.setattr(build, "needs_build", lambda: False)
+    with pytest.raises(ImportError):
+        _lib.lib()
+
+
+def test_kernel_plugin_rejects_host_tensors():
+    import numpy as np
+    import pytest
+    import torch
+    from paper_2103_07329_b200 import kernels as K
+    from paper_2103_07329_b200.errors import InvalidArgumentError
+    x = torch.zeros(4, 2, dtype=torch.float64)
+    with pytest.raises(InvalidArgumentError):
+        K.axpby(1.0, x, 1.0, x.clone())
+    with pytest.raises(InvalidArgumentError):
+        K.dot_partial(x, x)
+
+
+def test_reference_objects_are_accepted_by_duck_typing():
+    """A reference CsrBlock / BlockVector (same attributes) converts without
+    copying semantics changes (core.as_csr / as_block_vector)."""
+    import numpy as np
+    from paper_2103_07329_b200.core import as_block_vector, as_csr
+    from paper_2103_07329_b200.io import gen_poisson3d
+
+    class RefLike:                     # attribute contract of mrsolve.core.CsrBlock
+        def __init__(self, b):
+            self.nrows, self.ncols = b.nrows, b.ncols
+            self.row_ptr, self.col_idx, self.values = b.row_ptr, b.col_idx, b.values
+
+    A, b = gen_poisson3d(4, 3, 2)
+    C = as_csr(RefLike(A))
+    assert C.nrows == A.nrows and np.array_equal(C.values, A.values)
+    assert as_block_vector(b) is b
