@@ -46,7 +46,6 @@ cudaError_t launch_tail(const TailStep* steps, int nsteps, int64_t m, const int*
 int tail_cluster_size(int64_t m);
 int tail_rows_threshold();
 void set_tail_rows(int64_t v);
-void set_spmm_long_rows(int64_t v);
 // Grid the reduction kernels use (partials buffer sizing).
 int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);
