@@ -100,6 +100,8 @@ def parse():
     ap.add_argument("--no-spmm", action="store_true", help="skip the config-5 SpMM sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--quick", action="store_true", help="small SpMM sweep (m=8 only)")
+    ap.add_argument("--team", action="store_true",
+                    help="use the row-partitioned (NCCL) path even with one rank")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
                     help="workload (default c2, the BASELINE metric's configuration)")
     ap.add_argument("--exec", default="graph", choices=["graph", "eager"],
@@ -311,7 +313,7 @@ def main():
     Bglob = np.random.default_rng(SEED).uniform(-1.0, 1.0, (nglob, M))
     t0 = time.perf_counter()
     team = None
-    partitioned = world > 1
+    partitioned = world > 1 or args.team
     dist_error = None
     if partitioned:
         # row-partitioned solve of the one global system over NCCL (strong scaling)
