@@ -59,6 +59,15 @@ CONFIGS = {
         roles={"solver": {"method": "BiCGStab", "rel_tolerance": "1e-8"},
                "preconditioner": {"method": "MultiGrid", "mg_mixed_precision": "1"},
                "pre_smoother": _CHEB, "post_smoother": _CHEB}),
+    # C4 is specified at 256^3 on 8 GPUs (~450M nnz); the default here is the
+    # same operator family at 128^3 (56M nnz) -- --grid 256 for the full size
+    "c4": dict(grid=128, m=8, kind="s27", workload=(
+        "C4: 3D anisotropic variable-coefficient 27-point SPD operator (coefficients "
+        "log-uniform [1e-2,1e2] per cell, z-anisotropy 100:1, default_rng(4)), m=8 seeded RHS, "
+        "zero guess, classical RS AMG V(1,1) weighted-Jacobi (w=0.8) + PCG, fp64, tol 1e-8"),
+        roles={"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+               "preconditioner": {"method": "MultiGrid"},
+               "pre_smoother": _JAC, "post_smoother": _JAC}),
 }
 CFG = CONFIGS["c2"]
 GRID, M = CFG["grid"], CFG["m"]
@@ -66,11 +75,17 @@ WORKLOAD, ROLES = CFG["workload"], CFG["roles"]
 REF_SNIPPET = r"""
 import json, sys, time, numpy as np
 import mrsolve
-from mrsolve.core import BlockVector
+from mrsolve.core import BlockVector, CsrBlock
 from mrsolve.io import gen_poisson3d
 grid, m, seed, tol, steps, warmup = {grid}, {m}, {seed}, {tol}, {steps}, {warmup}
 roles = {roles}
-A, _ = gen_poisson3d(grid, grid, grid)
+if {s27}:       # builder-defined C4 operator (not in the reference): our generator
+    sys.path.insert(0, {root!r})
+    from paper_2103_07329_b200.io import gen_stencil27_aniso
+    G = gen_stencil27_aniso(grid, seed=4)
+    A = CsrBlock(G.nrows, G.ncols, G.row_ptr, G.col_idx, G.values)
+else:
+    A, _ = gen_poisson3d(grid, grid, grid)
 B = np.random.default_rng(seed).uniform(-1.0, 1.0, (A.nrows, m))
 t = mrsolve.ParamTree()
 for role, e in roles.items():
@@ -100,6 +115,7 @@ def parse():
     ap.add_argument("--no-spmm", action="store_true", help="skip the config-5 SpMM sweep")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--quick", action="store_true", help="small SpMM sweep (m=8 only)")
+    ap.add_argument("--grid", type=int, default=None, help="override the config's grid size")
     ap.add_argument("--team", action="store_true",
                     help="use the row-partitioned (NCCL) path even with one rank")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
@@ -191,7 +207,7 @@ def run_reference_cpu(steps: int, warmup: int, timeout: float = 900.0):
     if not os.path.isdir(os.path.join(ref, "mrsolve")):
         return None, "oracle/_ref missing (run oracle/build_ref.sh)"
     code = REF_SNIPPET.format(grid=GRID, m=M, seed=SEED, tol=TOL, steps=steps, warmup=warmup,
-                              roles=repr(ROLES))
+                              roles=repr(ROLES), s27=CFG.get("kind") == "s27", root=ROOT)
     env = dict(os.environ, PYTHONPATH=ref, MRSOLVE_KERNELS="cython", OMP_NUM_THREADS="1",
                OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
     cmd = [sys.executable, "-c", code]
@@ -280,16 +296,25 @@ def spmm_sweep(torch, K, quick: bool):
     return {"n": A.nrows, "nnz": A.nnz, "gen_s": gen_s, "points": out}
 
 
-def select(name):
+def select(name, grid=None):
     global CFG, GRID, M, WORKLOAD, ROLES
     CFG = CONFIGS[name]
-    GRID, M = CFG["grid"], CFG["m"]
+    GRID, M = (grid or CFG["grid"]), CFG["m"]
     WORKLOAD, ROLES = CFG["workload"], CFG["roles"]
+    if grid and grid != CFG["grid"]:
+        WORKLOAD = WORKLOAD + f" [grid {grid}^3]"
+
+
+def make_matrix():
+    from paper_2103_07329_b200 import gen_poisson3d, gen_stencil27_aniso
+    if CFG.get("kind") == "s27":
+        return gen_stencil27_aniso(GRID, seed=4)
+    return gen_poisson3d(GRID, GRID, GRID)[0]
 
 
 def main():
     args = parse()
-    select(args.config)
+    select(args.config, args.grid)
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -308,7 +333,7 @@ def main():
     from paper_2103_07329_b200.params import tree
     from paper_2103_07329_b200.solvers import prepare
 
-    A, _ = gen_poisson3d(GRID, GRID, GRID)
+    A = make_matrix()
     nglob = A.nrows
     Bglob = np.random.default_rng(SEED).uniform(-1.0, 1.0, (nglob, M))
     t0 = time.perf_counter()
@@ -419,15 +444,19 @@ def main():
     Rd = torch.empty_like(Bd)
     for _ in range(5):
         K.csr_spmv(D0, None, None, Xr, Rd, K.MODE_RSUB, Bd)
-    reps = 50
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record()
+    # each launch timed alone after an L2 flush (cold operands, as in the ncu
+    # capture that gives `traffic`); median of 50, events on torch's current
+    # stream, which is the stream csr_spmv launches on
+    reps, kts = 50, []
     for _ in range(reps):
+        flush_l2()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
         K.csr_spmv(D0, None, None, Xr, Rd, K.MODE_RSUB, Bd)
-    e1.record()
-    torch.cuda.synchronize()
-    kt = e0.elapsed_time(e1) * 1e-3 / reps
+        e1.record()
+        torch.cuda.synchronize()
+        kts.append(e0.elapsed_time(e1) * 1e-3)
+    kt = sorted(kts)[reps // 2]
     nslab = 0 if D0.slab_base is None else D0.slab_base.numel()
     kbytes = (A0.nnz * (A0.values.itemsize + D0.col_idx.element_size()) + (n + 1) * 4 + 4 * nslab
               + (A0.ncols + 2 * n) * M * 8)
@@ -435,7 +464,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("spmm_rsub_c2_bytes_per_launch")
+            traffic = json.load(open(tp)).get(f"spmm_rsub_{args.config}_bytes_per_launch")
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": kbytes / kt / 1e9, "peak": peak, "unit": "GB/s",

@@ -29,7 +29,7 @@ def main():
     from paper_2103_07329_b200.params import tree
     from paper_2103_07329_b200.solvers import prepare
     bench.select(a.config)
-    A, _ = gen_poisson3d(bench.GRID, bench.GRID, bench.GRID)
+    A = bench.make_matrix()
     B = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, (A.nrows, bench.M))).cuda()
     X = torch.zeros_like(B)
     flush = torch.ones(32 << 20, dtype=torch.float64, device="cuda")

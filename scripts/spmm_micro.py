@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--matrix", default="c2", choices=["c2", "c3", "c5", "c2l1"])
+    ap.add_argument("--matrix", default="c2", choices=["c2", "c3", "c4", "c5", "c2l1"])
     ap.add_argument("--m", type=int, default=8)
     ap.add_argument("--mode", default="rsub", choices=["assign", "rsub"])
     ap.add_argument("--reps", type=int, default=20)
@@ -30,6 +30,9 @@ def main():
     from paper_2103_07329_b200 import gen_poisson3d, gen_random_sdd, kernels as K
     if a.matrix == "c5":
         A = gen_random_sdd()
+    elif a.matrix == "c4":
+        from paper_2103_07329_b200 import gen_stencil27_aniso
+        A = gen_stencil27_aniso(128, seed=4)
     elif a.matrix == "c2l1":
         from paper_2103_07329_b200.amg import setup
         A = setup(gen_poisson3d(64, 64, 64)[0]).levels[1].A
