@@ -48,6 +48,7 @@ extern "C" {
 #define MRS_ERR_SINGULAR     6   /* zero / missing diagonal                     */
 #define MRS_ERR_DEGENERATE   7   /* AMG setup degeneracy after the retry        */
 #define MRS_ERR_STATE        8   /* call out of order (e.g. solve before finalize) */
+#define MRS_ERR_INSTABILITY  9   /* PBiCGStab recurrence drifted from the true residual */
 
 /* csr_spmv accumulation modes (reference kernels/python_ref.py:24-27) */
 #define MRS_MODE_ASSIGN 0   /* y  = A x     */
@@ -115,6 +116,8 @@ int mrs_fused_update_dot2(int64_t n, int64_t m, double* y, const double* u,
 
 #define MRS_METHOD_CG        0
 #define MRS_METHOD_BICGSTAB  1   /* classical van der Vorst, solvers.py:219-293 */
+#define MRS_METHOD_RBICGSTAB 2   /* reordered, two reduction groups, solvers.py:296-364 */
+#define MRS_METHOD_PBICGSTAB 3   /* pipelined (op = A M, drift check), solvers.py:367-479 */
 
 #define MRS_PC_NONE     0
 #define MRS_PC_JACOBI   1        /* _SweepPrecond(jacobi), solvers.py:716-726,782-788 */
@@ -148,6 +151,8 @@ typedef struct {
                                checks convergence (automatic fallback of 0) */
     int32_t merged;      /* BiCGStab merged=1 (solvers.py:258-283): ||s|| always
                             replaces rnorm in the omega breakdown test */
+    double  drift_limit; /* PBiCGStab: ||true r|| / ||recurrence r|| above this raises
+                            MRS_ERR_INSTABILITY (solvers.py:68, :415-423); 0 = 1e3 */
 } mrs_plan_desc;
 
 typedef struct mrs_plan mrs_plan;
@@ -165,7 +170,7 @@ int  mrs_plan_finalize(mrs_plan* p, void* stream);
 
 typedef struct {
     int32_t iterations;
-    int32_t status;          /* MRS_OK or MRS_ERR_BREAKDOWN */
+    int32_t status;          /* MRS_OK, MRS_ERR_BREAKDOWN or MRS_ERR_INSTABILITY */
     int32_t breakdown_column;
     int32_t breakdown_site;  /* which coefficient vanished (see solver.cu) */
     double  device_ms;       /* device time of the solve (CUDA events) */

@@ -136,6 +136,25 @@ SOLVE_CASES = {
         "preconditioner": {"method": "MultiGrid"},
         "pre_smoother": {"method": "Chebyshev", "polynomial_order": "3"},
         "post_smoother": {"method": "Chebyshev", "polynomial_order": "1"}}),
+    # reordered / pipelined BiCGStab
+    "rbicgstab_amg": ((16, 16, 16), 4, 4, {
+        "solver": {"method": "RBiCGStab", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "MultiGrid"},
+        "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+        "post_smoother": {"method": "Jacobi", "weight": "0.8"}}),
+    "rbicgstab_plain_merged": ((10, 10, 10), 3, 5, {
+        "solver": {"method": "RBiCGStab", "rel_tolerance": "1e-9", "merged": "1"}}),
+    "pbicgstab_plain": ((10, 10, 10), 3, 6, {
+        "solver": {"method": "PBiCGStab", "rel_tolerance": "1e-9"}}),
+    "pbicgstab_amg_agg_cheb": ((16, 16, 16), 2, 7, {
+        "solver": {"method": "PBiCGStab", "rel_tolerance": "1e-8", "max_iters": "20"},
+        "preconditioner": {"method": "MultiGrid", "mg_agg_num_levels": "2",
+                           "mg_coarse_matrix_size": "500", "mg_num_paths": "2"},
+        "pre_smoother": {"method": "Chebyshev", "polynomial_order": "2"},
+        "post_smoother": {"method": "Chebyshev", "polynomial_order": "2"}}),
+    "pbicgstab_jacobi_merged": ((12, 12, 12), 2, 8, {
+        "solver": {"method": "PBiCGStab", "rel_tolerance": "1e-8", "merged": "1"},
+        "preconditioner": {"method": "Jacobi"}}),
 }
 
 
@@ -243,15 +262,21 @@ def gen_eig(ms):
 
 
 def main():
+    """All fixtures, or only the named groups (e.g. ``gen_golden.py solves``)."""
     ms = import_reference()
     assert ms.kernels.BACKEND == "cython", ms.kernels.BACKEND
     os.makedirs(OUT, exist_ok=True)
-    rng = np.random.default_rng(20240817)
-    gen_kernels(ms, rng)
-    gen_generators(ms)
-    gen_eig(ms)
-    gen_solves(ms)
-    gen_hierarchies(ms)
+    want = set(sys.argv[1:]) or {"kernels", "generators", "eig", "solves", "hierarchies"}
+    if "kernels" in want:
+        gen_kernels(ms, np.random.default_rng(20240817))
+    if "generators" in want:
+        gen_generators(ms)
+    if "eig" in want:
+        gen_eig(ms)
+    if "solves" in want:
+        gen_solves(ms)
+    if "hierarchies" in want:
+        gen_hierarchies(ms)
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

@@ -9,16 +9,17 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-from .errors import (BreakdownError, ConfigurationError, DeviceError, InvalidArgumentError,
-                     SetupDegeneracyError, SingularDiagonalError)
+from .errors import (BreakdownError, ConfigurationError, DeviceError, InstabilityError,
+                     InvalidArgumentError, SetupDegeneracyError, SingularDiagonalError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIBPATH = os.path.join(HERE, "libmrsolve_b200.so")
 
 MRS_OK, MRS_ERR_ARG, MRS_ERR_CUDA, MRS_ERR_UNSUPPORTED, MRS_ERR_ALLOC = 0, 1, 2, 3, 4
 MRS_ERR_BREAKDOWN, MRS_ERR_SINGULAR, MRS_ERR_DEGENERATE, MRS_ERR_STATE = 5, 6, 7, 8
+MRS_ERR_INSTABILITY = 9
 
-METHOD_CG, METHOD_BICGSTAB = 0, 1
+METHOD_CG, METHOD_BICGSTAB, METHOD_RBICGSTAB, METHOD_PBICGSTAB = 0, 1, 2, 3
 PC_NONE, PC_JACOBI, PC_MG = 0, 1, 2
 SMOOTH_JACOBI, SMOOTH_CHEBYSHEV = 0, 1
 
@@ -47,7 +48,7 @@ class mrs_plan_desc(C.Structure):
                 ("m", C.c_int64), ("rel_tol", C.c_double), ("max_iters", C.c_int32),
                 ("pc_weight", C.c_double), ("pc_sweeps", C.c_int32), ("mg_cycles", C.c_int32),
                 ("pre", mrs_smoother), ("post", mrs_smoother), ("nlevels", C.c_int32),
-                ("exec", C.c_int32), ("merged", C.c_int32)]
+                ("exec", C.c_int32), ("merged", C.c_int32), ("drift_limit", C.c_double)]
 
 
 class mrs_stats(C.Structure):
@@ -157,6 +158,8 @@ def check(code: int, what: str = "mrsolve_b200 call"):
         raise SetupDegeneracyError(msg)
     if code == MRS_ERR_BREAKDOWN:
         raise BreakdownError(msg, -1)
+    if code == MRS_ERR_INSTABILITY:
+        raise InstabilityError(msg)
     raise DeviceError(msg, code)
 
 

@@ -31,6 +31,14 @@ enum VecOp : int {
     V_DOT3,           // (t.s, t.t, s.s)                        (bicgstab:271 + :273)
     V_BICG_XR,        // X = (X + a*ph) + w*sh; r = s + nw*t; (r0.r, r.r)  (bicgstab:285-288)
     V_DOT2,           // (x.y, u.v)
+    // reordered BiCGStab (solvers.py:296-364)
+    V_DOT5,           // (t.s, t.t, r0.s, r0.t, s.s)            (rbicgstab:336-338)
+    V_BICG_XR0,       // X = (X + a*ph) + w*sh; r = s + nw*t     (rbicgstab:345-351, no dots)
+    // pipelined BiCGStab (solvers.py:367-479)
+    V_PBICG_QY,       // (it > 1) p,s,z = r,w,t + beta*(p,s,z - omega*(s,z,v));
+                      // q = r + na*s; y = w + na*z; (q.y, y.y)  (pbicgstab:432-443)
+    V_PBICG_W,        // t += na*v; w = y + nw*t;
+                      // (r0.r, r0.w, r0.s, r0.z, r.r)        (pbicgstab:452-458, 461-463)
 };
 
 template <int OP> struct VK { static constexpr int K = 0; };
@@ -42,10 +50,18 @@ template <> struct VK<V_CG_UPDATE_JAC> { static constexpr int K = 2; };
 template <> struct VK<V_DOT3> { static constexpr int K = 3; };
 template <> struct VK<V_BICG_XR> { static constexpr int K = 2; };
 template <> struct VK<V_DOT2> { static constexpr int K = 2; };
+template <> struct VK<V_DOT5> { static constexpr int K = 5; };
+template <> struct VK<V_PBICG_QY> { static constexpr int K = 2; };
+template <> struct VK<V_PBICG_W> { static constexpr int K = 5; };
 
+// Operand roles of the pipelined-BiCGStab kernels (the fields are generic):
+//   V_PBICG_QY: y=p y2=s y3=z (read+write), y4=q y5=y (write), x=r w=w u=t v=v;
+//               a=-alpha b=beta c=-omega, guard_it=&it (it == 0: no p/s/z update)
+//   V_PBICG_W:  y=t (read+write), y2=w (write), x=v u=y z=r0 v=r s=s w=z;
+//               a=-alpha c=-omega
 struct VArgs {
     int64_t n, m;
-    double* y; double* y2; double* y3;
+    double* y; double* y2; double* y3; double* y4; double* y5;
     const double* x; const double* u; const double* v; const double* w; const double* z;
     const double* s;
     const double* a; const double* b; const double* c;    // per-column scalars (device)
@@ -105,25 +121,32 @@ __device__ __forceinline__ double seed_of(const VArgs& A, double v, double d) {
 
 // Operands of one element, loaded before any store of the unrolled group so
 // the loads of U rows overlap (outputs may alias inputs element-wise).
-struct Ld { double y, y2, x, u, v, w, z, s, d; };
+struct Ld { double y, y2, y3, x, u, v, w, z, s, d; };
 
 template <int OP> struct Uses {
     static constexpr bool y = OP == V_AXPBY || OP == V_ADD2 || OP == V_PAIRED || OP == V_UPDATE_DOT ||
                               OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_P_UPDATE ||
-                              OP == V_BICG_P || OP == V_BICG_XR;
-    static constexpr bool y2 = OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC;
+                              OP == V_BICG_P || OP == V_BICG_XR || OP == V_BICG_XR0 ||
+                              OP == V_PBICG_QY || OP == V_PBICG_W;
+    static constexpr bool y2 = OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_PBICG_QY;
+    static constexpr bool y3 = OP == V_PBICG_QY;
     static constexpr bool x = OP == V_AXPBY || OP == V_DOT || OP == V_UPDATE_DOT || OP == V_COPY ||
                               OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_P_UPDATE ||
                               OP == V_SEED || OP == V_BICG_P || OP == V_BICG_S || OP == V_DOT3 ||
-                              OP == V_DOT2;
+                              OP == V_DOT2 || OP == V_DOT5 || OP == V_PBICG_QY || OP == V_PBICG_W;
     static constexpr bool u = OP == V_ADD2 || OP == V_PAIRED || OP == V_UPDATE_DOT2 ||
                               OP == V_CG_UPDATE || OP == V_CG_UPDATE_JAC || OP == V_BICG_XR ||
-                              OP == V_DOT2;
+                              OP == V_DOT2 || OP == V_BICG_XR0 || OP == V_PBICG_QY ||
+                              OP == V_PBICG_W;
     static constexpr bool v = OP == V_ADD2 || OP == V_BICG_P || OP == V_BICG_S || OP == V_BICG_XR ||
-                              OP == V_DOT2;
-    static constexpr bool w = OP == V_PAIRED || OP == V_UPDATE_DOT2 || OP == V_BICG_XR;
-    static constexpr bool z = OP == V_DOT || OP == V_UPDATE_DOT2 || OP == V_BICG_XR || OP == V_DOT2;
-    static constexpr bool s = OP == V_PAIRED || OP == V_DOT3 || OP == V_BICG_XR;
+                              OP == V_DOT2 || OP == V_BICG_XR0 || OP == V_PBICG_QY ||
+                              OP == V_PBICG_W;
+    static constexpr bool w = OP == V_PAIRED || OP == V_UPDATE_DOT2 || OP == V_BICG_XR ||
+                              OP == V_BICG_XR0 || OP == V_PBICG_QY || OP == V_PBICG_W;
+    static constexpr bool z = OP == V_DOT || OP == V_UPDATE_DOT2 || OP == V_BICG_XR || OP == V_DOT2 ||
+                              OP == V_DOT5 || OP == V_PBICG_W;
+    static constexpr bool s = OP == V_PAIRED || OP == V_DOT3 || OP == V_BICG_XR || OP == V_DOT5 ||
+                              OP == V_BICG_XR0 || OP == V_PBICG_W;
     static constexpr bool d = OP == V_CG_UPDATE_JAC || OP == V_SEED;   // + any seeding op
 };
 
@@ -132,6 +155,7 @@ __device__ __forceinline__ void vec_load(const VArgs& A, int64_t e, int64_t i, L
     using Us = Uses<OP>;
     if constexpr (Us::y) L.y = A.y[e];
     if constexpr (Us::y2) L.y2 = A.y2[e];
+    if constexpr (Us::y3) L.y3 = A.y3[e];
     if constexpr (Us::x) L.x = __ldg(A.x + e);
     if constexpr (Us::u) L.u = A.u[e];
     if constexpr (Us::v) L.v = __ldg(A.v + e);
@@ -144,7 +168,7 @@ __device__ __forceinline__ void vec_load(const VArgs& A, int64_t e, int64_t i, L
 
 template <int OP>
 __device__ __forceinline__ void vec_compute(const VArgs& A, int64_t e, const Ld& L,
-                                            double sa, double sb, double sc,
+                                            double sa, double sb, double sc, bool first,
                                             double (&acc)[VK<OP>::K > 0 ? VK<OP>::K : 1]) {
     if constexpr (OP == V_AXPBY) {
         A.y[e] = add(mul(sb, L.y), mul(sa, L.x));
@@ -209,6 +233,41 @@ __device__ __forceinline__ void vec_compute(const VArgs& A, int64_t e, const Ld&
     } else if constexpr (OP == V_DOT2) {
         acc[0] = add(acc[0], mul(L.x, L.z));
         acc[1] = add(acc[1], mul(L.u, L.v));
+    } else if constexpr (OP == V_DOT5) {
+        // dot_many([(t, s), (t, t), (r0, s), (r0, t), (s, s)]): x=t s=s z=r0
+        acc[0] = add(acc[0], mul(L.x, L.s));
+        acc[1] = add(acc[1], mul(L.x, L.x));
+        acc[2] = add(acc[2], mul(L.z, L.s));
+        acc[3] = add(acc[3], mul(L.z, L.x));
+        acc[4] = add(acc[4], mul(L.s, L.s));
+    } else if constexpr (OP == V_BICG_XR0) {
+        A.y[e] = add(add(L.y, mul(sa, L.u)), mul(sb, L.v));
+        A.y2[e] = add(L.s, mul(sc, L.w));
+    } else if constexpr (OP == V_PBICG_QY) {
+        double p = L.y, s = L.y2, z = L.y3;
+        if (!first) {
+            // axpby(-omega, s, 1, p); axpby(1, r, beta, p) and the same for s, z
+            p = add(mul(sb, add(p, mul(sc, s))), L.x);
+            s = add(mul(sb, add(s, mul(sc, z))), L.w);
+            z = add(mul(sb, add(z, mul(sc, L.v))), L.u);
+            A.y[e] = p; A.y2[e] = s; A.y3[e] = z;
+        }
+        const double q = add(L.x, mul(sa, s));       // q = r - alpha s
+        const double yv = add(L.w, mul(sa, z));      // y = w - alpha z
+        A.y4[e] = q; A.y5[e] = yv;
+        acc[0] = add(acc[0], mul(q, yv));
+        acc[1] = add(acc[1], mul(yv, yv));
+        if (A.seed) A.seed_out[e] = seed_of(A, z, L.d);
+    } else if constexpr (OP == V_PBICG_W) {
+        const double t = add(L.y, mul(sa, L.x));     // t -= alpha v
+        const double w = add(L.u, mul(sc, t));       // w = y - omega t
+        A.y[e] = t; A.y2[e] = w;
+        acc[0] = add(acc[0], mul(L.z, L.v));         // (r0, r)
+        acc[1] = add(acc[1], mul(L.z, w));           // (r0, w)
+        acc[2] = add(acc[2], mul(L.z, L.s));         // (r0, s)
+        acc[3] = add(acc[3], mul(L.z, L.w));         // (r0, z)
+        acc[4] = add(acc[4], mul(L.v, L.v));         // (r, r)
+        if (A.seed) A.seed_out[e] = seed_of(A, w, L.d);
     }
 }
 
@@ -217,7 +276,8 @@ constexpr int kVecUnroll = 4;
 // they stay spill-free under the 64-register cap (4 CTAs/SM)
 template <int OP> __host__ __device__ constexpr int vec_unroll() {
     using Us = Uses<OP>;
-    return (Us::y + Us::y2 + Us::x + Us::u + Us::v + Us::w + Us::z + Us::s) >= 4 ? 2 : kVecUnroll;
+    constexpr int ops = Us::y + Us::y2 + Us::y3 + Us::x + Us::u + Us::v + Us::w + Us::z + Us::s;
+    return ops >= 7 ? 1 : ops >= 4 ? 2 : kVecUnroll;
 }
 
 // CTA b owns the contiguous row range [b*chunk, (b+1)*chunk) (chunk a multiple
@@ -238,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 4) vec_kernel(VArgs A, int64_t chunk
     double acc[K > 0 ? K : 1];
 #pragma unroll
     for (int k = 0; k < (K > 0 ? K : 1); ++k) acc[k] = 0.0;
+    const bool first = A.guard_it && *A.guard_it == 0;   // V_PBICG_QY
     if (rs < rpb) {
         const double sa = A.a ? __ldg(A.a + c) : 0.0;
         const double sb = A.b ? __ldg(A.b + c) : 0.0;
@@ -255,7 +316,7 @@ __global__ void __launch_bounds__(kThreads, 4) vec_kernel(VArgs A, int64_t chunk
 #pragma unroll
             for (int j = 0; j < U; ++j) {
                 const int64_t i = base + rs + (int64_t)j * rpb;
-                if (i < r1) vec_compute<OP>(A, i * m + c, L[j], sa, sb, sc, acc);
+                if (i < r1) vec_compute<OP>(A, i * m + c, L[j], sa, sb, sc, first, acc);
             }
         }
     }

@@ -97,6 +97,7 @@ const char* mrs_status_string(int32_t s) {
     case MRS_ERR_SINGULAR: return "zero or missing diagonal entry";
     case MRS_ERR_DEGENERATE: return "AMG setup degeneracy";
     case MRS_ERR_STATE: return "call out of order";
+    case MRS_ERR_INSTABILITY: return "pipelined BiCGStab residual recurrence drifted from the true residual";
     }
     return "unknown status";
 }

@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads) epilogue_kernel(SolveState* st, cons
                                                             int Km, int m, int epi,
                                                             const int* guard) {
     if (guard && *guard) return;
-    __shared__ double s_v[3 * kMaxM];
+    __shared__ double s_v[kMaxK * kMaxM];
     for (int i = threadIdx.x; i < Km; i += blockDim.x) s_v[i] = vals[i];
     __syncthreads();
     run_epilogue(epi, st, s_v, m);

@@ -74,6 +74,9 @@ int vec_op_k(int op) {
     case V_DOT3: return VK<V_DOT3>::K;
     case V_BICG_XR: return VK<V_BICG_XR>::K;
     case V_DOT2: return VK<V_DOT2>::K;
+    case V_DOT5: return VK<V_DOT5>::K;
+    case V_PBICG_QY: return VK<V_PBICG_QY>::K;
+    case V_PBICG_W: return VK<V_PBICG_W>::K;
     }
     return 0;
 }
@@ -96,6 +99,10 @@ cudaError_t launch_vec(int op, VArgs a, cudaStream_t s) {
     case V_DOT3: return vec_op<V_DOT3>(a, s);
     case V_BICG_XR: return vec_op<V_BICG_XR>(a, s);
     case V_DOT2: return vec_op<V_DOT2>(a, s);
+    case V_DOT5: return vec_op<V_DOT5>(a, s);
+    case V_BICG_XR0: return vec_op<V_BICG_XR0>(a, s);
+    case V_PBICG_QY: return vec_op<V_PBICG_QY>(a, s);
+    case V_PBICG_W: return vec_op<V_PBICG_W>(a, s);
     }
     return cudaErrorInvalidValue;
 }

@@ -38,6 +38,11 @@ struct SolveState {
     int err_col;
     int err_site;
     int merged;              // BiCGStab merged variant (snorm always from (s,s))
+    int pskip;               // RBiCGStab: skip the end-of-iteration p update
+    int nodrift;             // PBiCGStab: skip this iteration's drift check
+    double drift_limit;      // PBiCGStab DRIFT_LIMIT (solvers.py:68)
+    double one[kMaxM];       // per-column constants for axpby-shaped steps
+    double neg_one[kMaxM];
     int has_cond;            // graph conditional handle valid
     cudaGraphConditionalHandle cond;
     double* history;         // (max_iters + 1) * m, device
@@ -57,12 +62,22 @@ enum Epilogue : int {
     EPI_FINAL,         // out = r.r (true residual) -> final_rel
     EPI_CG_RNORM_BETA, // out = (r.r, r.z)     -> EPI_CG_RNORM then, if not converged, EPI_CG_BETA
     EPI_CG_RNORM_BETA1,// out = r.r, z = r (no preconditioner): same with r.z = r.r
+    // reordered BiCGStab (solvers.py:296-364)
+    EPI_RBICG_OMEGA,   // out = (t.s, t.t, r0.s, r0.t, s.s) -> omega, rho', rnorm, history,
+                       //   stop; beta, rho while not converged
+    // pipelined BiCGStab (solvers.py:367-479)
+    EPI_PBICG_INIT,    // out = (r0.r, r0.w)  -> rho, alpha
+    EPI_PBICG_OMEGA,   // out = (q.y, y.y)    -> it++, omega
+    EPI_PBICG_RHO,     // out = (r0.r, r0.w, r0.s, r0.z, r.r) -> rnorm, history, beta,
+                       //   alpha, rho, stop, drift-check flag
+    EPI_PBICG_DRIFT,   // out = chk.chk       -> instability check
 };
+constexpr int kMaxK = 5;   // reduced values per column of one reduction
 
 // Breakdown sites, reported to the host for the exception message.
 enum BreakSite : int {
     BRK_CG_CURVATURE = 1, BRK_CG_RHO = 2, BRK_BICG_RV = 3, BRK_BICG_OMEGA = 4,
-    BRK_BICG_RHO = 5, BRK_BICG_OMEGA_PREV = 6,
+    BRK_BICG_RHO = 5, BRK_BICG_OMEGA_PREV = 6, BRK_PBICG_R0W = 7, BRK_PBICG_R0S = 8,
 };
 
 struct RedArgs {
@@ -115,6 +130,7 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
         int all = __syncthreads_and(conv);
         if (threadIdx.x == 0) {
             st->it = 0; st->skip = 0; st->err = MRS_OK; st->err_col = 1 << 30; st->err_site = 0;
+            st->pskip = 0; st->nodrift = 1;
             st->stop = (all || st->max_iters <= 0) ? 1 : 0;
             set_loop(st, !st->stop);
         }
@@ -229,12 +245,129 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
     case EPI_FINAL:
         if (act) st->final_rel[c] = divd(sqrt(v[c]), st->bscale[c]);
         break;
+    case EPI_RBICG_OMEGA: {
+        // solvers.py:334-359.  omega breaks down BEFORE the X/r update (skip
+        // everything); beta after it (the update still runs, p does not).
+        double w = 0.0, rn = 0.0;
+        if (act) {
+            const double ts = v[c], tt = v[m + c], r0s = v[2 * m + c], r0t = v[3 * m + c];
+            const double ss = v[4 * m + c];
+            w = coef(ts, tt, sqrt(ss), c, st, BRK_BICG_OMEGA, bad);
+            st->omega[c] = w; st->neg_omega[c] = -w;
+            st->rho_next[c] = sub(r0s, mul(w, r0t));
+            // max(ss - 2 omega ts + omega^2 tt, 0), numpy's left-to-right order
+            double rr = add(sub(ss, mul(mul(2.0, w), ts)), mul(mul(w, w), tt));
+            rr = (rr != rr) ? rr : (rr > 0.0 ? rr : 0.0);
+            rn = sqrt(rr);
+        }
+        if (__syncthreads_or(bad)) break;          // omega breakdown: common path below
+        bool conv = true;
+        if (act) {
+            st->rnorm[c] = rn;
+            st->history[(size_t)st->it * m + c] = divd(rn, st->bscale[c]);
+            conv = rn <= mul(st->tol, st->bscale[c]);
+        }
+        const int all = __syncthreads_and(conv);
+        if (!all) {
+            // beta = coef(rho', rho) * coef(alpha, omega); the first factor's
+            // breakdown is reported before the second's (like the reference)
+            double b1 = 0.0;
+            if (act) b1 = coef(st->rho_next[c], st->rho[c], rn, c, st, BRK_BICG_RHO, bad);
+            if (!__syncthreads_or(bad) && act) {
+                const double b2 = coef(st->alpha[c], w, rn, c, st, BRK_BICG_OMEGA_PREV, bad);
+                st->beta[c] = mul(b1, b2);
+                st->rho[c] = st->rho_next[c];
+            }
+        }
+        const int anybad = __syncthreads_or(bad);
+        if (threadIdx.x == 0) {
+            st->pskip = (all || anybad) ? 1 : 0;
+            st->stop = (all || anybad || st->it >= st->max_iters) ? 1 : 0;
+            if (anybad) st->err = MRS_ERR_BREAKDOWN;
+            set_loop(st, !st->stop);
+        }
+        return;
+    }
+    case EPI_PBICG_INIT:
+        // solvers.py:401-402
+        if (act) {
+            st->rho[c] = v[c];
+            const double a = coef(v[c], v[m + c], st->rnorm[c], c, st, BRK_PBICG_R0W, bad);
+            st->alpha[c] = a; st->neg_alpha[c] = -a;
+            st->omega[c] = 0.0; st->neg_omega[c] = -0.0;
+        }
+        if (threadIdx.x == 0) st->nodrift = 1;
+        break;
+    case EPI_PBICG_OMEGA:
+        // solvers.py:443-445
+        if (act) {
+            const double w = coef(v[c], v[m + c], st->rnorm[c], c, st, BRK_BICG_OMEGA, bad);
+            st->omega[c] = w; st->neg_omega[c] = -w;
+        }
+        if (threadIdx.x == 0) st->it += 1;
+        break;
+    case EPI_PBICG_RHO: {
+        // solvers.py:461-472 (evaluated every iteration, converged or not)
+        bool conv = true;
+        double rn = 0.0;
+        if (act) {
+            const double rr = v[4 * m + c];
+            rn = sqrt((rr != rr) ? rr : (rr > 0.0 ? rr : 0.0));
+            st->rnorm[c] = rn;
+            st->history[(size_t)st->it * m + c] = divd(rn, st->bscale[c]);
+            conv = rn <= mul(st->tol, st->bscale[c]);
+        }
+        const int all = __syncthreads_and(conv);
+        double b1 = 0.0, beta = 0.0;
+        if (act) b1 = coef(v[c], st->rho[c], rn, c, st, BRK_BICG_RHO, bad);
+        if (!__syncthreads_or(bad)) {
+            if (act) beta = mul(b1, coef(st->alpha[c], st->omega[c], rn, c, st,
+                                         BRK_BICG_OMEGA_PREV, bad));
+            if (!__syncthreads_or(bad) && act) {
+                const double r0w = v[m + c], r0s = v[2 * m + c], r0z = v[3 * m + c];
+                const double r0s_next = add(r0w, mul(beta, sub(r0s, mul(st->omega[c], r0z))));
+                const double a = coef(v[c], r0s_next, rn, c, st, BRK_PBICG_R0S, bad);
+                st->beta[c] = beta;
+                st->alpha[c] = a; st->neg_alpha[c] = -a;
+                st->rho[c] = v[c];
+            }
+        }
+        const int anybad = __syncthreads_or(bad);
+        if (threadIdx.x == 0) {
+            const int stop = all || anybad || st->it >= st->max_iters;
+            st->stop = stop;
+            // the remaining products of this iteration only feed the next one
+            st->skip = stop ? 1 : 0;
+            st->nodrift = (!anybad && (st->it % 20 == 0 || all)) ? 0 : 1;
+            if (anybad) st->err = MRS_ERR_BREAKDOWN;
+            set_loop(st, !stop);
+        }
+        return;
+    }
+    case EPI_PBICG_DRIFT: {
+        // solvers.py:415-423: ||r_init - op(zacc)|| / max(rnorm, tiny) > limit
+        bool drift = false;
+        if (act) {
+            const double rec = st->rnorm[c] > 2.2250738585072014e-308 ? st->rnorm[c]
+                                                                        : 2.2250738585072014e-308;
+            drift = divd(sqrt(v[c]), rec) > st->drift_limit;
+        }
+        if (__syncthreads_or(drift) && threadIdx.x == 0) {
+            st->err = MRS_ERR_INSTABILITY;
+            st->stop = 1;
+            st->skip = 1;
+            set_loop(st, false);
+        }
+        return;
+    }
     }
     int anybad = __syncthreads_or(bad);
     if (anybad && threadIdx.x == 0) {
         st->err = MRS_ERR_BREAKDOWN;
         st->skip = 1;
         st->stop = 1;
+        st->pskip = 1;
+        st->nodrift = 1;
         set_loop(st, false);
     }
 }
@@ -243,7 +376,7 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
 // All threads of every CTA call this.
 static __device__ void finish_reduction(const RedArgs& ra, const double* blk, int Km, int m) {
     __shared__ bool s_last;
-    __shared__ double s_out[3 * kMaxM];
+    __shared__ double s_out[kMaxK * kMaxM];
     const int G = gridDim.x;
     // value-major partials [Km][G]: the last CTA reads each value's G partials
     // with coalesced warp loads

@@ -2,8 +2,10 @@
 // of one solve, and its CUDA-graph execution with a device-side while loop.
 //
 // Replaces solvers.prepare(...).run(B, X) (src/solvers.py:850-959) for
-//   CG        (cg_solve, solvers.py:152-188)
-//   BiCGStab  (_bicgstab_classical, merged=0, solvers.py:219-293)
+//   CG         (cg_solve, solvers.py:152-188)
+//   BiCGStab   (_bicgstab_classical, solvers.py:219-293)
+//   RBiCGStab  (_bicgstab_reordered, solvers.py:296-364)
+//   PBiCGStab  (_bicgstab_pipelined, solvers.py:367-479)
 // preconditioned by nothing, Jacobi sweeps (_SweepPrecond, :716-726) or a
 // MultiGrid V-cycle (solvers.py:615-675) with Jacobi (blas2.py:165-185) or
 // Chebyshev (solvers.py:520-571) smoothing and a dense coarsest solve.
@@ -78,6 +80,10 @@ struct mrs_plan {
     double *B = nullptr, *X = nullptr, *r = nullptr, *r0 = nullptr, *p = nullptr, *q = nullptr;
     double *v = nullptr, *s = nullptr, *t = nullptr, *ph = nullptr, *sh = nullptr, *z = nullptr,
            *zt = nullptr;
+    // PBiCGStab only: r_init, accumulated correction, w, y, drift-check vector,
+    // second preconditioner scratch pair
+    double *rinit = nullptr, *zacc = nullptr, *w = nullptr, *yv = nullptr, *chk = nullptr,
+           *pa = nullptr, *pb = nullptr;
     // device state + reduction scratch
     SolveState* st = nullptr;
     double* history = nullptr;
@@ -617,6 +623,160 @@ void build_bicgstab(mrs_plan* P, bool x_zero, Program& pg) {
     }
 }
 
+// Reordered BiCGStab (solvers.py:296-364): two reduction groups per
+// iteration; rho' and ||r'|| come from the linear relations
+// rho' = (r0,s) - omega (r0,t), ||r'||^2 = (s,s) - 2 omega (t,s) + omega^2 (t,t).
+// merged=1 is bitwise identical here (paired_update == add2_scaled + axpby).
+void build_rbicgstab(mrs_plan* P, bool x_zero, Program& pg) {
+    const int64_t n = P->n;
+    SolveState* st = P->st;
+    const int* skip = &st->skip;
+    const DevCsr& A = P->L[0].A;
+    const bool pc_on = P->desc.precond != MRS_PC_NONE;
+    PCPlan pph = plan_precond(P, skip, P->p, P->ph, P->zt, pc_on, -1);
+    PCPlan psh = plan_precond(P, skip, P->s, P->sh, P->zt, pc_on, -1);
+    {   // prologue (solvers.py:302-319)
+        Builder b{P, &pg.pro, nullptr};
+        b.dot(P->B, P->B, n, EPI_BSCALE);
+        if (x_zero) b.copy(P->B, P->r, n);
+        else b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.copy(P->r, P->r0, n);
+        b.dot(P->r, P->r, n, EPI_RNORM_INIT);
+        b.dot(P->r0, P->r, n, EPI_RHO);
+        b.copy(P->r, P->p, n, pph.seed);        // p = r (first iteration) + seed of M p
+    }
+    {   // body (solvers.py:322-359)
+        Builder b{P, &pg.body, skip};
+        const double* ph = pc_on ? pph.out : P->p;
+        append(pg.body, pph.ops);
+        b.bytes += pph.bytes; b.kernels += pph.kernels;
+        b.spmv(A, ph, P->v, MRS_MODE_ASSIGN, nullptr, EPI_BICG_ALPHA, P->r0);  // v = A ph; (r0,v)
+        VArgs sa = Builder::v0(); sa.n = n; sa.y = P->s; sa.x = P->r; sa.v = P->v;
+        sa.a = st->neg_alpha;
+        Builder::set_seed(sa, psh.seed);
+        b.vec(V_BICG_S, sa, 3 * b.V(n) + b.seed_bytes(psh.seed, n));       // s = r - alpha v
+        const double* sh = pc_on ? psh.out : P->s;
+        append(pg.body, psh.ops);
+        b.bytes += psh.bytes; b.kernels += psh.kernels;
+        b.spmv(A, sh, P->t, MRS_MODE_ASSIGN);                               // t = A sh
+        VArgs d5 = Builder::v0(); d5.n = n; d5.x = P->t; d5.s = P->s; d5.z = P->r0;
+        d5.red = b.red(EPI_RBICG_OMEGA);
+        b.vec(V_DOT5, d5, 3 * b.V(n));                                      // reduction group 2
+        VArgs xr = Builder::v0(); xr.n = n; xr.y = P->X; xr.u = ph; xr.v = sh; xr.s = P->s;
+        xr.w = P->t; xr.y2 = P->r;
+        xr.a = st->alpha; xr.b = st->omega; xr.c = st->neg_omega;
+        b.vec(V_BICG_XR0, xr, 7 * b.V(n));                                  // X, r
+        VArgs pu = Builder::v0(); pu.n = n; pu.y = P->p; pu.x = P->r; pu.v = P->v;
+        pu.b = st->beta; pu.c = st->neg_omega; pu.guard = &st->pskip;
+        Builder::set_seed(pu, pph.seed);
+        b.vec(V_BICG_P, pu, 4 * b.V(n) + b.seed_bytes(pph.seed, n));       // p = r + beta(p - w v)
+        pg.body_bytes = b.bytes;
+        pg.body_kernels = b.kernels;
+    }
+    {
+        Builder b{P, &pg.epi, nullptr};
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_FINAL);
+    }
+}
+
+// Pipelined BiCGStab (solvers.py:367-479): the solver runs on op = A M in
+// the preconditioned variable (zacc); two products and two reduction groups
+// per iteration; every 20th iteration (and at convergence) the recurrence
+// residual is cross-checked against r_init - op(zacc).  X += M zacc at the end.
+void build_pbicgstab(mrs_plan* P, bool x_zero, Program& pg) {
+    const int64_t n = P->n;
+    SolveState* st = P->st;
+    const int* skip = &st->skip;
+    const int* nodrift = &st->nodrift;
+    const DevCsr& A = P->L[0].A;
+    const bool pc_on = P->desc.precond != MRS_PC_NONE;
+    // preconditioner applications: consecutive ops use disjoint scratch pairs,
+    // so a product seeding the next application never writes what it reads
+    PCPlan pc_r = plan_precond(P, nullptr, P->r, P->ph, P->zt, pc_on, -1);
+    PCPlan pc_w0 = plan_precond(P, nullptr, P->w, P->pa, P->pb, pc_on, -1);
+    PCPlan pc_z = plan_precond(P, skip, P->z, P->ph, P->zt, pc_on, -1);
+    PCPlan pc_w = plan_precond(P, skip, P->w, P->pa, P->pb, pc_on, -1);
+    PCPlan pc_d = plan_precond(P, nodrift, P->zacc, P->ph, P->zt, false, -1);
+    PCPlan pc_f = plan_precond(P, nullptr, P->zacc, P->ph, P->zt, false, -1);
+    const size_t vbytes = (size_t)P->L[0].vrows * P->m * 8;
+    {   // prologue (solvers.py:388-409)
+        Builder b{P, &pg.pro, nullptr};
+        b.dot(P->B, P->B, n, EPI_BSCALE);
+        if (x_zero) b.copy(P->B, P->rinit, n);
+        else b.spmv(A, P->X, P->rinit, MRS_MODE_RSUB, P->B);
+        b.copy(P->rinit, P->r, n, pc_r.seed);
+        b.copy(P->rinit, P->r0, n);
+        double* za = P->zacc;
+        pg.pro.push_back([=](cudaStream_t s) { return cudaMemsetAsync(za, 0, vbytes, s); });
+        b.dot(P->r, P->r, n, EPI_RNORM_INIT);
+        append(pg.pro, pc_r.ops);
+        b.spmv(A, pc_on ? pc_r.out : P->r, P->w, MRS_MODE_ASSIGN, nullptr, -1, nullptr,
+               pc_w0.seed);                                                 // w = op(r)
+        append(pg.pro, pc_w0.ops);
+        b.spmv(A, pc_on ? pc_w0.out : P->w, P->t, MRS_MODE_ASSIGN);        // t = op(w)
+        VArgs d2 = Builder::v0(); d2.n = n; d2.x = P->r0; d2.z = P->r; d2.u = P->r0; d2.v = P->w;
+        d2.red = b.red(EPI_PBICG_INIT);
+        b.vec(V_DOT2, d2, 3 * b.V(n));                                      // rho, alpha
+        b.copy(P->r, P->p, n);                                              // first iteration:
+        b.copy(P->w, P->s, n);                                              //   p, s, z = r, w, t
+        b.copy(P->t, P->z, n, pc_z.seed);
+    }
+    {   // body (solvers.py:427-474)
+        Builder b{P, &pg.body, skip};
+        VArgs qy = Builder::v0(); qy.n = n;
+        qy.y = P->p; qy.y2 = P->s; qy.y3 = P->z; qy.y4 = P->q; qy.y5 = P->yv;
+        qy.x = P->r; qy.w = P->w; qy.u = P->t; qy.v = P->v;
+        qy.a = st->neg_alpha; qy.b = st->beta; qy.c = st->neg_omega; qy.guard_it = &st->it;
+        Builder::set_seed(qy, pc_z.seed);
+        qy.red = b.red(EPI_PBICG_OMEGA);
+        b.vec(V_PBICG_QY, qy, 12 * b.V(n) + b.seed_bytes(pc_z.seed, n));  // group 1 -> omega
+        append(pg.body, pc_z.ops);
+        b.bytes += pc_z.bytes; b.kernels += pc_z.kernels;
+        b.spmv(A, pc_on ? pc_z.out : P->z, P->v, MRS_MODE_ASSIGN);         // v = op(z)
+        VArgs xr = Builder::v0(); xr.n = n; xr.y = P->zacc; xr.u = P->p; xr.v = P->q;
+        xr.s = P->q; xr.w = P->yv; xr.y2 = P->r;
+        xr.a = st->alpha; xr.b = st->omega; xr.c = st->neg_omega;
+        b.vec(V_BICG_XR0, xr, 6 * b.V(n));                                  // zacc, r
+        VArgs wk = Builder::v0(); wk.n = n; wk.y = P->t; wk.y2 = P->w; wk.x = P->v;
+        wk.u = P->yv; wk.z = P->r0; wk.v = P->r; wk.s = P->s; wk.w = P->z;
+        wk.a = st->neg_alpha; wk.c = st->neg_omega;
+        Builder::set_seed(wk, pc_w.seed);
+        wk.red = b.red(EPI_PBICG_RHO);
+        b.vec(V_PBICG_W, wk, 9 * b.V(n) + b.seed_bytes(pc_w.seed, n));     // t, w; group 2
+        append(pg.body, pc_w.ops);
+        b.bytes += pc_w.bytes; b.kernels += pc_w.kernels;
+        b.spmv(A, pc_on ? pc_w.out : P->w, P->t, MRS_MODE_ASSIGN);         // t = op(w)
+        pg.body_bytes = b.bytes;
+        pg.body_kernels = b.kernels;
+        // drift check (solvers.py:415-423), only when the epilogue asked for it
+        Builder bd{P, &pg.body, nodrift};
+        append(pg.body, pc_d.ops);
+        bd.spmv(A, pc_on ? pc_d.out : P->zacc, P->chk, MRS_MODE_ASSIGN);   // chk = op(zacc)
+        VArgs ud = Builder::v0(); ud.n = n; ud.y = P->chk; ud.x = P->rinit;
+        ud.a = st->one; ud.b = st->neg_one; ud.red = bd.red(EPI_PBICG_DRIFT);
+        bd.vec(V_UPDATE_DOT, ud, 3 * bd.V(n));                              // r_init - chk; norm
+    }
+    {   // X += M zacc (solvers.py:476-479), then the true residual
+        Builder b{P, &pg.epi, nullptr};
+        append(pg.epi, pc_f.ops);
+        VArgs xu = Builder::v0(); xu.n = n; xu.y = P->X; xu.x = pc_on ? pc_f.out : P->zacc;
+        xu.a = st->one; xu.b = st->one;
+        b.vec(V_AXPBY, xu, 3 * b.V(n));
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_FINAL);
+    }
+}
+
+void build_program(mrs_plan* P, bool x_zero, Program& pg) {
+    switch (P->desc.method) {
+    case MRS_METHOD_CG: build_cg(P, x_zero, pg); break;
+    case MRS_METHOD_BICGSTAB: build_bicgstab(P, x_zero, pg); break;
+    case MRS_METHOD_RBICGSTAB: build_rbicgstab(P, x_zero, pg); break;
+    default: build_pbicgstab(P, x_zero, pg); break;
+    }
+}
+
 __global__ void set_cond_kernel(SolveState* st, cudaGraphConditionalHandle h, int has) {
     st->has_cond = has;
     st->cond = h;
@@ -632,8 +792,7 @@ cudaError_t run_list(const std::vector<Launch>& v, cudaStream_t s) {
 
 int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s) {
     Program pg;
-    if (P->desc.method == MRS_METHOD_CG) build_cg(P, x_zero, pg);
-    else build_bicgstab(P, x_zero, pg);
+    build_program(P, x_zero, pg);
     int gi = x_zero ? 1 : 0;
 
     cudaGraph_t g;
@@ -756,7 +915,7 @@ extern "C" {
 int mrs_plan_create(const mrs_plan_desc* desc, mrs_plan** out) {
     if (!desc || !out) return MRS_ERR_ARG;
     if (desc->m < 1 || desc->m > kMaxM || desc->nrows < 1) return MRS_ERR_ARG;
-    if (desc->method != MRS_METHOD_CG && desc->method != MRS_METHOD_BICGSTAB) return MRS_ERR_UNSUPPORTED;
+    if (desc->method < MRS_METHOD_CG || desc->method > MRS_METHOD_PBICGSTAB) return MRS_ERR_UNSUPPORTED;
     if (desc->precond < MRS_PC_NONE || desc->precond > MRS_PC_MG) return MRS_ERR_UNSUPPORTED;
     int nl = desc->precond == MRS_PC_MG ? desc->nlevels : 1;
     if (nl < 1) return MRS_ERR_ARG;
@@ -780,7 +939,10 @@ int mrs_plan_set_level(mrs_plan* p, int32_t l, const mrs_host_csr* A, const mrs_
     if ((rc = upload_csr(R, lv.R, p->owned))) return rc;
     lv.lmin = lmin; lv.lmax = lmax;
     std::vector<double> d;
-    const bool need_diag = !(l == (int)p->L.size() - 1 && p->desc.precond == MRS_PC_MG);
+    // smoothers / Jacobi need the diagonal; the coarsest MG level and a plain
+    // Krylov solve do not (the reference only checks it where it divides)
+    const bool need_diag = p->desc.precond != MRS_PC_NONE &&
+                           !(l == (int)p->L.size() - 1 && p->desc.precond == MRS_PC_MG);
     if (need_diag) {
         if ((rc = host_diag(A, d))) return rc;
         for (double v : d)
@@ -865,11 +1027,18 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
         *v = dalloc<double>(V, o);
         if (!*v) return MRS_ERR_ALLOC;
     }
+    if (p->desc.method == MRS_METHOD_PBICGSTAB) {
+        double** pv[] = {&p->rinit, &p->zacc, &p->w, &p->yv, &p->chk, &p->pa, &p->pb};
+        for (double** v : pv) {
+            *v = dalloc<double>(V, o);
+            if (!*v) return MRS_ERR_ALLOC;
+        }
+    }
     p->st = dalloc<SolveState>(1, o);
     p->history = dalloc<double>((size_t)(p->desc.max_iters + 1) * m, o);
-    p->partials = dalloc<double>((size_t)max_grid() * 3 * m, o);
+    p->partials = dalloc<double>((size_t)max_grid() * kMaxK * m, o);
     p->ticket = dalloc<unsigned int>(1, o);
-    p->red_out = dalloc<double>(3 * m, o);
+    p->red_out = dalloc<double>(kMaxK * m, o);
     if (!p->st || !p->history || !p->partials || !p->ticket || !p->red_out) return MRS_ERR_ALLOC;
     MRS_CUDA_OK(cudaMemset(p->ticket, 0, sizeof(unsigned int)));
     SolveState hs;
@@ -880,6 +1049,9 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     hs.history = p->history;
     hs.err_col = 1 << 30;
     hs.merged = p->desc.merged ? 1 : 0;
+    hs.drift_limit = p->desc.drift_limit > 0.0 ? p->desc.drift_limit : 1e3;
+    hs.nodrift = 1;
+    for (int c = 0; c < kMaxM; ++c) { hs.one[c] = 1.0; hs.neg_one[c] = -1.0; }
     MRS_CUDA_OK(cudaMemcpy(p->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
     MRS_CUDA_OK(cudaEventCreate(&p->ev0));
     MRS_CUDA_OK(cudaEventCreate(&p->ev1));
@@ -902,8 +1074,7 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     p->finalized = true;
     // estimate the per-iteration byte model / kernel count once
     Program pg;
-    if (p->desc.method == MRS_METHOD_CG) build_cg(p, true, pg);
-    else build_bicgstab(p, true, pg);
+    build_program(p, true, pg);
     p->it_bytes = pg.body_bytes;
     p->body_kernels = (int)pg.body.size();
     p->fixed_kernels = (int)(pg.pro.size() + pg.epi.size()) + 1;
@@ -937,8 +1108,7 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
     } else if (p->desc.exec == 2) {
         if (!p->body_exec[gi]) {
             Program pg;
-            if (p->desc.method == MRS_METHOD_CG) build_cg(p, x_is_zero != 0, pg);
-            else build_bicgstab(p, x_is_zero != 0, pg);
+            build_program(p, x_is_zero != 0, pg);
             p->pro_list[gi] = pg.pro;
             p->epi_list[gi] = pg.epi;
             cudaStream_t cs;
@@ -969,8 +1139,7 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
         // eager: no conditional handle; the host polls st->stop per iteration
         set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);
         MRS_CUDA_OK(cudaGetLastError());
-        if (p->desc.method == MRS_METHOD_CG) build_cg(p, x_is_zero != 0, pg);
-        else build_bicgstab(p, x_is_zero != 0, pg);
+        build_program(p, x_is_zero != 0, pg);
         MRS_CUDA_OK(run_list(pg.pro, s));
         for (;;) {
             int stop = 0;
@@ -1000,7 +1169,7 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
         MRS_CUDA_OK(cudaMemcpy(history, p->history, sizeof(double) * (hs.it + 1) * p->m,
                                cudaMemcpyDeviceToHost));
     }
-    return hs.err == MRS_OK ? MRS_OK : MRS_ERR_BREAKDOWN;
+    return hs.err;
 }
 
 int mrs_plan_set_comm(mrs_plan* p, mrs_comm* c) {
@@ -1061,8 +1230,7 @@ int mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32
     if (!p || !p->finalized || !us || !count || iters < 1) return MRS_ERR_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     Program pg;
-    if (p->desc.method == MRS_METHOD_CG) build_cg(p, true, pg);
-    else build_bicgstab(p, true, pg);
+    build_program(p, true, pg);
     const size_t bytes = (size_t)p->n * p->m * 8;
     MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
     set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);

@@ -8,12 +8,12 @@ Chebyshev eigenvalue bounds, the dense coarse inverse -- and uploads it
 once; ``run`` executes one whole solve on the device as a single CUDA graph
 launch (iteration loop driven on the device; see csrc/solver.cu).
 
-Device path: solver CG or BiCGStab (classical; merged=0/1),
-preconditioner none / Jacobi / MultiGrid V-cycle, smoothers Jacobi or
-Chebyshev.  Everything else the reference's ParamTree can express
-(Gauss-Seidel smoothing, RBiCGStab/PBiCGStab, Direct and stationary solvers)
-is outside this path and raises ConfigurationError -- there is no CPU
-fallback.
+Device path: solver CG or BiCGStab in its
+three formulations -- classical, reordered (RBiCGStab), pipelined
+(PBiCGStab); merged=0/1 --, preconditioner none / Jacobi / MultiGrid V-cycle,
+smoothers Jacobi or Chebyshev.  Everything else the reference's ParamTree can
+express (Gauss-Seidel smoothing, Direct and stationary solvers) is outside
+this path and raises ConfigurationError -- there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -30,7 +30,11 @@ from .errors import (BreakdownError, ConfigurationError, InvalidArgumentError,
                      ShapeMismatchError)
 from .params import METHOD_FAMILIES, ParamTree
 
-__all__ = ["SolveStats", "ConfiguredSolver", "prepare", "solve", "DevicePlan"]
+__all__ = ["SolveStats", "ConfiguredSolver", "prepare", "solve", "DevicePlan", "DRIFT_LIMIT"]
+
+#: pipelined BiCGStab drift limit (solvers.py:68): ||r_init - op(zacc)|| over
+#: the recurrence norm above this raises InstabilityError.  Read at prepare().
+DRIFT_LIMIT = 1e3
 
 _BREAK_MSG = {
     1: "CG search-direction curvature vanished",
@@ -39,6 +43,8 @@ _BREAK_MSG = {
     4: "BiCGStab stabilization step vanished",
     5: "BiCGStab rho vanished",
     6: "BiCGStab omega vanished",
+    7: "BiCGStab (r0, Ar) vanished",
+    8: "BiCGStab (r0, s) vanished",
 }
 
 
@@ -243,18 +249,22 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
     sp = config.role("solver")
     method = sp.method
     family = METHOD_FAMILIES[method]
-    if family not in ("CG", "BiCGStab") or method in ("RBiCGStab", "PBiCGStab"):
+    if family not in ("CG", "BiCGStab"):
         raise ConfigurationError(
-            f"solver {method!r} is not on the device solve path (CG and classical BiCGStab "
-            "are; see SURVEY.md 8(f))")
+            f"solver {method!r} is not on the device solve path (CG and the three BiCGStab "
+            "formulations are; see SURVEY.md 8(f))")
     tol = sp.get_float("rel_tolerance")
     iters = sp.get_int("max_iters")
     merged = bool(sp.get_int("merged")) if family == "BiCGStab" else False
-    name = "CG" if family == "CG" else ("BiCGStab" + ("/merged" if merged else ""))
+    # SolveStats.method as the reference names it (solvers.py:292, :363, :478)
+    name = "CG" if family == "CG" else (method + ("/merged" if merged else ""))
 
     pl = config.role("preconditioner")
     desc = _lib.mrs_plan_desc()
-    desc.method = _lib.METHOD_CG if family == "CG" else _lib.METHOD_BICGSTAB
+    desc.method = {"CG": _lib.METHOD_CG, "BiCGStab": _lib.METHOD_BICGSTAB,
+                   "RBiCGStab": _lib.METHOD_RBICGSTAB,
+                   "PBiCGStab": _lib.METHOD_PBICGSTAB}[method if family == "BiCGStab" else "CG"]
+    desc.drift_limit = DRIFT_LIMIT
     desc.nrows = Ab.nrows
     desc.rel_tol = tol
     desc.max_iters = iters

@@ -168,9 +168,112 @@ def test_device_tensor_run_matches_host_run():
 def test_unsupported_configs_raise():
     A, _ = gen_poisson3d(4, 4, 4)
     with pytest.raises(ConfigurationError):
-        prepare(tree({"solver": {"method": "PBiCGStab"}}), A)
+        prepare(tree({"solver": {"method": "Direct"}}), A)
     with pytest.raises(ConfigurationError):
         prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"}}), A)
+
+
+VARIANTS = ("BiCGStab", "RBiCGStab", "PBiCGStab")
+
+
+@pytest.mark.parametrize("method", VARIANTS)
+def test_bicgstab_variant_names_and_merged(method):
+    """SolveStats.method as the reference names it; merged=1 is bitwise the
+    same iterate sequence for the reordered and pipelined forms
+    (tests/test_solvers.py:461-471)."""
+    A, b = gen_poisson3d(8, 8, 8)
+    out = []
+    for merged in ("0", "1"):
+        x = BlockVector.zeros(512, 1)
+        st = solve(tree({"solver": {"method": method, "merged": merged,
+                                    "rel_tolerance": "1e-10"}}), A, b, x)
+        assert st.method == method + ("/merged" if merged == "1" else "")
+        assert st.all_converged
+        out.append(x.data.copy())
+    if method != "BiCGStab":
+        np.testing.assert_array_equal(out[0], out[1])
+
+
+@pytest.mark.parametrize("system", ["poisson16", "sdd150"])
+def test_bicgstab_variant_equivalence(system):
+    """tests/test_acceptance.py:139-171: the first 10 residual-history entries
+    of the variants agree with the classical one within 1e-6 relative and the
+    solutions within 1e-8."""
+    rng = np.random.default_rng(11)
+    if system == "poisson16":
+        A, b = gen_poisson3d(16, 16, 16)
+        B = b.data
+    else:
+        n = 150
+        a = rng.standard_normal((n, n)) * (rng.random((n, n)) < 0.1)
+        a += np.diag(np.abs(a).sum(axis=1) + 1.0)
+        A, B = CsrBlock.from_dense(a), rng.standard_normal((n, 1))
+    hist, sols = [], []
+    for method, merged in (("BiCGStab", "0"), ("RBiCGStab", "0"), ("PBiCGStab", "0"),
+                           ("BiCGStab", "1")):
+        x = BlockVector.zeros(A.nrows, 1)
+        st = solve(tree({"solver": {"method": method, "merged": merged, "rel_tolerance": "1e-10",
+                                    "max_iters": "200"}}), A, BlockVector.from_array(B), x)
+        assert st.all_converged
+        hist.append(np.array([h[0] for h in st.residual_history[:11]]))
+        sols.append(x.data.copy())
+    for h, xv in zip(hist[1:], sols[1:]):
+        k = min(len(h), len(hist[0]))
+        assert np.max(np.abs(h[:k] - hist[0][:k]) / np.abs(hist[0][:k])) <= 1e-6
+        assert np.max(np.abs(xv - sols[0])) <= 1e-8
+
+
+@pytest.mark.parametrize("method", VARIANTS)
+def test_bicgstab_variants_breakdown_column(method):
+    """r0 orthogonal to A r0 in column 0 (tests/test_solvers.py:158-165)."""
+    a = np.array([[0.0, 1.0], [1.0, 0.0]])
+    b = np.array([[1.0, 3.0], [0.0, 4.0]])
+    with pytest.raises(BreakdownError) as ei:
+        solve(tree({"solver": {"method": method}}), CsrBlock.from_dense(a),
+              BlockVector.from_array(b), BlockVector.zeros(2, 2))
+    assert ei.value.column == 0
+
+
+def test_pipelined_drift_check_raises(monkeypatch):
+    """tests/test_solvers.py:176-185: with DRIFT_LIMIT below the rounding
+    noise the device cross-check fires (InstabilityError), and the default
+    limit is the reference's 1e3."""
+    from paper_2103_07329_b200 import solvers as S
+    from paper_2103_07329_b200.errors import InstabilityError
+    assert S.DRIFT_LIMIT == 1e3
+    A, b = gen_poisson3d(8, 8, 8)
+    monkeypatch.setattr(S, "DRIFT_LIMIT", 1e-12)
+    for mode in ("graph", "eager"):
+        with pytest.raises(InstabilityError):
+            prepare(tree({"solver": {"method": "PBiCGStab", "rel_tolerance": "1e-10"}}), A,
+                    exec_mode=mode).run(b, BlockVector.zeros(512, 1))
+
+
+@pytest.mark.parametrize("method", ["RBiCGStab", "PBiCGStab"])
+def test_variants_multi_rhs_column_independence(method):
+    """tests/test_acceptance.py:95-136 (criterion 2) for the reordered and
+    pipelined forms: joint solves equal per-column solves within 1e-10."""
+    A, _ = gen_poisson3d(16, 16, 16)
+    B = np.random.default_rng(913).standard_normal((A.nrows, 4))
+    cs = prepare(tree({"solver": {"method": method, "rel_tolerance": "0", "max_iters": "10"}}), A)
+    X = BlockVector.zeros(A.nrows, 4)
+    cs.run(BlockVector.from_array(B), X)
+    for j in range(4):
+        xj = BlockVector.zeros(A.nrows, 1)
+        cs.run(BlockVector.from_array(B[:, j:j + 1].copy()), xj)
+        assert np.max(np.abs(X.data[:, j] - xj.data[:, 0])) <= 1e-10
+
+
+def test_amg_pbicgstab_iteration_budget():
+    """tests/test_solvers.py:384-398: AMG (Chebyshev-2) PBiCGStab on 16^3
+    converges within 20 iterations."""
+    A, b = gen_poisson3d(16, 16, 16)
+    x = BlockVector.zeros(16 ** 3, 1)
+    st = solve(tree({"solver": {"method": "PBiCGStab", "rel_tolerance": "1e-8"},
+                     "preconditioner": {"method": "MultiGrid", "mg_coarse_matrix_size": "500"},
+                     "pre_smoother": {"method": "Chebyshev", "polynomial_order": "2"},
+                     "post_smoother": {"method": "Chebyshev", "polynomial_order": "2"}}), A, b, x)
+    assert st.all_converged and st.iterations <= 20
 
 
 @pytest.mark.parametrize("m", [1, 2, 3, 16, 32, 64])

@@ -29,6 +29,11 @@ CASES = {
                            "pre_smoother": CHEB, "post_smoother": CHEB},
     "jacobi_pcg": {"solver": {"method": "CG", "max_iters": "500"},
                    "preconditioner": {"method": "Jacobi"}},
+    "amg_rbicgstab": {"solver": {"method": "RBiCGStab"}, "preconditioner": {"method": "MultiGrid"},
+                      "pre_smoother": JAC, "post_smoother": JAC},
+    "amg_pbicgstab": {"solver": {"method": "PBiCGStab"},
+                      "preconditioner": {"method": "MultiGrid", "mg_coarse_matrix_size": "100"},
+                      "pre_smoother": CHEB, "post_smoother": CHEB},
 }
 
 

@@ -89,6 +89,8 @@ def _solve_case(name, g):
         precond = O.JacobiPrecond(A, float(pre.get("weight", 1.0)), int(pre.get("max_iters", 1)))
     elif pre and pre["method"] == "MultiGrid":
         h = setup(A, coarse_size=int(pre.get("mg_coarse_matrix_size", 500)),
+                  agg_num_levels=int(pre.get("mg_agg_num_levels", 0)),
+                  num_paths=int(pre.get("mg_num_paths", 1)),
                   mixed=bool(int(pre.get("mg_mixed_precision", 0))))
         def spec(r):
             d = roles[r]
@@ -96,14 +98,18 @@ def _solve_case(name, g):
                 return ("jacobi", float(d.get("weight", 1.0)), int(d.get("max_iters", 1)))
             return ("chebyshev", int(d.get("polynomial_order", 2)))
         precond = O.MultiGrid(h, spec("pre_smoother"), spec("post_smoother"))
-    drv = O.cg_solve if sp_["method"] == "CG" else O.bicgstab_solve
-    st = drv(A, B, X, precond, tol, 100)
+    drv = {"CG": O.cg_solve, "BiCGStab": O.bicgstab_solve, "RBiCGStab": O.rbicgstab_solve,
+           "PBiCGStab": O.pbicgstab_solve}[sp_["method"]]
+    st = drv(A, B, X, precond, tol, int(sp_.get("max_iters", 100)))
     return st, X
 
 
-@pytest.mark.parametrize("name", ["c1_jacobi_pcg", "c2_amg_pcg", "c3_amg_bicgstab_mixed",
-                                  "c2_amg_pcg_20", "plain_bicgstab", "plain_cg",
-                                  "c3_amg_bicgstab_full_cheb3"])
+def _cases():
+    import oracle.gen_golden as GG
+    return list(GG.SOLVE_CASES)
+
+
+@pytest.mark.parametrize("name", _cases())
 def test_oracle_solves_match_reference(golden_solves, name):
     g = golden_solves
     st, X = _solve_case(name, g)
