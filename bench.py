@@ -69,6 +69,22 @@ CONFIGS = {
                "preconditioner": {"method": "MultiGrid"},
                "pre_smoother": _JAC, "post_smoother": _JAC}),
 }
+# the same C3 problem through the reordered / pipelined formulations
+# and the paper's Fig. 3 solver (PBiCGStab + AMG with
+# aggressive coarsening on two levels, tests/test_acceptance.py:206-214)
+for _v in ("RBiCGStab", "PBiCGStab"):
+    _c = dict(CONFIGS["c3"])
+    _c["roles"] = dict(_c["roles"], solver={"method": _v, "rel_tolerance": "1e-8"})
+    _c["workload"] = _c["workload"].replace("+ BiCGStab", f"+ {_v}")
+    CONFIGS["c3" + _v[0].lower()] = _c
+CONFIGS["fig3"] = dict(grid=128, m=16, workload=(
+    "Fig. 3 solver on 3D Poisson 7-pt 128^3, m=16 seeded RHS, zero guess: PBiCGStab + RS AMG "
+    "(aggressive coarsening on 2 levels, 2 paths, coarse <= 500) V(1,1) Chebyshev-2, fp64, "
+    "tol 1e-8"),
+    roles={"solver": {"method": "PBiCGStab", "rel_tolerance": "1e-8"},
+           "preconditioner": {"method": "MultiGrid", "mg_agg_num_levels": "2",
+                              "mg_coarse_matrix_size": "500", "mg_num_paths": "2"},
+           "pre_smoother": _CHEB, "post_smoother": _CHEB})
 CFG = CONFIGS["c2"]
 GRID, M = CFG["grid"], CFG["m"]
 WORKLOAD, ROLES = CFG["workload"], CFG["roles"]
