@@ -261,12 +261,25 @@ def gen_eig(ms):
     np.savez_compressed(os.path.join(OUT, "eig.npz"), **out)
 
 
+def gen_sysfile(ms):
+    """An XAMGBIN1 file written by the reference's own write_system
+    (io.py:46-68): pins our reader and writer byte for byte."""
+    from mrsolve.core import BlockVector
+    from mrsolve.io import gen_poisson3d, write_system
+    A, _ = gen_poisson3d(3, 2, 2)
+    rng = np.random.default_rng(41)
+    rhs = BlockVector.from_array(rng.standard_normal((A.nrows, 3)))
+    guess = BlockVector.from_array(rng.standard_normal((A.nrows, 3)))
+    write_system(os.path.join(OUT, "xamgbin1_ref.bin"), A, rhs, guess)
+
+
 def main():
     """All fixtures, or only the named groups (e.g. ``gen_golden.py solves``)."""
     ms = import_reference()
     assert ms.kernels.BACKEND == "cython", ms.kernels.BACKEND
     os.makedirs(OUT, exist_ok=True)
-    want = set(sys.argv[1:]) or {"kernels", "generators", "eig", "solves", "hierarchies"}
+    want = set(sys.argv[1:]) or {"kernels", "generators", "eig", "solves", "hierarchies",
+                                 "sysfile"}
     if "kernels" in want:
         gen_kernels(ms, np.random.default_rng(20240817))
     if "generators" in want:
@@ -277,6 +290,8 @@ def main():
         gen_solves(ms)
     if "hierarchies" in want:
         gen_hierarchies(ms)
+    if "sysfile" in want:
+        gen_sysfile(ms)
     for f in sorted(os.listdir(OUT)):
         print(f, os.path.getsize(os.path.join(OUT, f)))
 

@@ -20,8 +20,14 @@ import numpy as np
 
 from .core import CsrBlock, BlockVector
 from .errors import InvalidArgumentError
+# XAMGBIN1 system files and YAML run configurations (reference io.py:46-149,
+# :205-283) live in sysfile.py; re-exported here under the reference's names
+from .sysfile import (MAGIC, BenchmarkSpec, SystemSpec, parse_run_config,  # noqa: F401
+                      read_system, write_system)
 
-__all__ = ["gen_poisson3d", "gen_stencil27_aniso", "gen_random_sdd", "seeded_rhs"]
+__all__ = ["gen_poisson3d", "gen_stencil27_aniso", "gen_random_sdd", "seeded_rhs",
+           "MAGIC", "read_system", "write_system", "SystemSpec", "BenchmarkSpec",
+           "parse_run_config"]
 
 
 def _block(n, ncols, indptr, indices, data):
