@@ -77,6 +77,13 @@ for _v in ("RBiCGStab", "PBiCGStab"):
     _c["roles"] = dict(_c["roles"], solver={"method": _v, "rel_tolerance": "1e-8"})
     _c["workload"] = _c["workload"].replace("+ BiCGStab", f"+ {_v}")
     CONFIGS["c3" + _v[0].lower()] = _c
+# C2 with the reference's DEFAULT MultiGrid smoother (one symmetric hybrid
+# Gauss-Seidel sweep, exact sequential order by level scheduling)
+CONFIGS["c2g"] = dict(CONFIGS["c2"], workload=(
+    "C2 system (3D Poisson 7-pt 64^3, m=8 seeded RHS, zero guess) with the reference-default "
+    "MultiGrid smoother: RS AMG V(1,1) symmetric Gauss-Seidel + PCG, fp64, tol 1e-8"),
+    roles={"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+           "preconditioner": {"method": "MultiGrid"}})
 CONFIGS["fig3"] = dict(grid=128, m=16, workload=(
     "Fig. 3 solver on 3D Poisson 7-pt 128^3, m=16 seeded RHS, zero guess: PBiCGStab + RS AMG "
     "(aggressive coarsening on 2 levels, 2 paths, coarse <= 500) V(1,1) Chebyshev-2, fp64, "

@@ -112,6 +112,15 @@ int mrs_fused_update_dot2(int64_t n, int64_t m, double* y, const double* u,
                           const double* c, const double* w, const double* z,
                           double* d1, double* d2, void* stream);
 
+/* _ckernels.pyx:60-79 gs_sweep: one Gauss-Seidel half-sweep (forward != 0:
+ * rows ascending) in place on x, v = b - c, v -= a_ik x_k for k != diag_pos[i]
+ * in entry order, x_i = v / a_ii -- bitwise the sequential sweep (level
+ * scheduled, sgs.cuh).  Square A; diag_pos int64[nrows] (device); b, c, x
+ * (nrows, m) float64 device, m <= 256.  Synchronous on `stream` (the level
+ * schedule is built on the host per call). */
+int mrs_gs_sweep(const mrs_csr* A, const int64_t* diag_pos, const double* b,
+                 const double* c, double* x, int64_t m, int32_t forward, void* stream);
+
 /* ---- 2. solver plan (src/solvers.py:850-959) ---------------------------- */
 
 #define MRS_METHOD_CG        0
@@ -122,15 +131,24 @@ int mrs_fused_update_dot2(int64_t n, int64_t m, double* y, const double* u,
 #define MRS_PC_NONE     0
 #define MRS_PC_JACOBI   1        /* _SweepPrecond(jacobi), solvers.py:716-726,782-788 */
 #define MRS_PC_MG       2        /* MultiGrid V-cycle, solvers.py:615-675 */
+#define MRS_PC_SGS      3        /* _SweepPrecond(sgs_sweep), solvers.py:792-797 */
 
 #define MRS_SMOOTH_JACOBI     0  /* blas2.jacobi_sweep, blas2.py:165-185 */
 #define MRS_SMOOTH_CHEBYSHEV  1  /* solvers.chebyshev_apply, solvers.py:520-571 */
+#define MRS_SMOOTH_SGS        2  /* blas2.sgs_sweep (hybrid Gauss-Seidel, one leaf:
+                                    exact sequential order), blas2.py:113-162; the
+                                    reference's default MultiGrid smoother */
+
+#define MRS_SGS_SYMMETRIC 0      /* forward then backward half-sweep */
+#define MRS_SGS_FORWARD   1
+#define MRS_SGS_BACKWARD  2
 
 typedef struct {
     int32_t kind;        /* MRS_SMOOTH_* */
     int32_t sweeps;      /* Jacobi: sweeps per application (max_iters) */
     double  weight;      /* Jacobi omega */
     int32_t order;       /* Chebyshev polynomial order */
+    int32_t direction;   /* Gauss-Seidel: MRS_SGS_* */
 } mrs_smoother;
 
 typedef struct {
@@ -153,6 +171,7 @@ typedef struct {
                             replaces rnorm in the omega breakdown test */
     double  drift_limit; /* PBiCGStab: ||true r|| / ||recurrence r|| above this raises
                             MRS_ERR_INSTABILITY (solvers.py:68, :415-423); 0 = 1e3 */
+    int32_t pc_direction;/* MRS_PC_SGS: MRS_SGS_* (sweeps = pc_sweeps) */
 } mrs_plan_desc;
 
 typedef struct mrs_plan mrs_plan;

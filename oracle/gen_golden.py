@@ -155,6 +155,20 @@ SOLVE_CASES = {
     "pbicgstab_jacobi_merged": ((12, 12, 12), 2, 8, {
         "solver": {"method": "PBiCGStab", "rel_tolerance": "1e-8", "merged": "1"},
         "preconditioner": {"method": "Jacobi"}}),
+    # hybrid Gauss-Seidel: the reference's DEFAULT
+    # MultiGrid smoother, explicit directions / sweeps, and a GS preconditioner
+    "amg_pcg_default_sgs": ((12, 12, 12), 2, 9, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "MultiGrid"}}),
+    "amg_bicgstab_gs_mixed": ((12, 10, 8), 3, 10, {
+        "solver": {"method": "BiCGStab", "rel_tolerance": "1e-8"},
+        "preconditioner": {"method": "MultiGrid", "mg_mixed_precision": "1",
+                           "mg_coarse_matrix_size": "60"},
+        "pre_smoother": {"method": "Gauss-Seidel", "direction": "forward", "max_iters": "2"},
+        "post_smoother": {"method": "Gauss-Seidel", "direction": "backward"}}),
+    "sgs_precond_cg": ((10, 10, 10), 2, 11, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-9"},
+        "preconditioner": {"method": "Gauss-Seidel"}}),
 }
 
 

@@ -20,8 +20,9 @@ MRS_ERR_BREAKDOWN, MRS_ERR_SINGULAR, MRS_ERR_DEGENERATE, MRS_ERR_STATE = 5, 6, 7
 MRS_ERR_INSTABILITY = 9
 
 METHOD_CG, METHOD_BICGSTAB, METHOD_RBICGSTAB, METHOD_PBICGSTAB = 0, 1, 2, 3
-PC_NONE, PC_JACOBI, PC_MG = 0, 1, 2
-SMOOTH_JACOBI, SMOOTH_CHEBYSHEV = 0, 1
+PC_NONE, PC_JACOBI, PC_MG, PC_SGS = 0, 1, 2, 3
+SMOOTH_JACOBI, SMOOTH_CHEBYSHEV, SMOOTH_SGS = 0, 1, 2
+SGS_DIRECTIONS = {"symmetric": 0, "forward": 1, "backward": 2}
 
 
 class mrs_csr(C.Structure):
@@ -40,7 +41,7 @@ class mrs_host_csr(C.Structure):
 
 class mrs_smoother(C.Structure):
     _fields_ = [("kind", C.c_int32), ("sweeps", C.c_int32), ("weight", C.c_double),
-                ("order", C.c_int32)]
+                ("order", C.c_int32), ("direction", C.c_int32)]
 
 
 class mrs_plan_desc(C.Structure):
@@ -48,7 +49,8 @@ class mrs_plan_desc(C.Structure):
                 ("m", C.c_int64), ("rel_tol", C.c_double), ("max_iters", C.c_int32),
                 ("pc_weight", C.c_double), ("pc_sweeps", C.c_int32), ("mg_cycles", C.c_int32),
                 ("pre", mrs_smoother), ("post", mrs_smoother), ("nlevels", C.c_int32),
-                ("exec", C.c_int32), ("merged", C.c_int32), ("drift_limit", C.c_double)]
+                ("exec", C.c_int32), ("merged", C.c_int32), ("drift_limit", C.c_double),
+                ("pc_direction", C.c_int32)]
 
 
 class mrs_stats(C.Structure):
@@ -77,6 +79,8 @@ SIGNATURES = {
     "mrs_dot": (C.c_int, [C.c_int64, C.c_int64] + [C.c_void_p] * 4),
     "mrs_fused_update_dot": (C.c_int, [C.c_int64, C.c_int64] + [C.c_void_p] * 6),
     "mrs_fused_update_dot2": (C.c_int, [C.c_int64, C.c_int64] + [C.c_void_p] * 8),
+    "mrs_gs_sweep": (C.c_int, [C.POINTER(mrs_csr), C.c_void_p, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]),
     "mrs_plan_create": (C.c_int, [C.POINTER(mrs_plan_desc), C.POINTER(C.c_void_p)]),
     "mrs_plan_set_level": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(mrs_host_csr),
                                      C.POINTER(mrs_host_csr), C.POINTER(mrs_host_csr),

@@ -116,6 +116,7 @@ __device__ __forceinline__ void block_reduce_cols(double (&acc)[K], int m, doubl
 // Zero-guess smoother seed of a produced value v with row diagonal d
 // (spmm.cuh seed_value).
 __device__ __forceinline__ double seed_of(const VArgs& A, double v, double d) {
+    if (A.seed == 3) return 0.0;                       // Gauss-Seidel: x = 0
     return A.seed == 1 ? mul(A.seed_w, divd(v, d)) : divd(v, mul(d, A.seed_w));
 }
 

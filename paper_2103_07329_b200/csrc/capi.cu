@@ -7,8 +7,11 @@
 // the caller's stream.
 #include <cstdint>
 #include <cstring>
+#include <vector>
 
 #include "dispatch.h"
+#include "sgs.cuh"
+#include "sgs_sched.h"
 
 using namespace mrs;
 
@@ -129,6 +132,85 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_
     // unaligned views fall back to the scalar-per-column kernel
     bool vec_ok = aligned16(x) && aligned16(y) && (!b || aligned16(b));
     cudaError_t e = launch_spmm(OP_SPMV, D, a, m, (cudaStream_t)stream, !vec_ok && m > 1);
+    return e == cudaSuccess ? MRS_OK : MRS_ERR_CUDA;
+}
+
+// _ckernels.pyx:60-79 (gs_sweep): one Gauss-Seidel half-sweep over all rows in
+// the sequential order, v = b - c, v -= a_ik x_k (k != diag_pos), x_i = v / a_ii.
+// Synchronous on `stream`: the level schedule (sgs_sched.h) is built on the
+// host from the device structure on every call; solver plans build theirs once.
+int mrs_gs_sweep(const mrs_csr* A, const int64_t* diag_pos, const double* b, const double* c,
+                 double* x, int64_t m, int32_t forward, void* stream) {
+    if (!A || !diag_pos || !b || !c || !x || m < 1 || m > kThreads) return MRS_ERR_ARG;
+    if (A->idx_bytes != 1 && A->idx_bytes != 2 && A->idx_bytes != 4) return MRS_ERR_ARG;
+    if (A->val_bytes != 4 && A->val_bytes != 8) return MRS_ERR_ARG;
+    if (A->nrows < 0 || A->nnz < 0 || A->nnz > INT32_MAX || A->ncols != A->nrows) return MRS_ERR_ARG;
+    if (A->slab_base && (A->idx_bytes != 2 || A->slab_shift < 0 || A->slab_shift > 30))
+        return MRS_ERR_ARG;
+    if (m % 2 == 0 && !(aligned16(b) && aligned16(c) && aligned16(x))) return MRS_ERR_ARG;
+    const int64_t n = A->nrows, nnz = A->nnz;
+    if (n == 0) return MRS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    MRS_CUDA_OK(cudaStreamSynchronize(s));
+    std::vector<int32_t> rp32(n + 1);
+    std::vector<uint8_t> ci((size_t)nnz * A->idx_bytes), vals((size_t)nnz * A->val_bytes);
+    std::vector<int64_t> dp(n);
+    std::vector<int32_t> sb;
+    MRS_CUDA_OK(cudaMemcpy(rp32.data(), A->row_ptr, (n + 1) * 4, cudaMemcpyDeviceToHost));
+    MRS_CUDA_OK(cudaMemcpy(ci.data(), A->col_idx, ci.size(), cudaMemcpyDeviceToHost));
+    MRS_CUDA_OK(cudaMemcpy(vals.data(), A->values, vals.size(), cudaMemcpyDeviceToHost));
+    MRS_CUDA_OK(cudaMemcpy(dp.data(), diag_pos, n * 8, cudaMemcpyDeviceToHost));
+    if (A->slab_base) {
+        sb.resize(((n - 1) >> A->slab_shift) + 1);
+        MRS_CUDA_OK(cudaMemcpy(sb.data(), A->slab_base, sb.size() * 4, cudaMemcpyDeviceToHost));
+    }
+    std::vector<int64_t> rp(rp32.begin(), rp32.end());
+    const int ib = A->idx_bytes;
+    auto col = [&](int64_t i, int64_t k) -> int64_t {
+        int64_t cc = ib == 4 ? ((const uint32_t*)ci.data())[k]
+                   : ib == 2 ? ((const uint16_t*)ci.data())[k] : ci[k];
+        return A->slab_base ? cc + sb[i >> A->slab_shift] : cc;
+    };
+    std::vector<int32_t> dp32(n), order, lptr, ci16;
+    std::vector<double> d(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (dp[i] < rp[i] || dp[i] >= rp[i + 1]) return MRS_ERR_ARG;
+        dp32[i] = (int32_t)dp[i];
+        d[i] = A->val_bytes == 8 ? ((const double*)vals.data())[dp[i]]
+                                 : (double)((const float*)vals.data())[dp[i]];
+    }
+    sgs_levels(n, rp.data(), col, forward ? 0 : 1, order, lptr);
+    // temporaries: schedule, diagonal, u8 columns widened to u16
+    void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    auto release = [&]() { for (void* q : buf) if (q) cudaFree(q); };
+    const size_t sz[5] = {order.size() * 4, lptr.size() * 4, (size_t)n * 4, (size_t)n * 8,
+                          ib == 1 ? (size_t)nnz * 2 : 0};
+    for (int q = 0; q < 5; ++q)
+        if (sz[q] && cudaMalloc(&buf[q], sz[q]) != cudaSuccess) { release(); return MRS_ERR_ALLOC; }
+    const void* cols = A->col_idx;
+    int ibd = ib;
+    bool ok = cudaMemcpy(buf[0], order.data(), sz[0], cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(buf[1], lptr.data(), sz[1], cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(buf[2], dp32.data(), sz[2], cudaMemcpyHostToDevice) == cudaSuccess &&
+              cudaMemcpy(buf[3], d.data(), sz[3], cudaMemcpyHostToDevice) == cudaSuccess;
+    if (ok && ib == 1) {
+        std::vector<uint16_t> w(ci.begin(), ci.end());
+        ok = cudaMemcpy(buf[4], w.data(), sz[4], cudaMemcpyHostToDevice) == cudaSuccess;
+        cols = buf[4];
+        ibd = 2;
+    }
+    if (!ok) { release(); return MRS_ERR_CUDA; }
+    SgsArgs a;
+    memset(&a, 0, sizeof(a));
+    a.rp = A->row_ptr; a.ci = cols; a.vals = A->values;
+    a.slab_base = A->slab_base; a.slab_shift = A->slab_shift;
+    a.order = (const int32_t*)buf[0]; a.lptr = (const int32_t*)buf[1];
+    a.nlev = (int)lptr.size() - 1;
+    a.dpos = (const int32_t*)buf[2]; a.d = (const double*)buf[3];
+    a.b = b; a.c = c; a.x = x; a.m = (int)m;
+    cudaError_t e = launch_sgs(a, A->val_bytes, ibd, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    release();
     return e == cudaSuccess ? MRS_OK : MRS_ERR_CUDA;
 }
 

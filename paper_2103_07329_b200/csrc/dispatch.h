@@ -46,6 +46,9 @@ cudaError_t launch_tail(const TailStep* steps, int nsteps, int64_t m, const int*
 int tail_cluster_size(int64_t m);
 int tail_rows_threshold();
 void set_tail_rows(int64_t v);
+// Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
+struct SgsArgs;
+cudaError_t launch_sgs(const SgsArgs& a, int vb, int ib, cudaStream_t s);
 // Grid the reduction kernels use (partials buffer sizing).
 int vec_grid(int64_t n, int64_t m);
 int spmm_grid(int64_t nrows, int64_t m);

@@ -27,6 +27,8 @@
 #include <vector>
 
 #include "comm.h"
+#include "sgs.cuh"
+#include "sgs_sched.h"
 #include "tail.cuh"
 #include "dispatch.h"
 
@@ -52,6 +54,12 @@ struct LevelDev {
     double* r = nullptr;
     double* dva = nullptr;
     double* dvb = nullptr;
+    // Gauss-Seidel: level schedules of the forward [0] / backward [1] sweep
+    int32_t* sgs_order[2] = {nullptr, nullptr};
+    int32_t* sgs_lptr[2] = {nullptr, nullptr};
+    int sgs_nlev[2] = {0, 0};
+    int32_t* dpos = nullptr;   // diagonal entry of each row
+    bool sgs = false;
 };
 
 template <typename T> T* dalloc(size_t n, std::vector<void*>& owned) {
@@ -269,18 +277,38 @@ struct Builder {
         return p.desc.precond == MRS_PC_MG && l == (int)p.L.size() - 1;
     }
 
+    // Gauss-Seidel sweep in place on x (blas2.py:113-162): forward and/or
+    // backward half, each one cluster launch over the level schedule.
+    void sgs_sweep(LevelDev& lv, const double* b, double* x, int direction) {
+        if (rec) { rec_fail = true; return; }
+        const int64_t n = lv.A.nrows;
+        for (int h = 0; h < 2; ++h) {
+            if ((h == 0 && direction == MRS_SGS_BACKWARD) || (h == 1 && direction == MRS_SGS_FORWARD))
+                continue;
+            SgsArgs a;
+            memset(&a, 0, sizeof(a));
+            a.rp = lv.A.rp; a.ci = lv.A.ci; a.vals = lv.A.v;
+            a.slab_base = lv.A.slab_base; a.slab_shift = lv.A.slab_shift;
+            a.order = lv.sgs_order[h]; a.lptr = lv.sgs_lptr[h]; a.nlev = lv.sgs_nlev[h];
+            a.dpos = lv.dpos; a.d = lv.d; a.b = b; a.x = x; a.m = (int)P->m; a.guard = guard;
+            const int vb = lv.A.vb, ib = lv.A.ib;
+            out->push_back([=](cudaStream_t s) { return launch_sgs(a, vb, ib, s); });
+            bytes += lv.A.bytes() + 3 * V(n) + 16.0 * n;
+            kernels++;
+        }
+    }
+
     // Seed a level needs when entered with a zero x (buffers of x given).
     Seed level_seed(int l, const XB& x) const {
         const mrs_plan& p = *P;
         Seed sd;
         if (coarsest(p, l)) return sd;
         const LevelDev& lv = p.L[l];
-        const mrs_smoother& sm = p.desc.precond == MRS_PC_JACOBI
-                                     ? mrs_smoother{MRS_SMOOTH_JACOBI, p.desc.pc_sweeps,
-                                                    p.desc.pc_weight, 0}
-                                     : p.desc.pre;
+        const mrs_smoother sm = pc_smoother(p.desc);
         sd.d = lv.d;
-        if (sm.kind == MRS_SMOOTH_JACOBI) {
+        if (sm.kind == MRS_SMOOTH_SGS) {
+            sd.mode = 3; sd.out = x.cur;            // Gauss-Seidel starts from x = 0
+        } else if (sm.kind == MRS_SMOOTH_JACOBI) {
             sd.mode = 1; sd.out = x.cur; sd.w = sm.weight;
         } else {
             sd.mode = 2; sd.w = 0.5 * (lv.lmax + lv.lmin);
@@ -323,9 +351,22 @@ struct Builder {
         }
     }
 
+    // The smoother a level-0 sweep preconditioner applies, or the MG pre-smoother.
+    static mrs_smoother pc_smoother(const mrs_plan_desc& d) {
+        if (d.precond == MRS_PC_JACOBI) return mrs_smoother{MRS_SMOOTH_JACOBI, d.pc_sweeps, d.pc_weight, 0, 0};
+        if (d.precond == MRS_PC_SGS) return mrs_smoother{MRS_SMOOTH_SGS, d.pc_sweeps, 0.0, 0, d.pc_direction};
+        return d.pre;
+    }
+
     // Smoother on a NONZERO x (post-smoothing; pre-smoothing of later cycles).
     void smooth_nonzero(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x, int dot_epi) {
         const int64_t n = lv.A.nrows;
+        if (sm.kind == MRS_SMOOTH_SGS) {
+            const int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
+            for (int k = 0; k < sweeps; ++k) sgs_sweep(lv, b, x.cur, sm.direction);
+            if (dot_epi >= 0) dot(b, x.cur, n, dot_epi);
+            return;
+        }
         if (sm.kind == MRS_SMOOTH_JACOBI) {
             if (sm.weight == 0.0) {          // blas2.py:487-489: no-op
                 if (dot_epi >= 0) dot(b, x.cur, n, dot_epi);
@@ -356,6 +397,10 @@ struct Builder {
     void smooth_zero_seeded(LevelDev& lv, const double* b, const mrs_smoother& sm, XB& x,
                             int dot_epi) {
         const int64_t n = lv.A.nrows;
+        if (sm.kind == MRS_SMOOTH_SGS) {                 // x.cur = 0 (seed mode 3)
+            smooth_nonzero(lv, b, sm, x, dot_epi);
+            return;
+        }
         if (sm.kind == MRS_SMOOTH_JACOBI) {
             const int sweeps = sm.sweeps < 1 ? 1 : sm.sweeps;
             if (sm.weight != 0.0)
@@ -473,12 +518,11 @@ PCPlan plan_precond(mrs_plan* P, const int* guard, const double* r, double* want
         if (d.precond == MRS_PC_NONE) {
             pc.out = const_cast<double*>(r);
             if (dot_epi >= 0) bd.dot(r, r, P->n, dot_epi);
-        } else if (d.precond == MRS_PC_JACOBI) {
+        } else if (d.precond == MRS_PC_JACOBI || d.precond == MRS_PC_SGS) {
             LevelDev& lv = P->L[0];
             pc.seed = bd.level_seed(0, x);
             if (!producer_seeds) bd.seed_kernel(r, P->n, pc.seed);
-            mrs_smoother sm{MRS_SMOOTH_JACOBI, d.pc_sweeps, d.pc_weight, 0};
-            bd.smooth_zero_seeded(lv, r, sm, x, dot_epi);
+            bd.smooth_zero_seeded(lv, r, Builder::pc_smoother(d), x, dot_epi);
             pc.out = x.cur;
         } else {
             const int cycles = d.mg_cycles < 1 ? 1 : d.mg_cycles;
@@ -885,6 +929,45 @@ int upload_csr(const mrs_host_csr* h, DevCsr& d, std::vector<void*>& owned) {
     return MRS_OK;
 }
 
+// Column of entry k (row i) of a host CSR, decoding slab-relative indices.
+static inline int64_t host_col(const mrs_host_csr* h, int64_t i, int64_t k) {
+    int64_t c = h->idx_bytes == 4 ? ((const uint32_t*)h->col_idx)[k]
+              : h->idx_bytes == 2 ? ((const uint16_t*)h->col_idx)[k]
+                                  : ((const uint8_t*)h->col_idx)[k];
+    if (h->slab_base) c += h->slab_base[i >> h->slab_shift];
+    return c;
+}
+
+// Level schedules of both Gauss-Seidel sweep directions + diagonal positions
+// of a level (sgs.cuh, sgs_sched.h).
+static int build_sgs_schedule(const mrs_host_csr* h, LevelDev& lv, std::vector<void*>& owned) {
+    const int64_t n = h->nrows;
+    std::vector<int32_t> dp(n, -1);
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t k = h->row_ptr[i]; k < h->row_ptr[i + 1]; ++k)
+            if (host_col(h, i, k) == i) { dp[i] = (int32_t)k; break; }
+    for (int64_t i = 0; i < n; ++i)
+        if (dp[i] < 0) return MRS_ERR_SINGULAR;
+    lv.dpos = dalloc<int32_t>(n, owned);
+    if (!lv.dpos) return MRS_ERR_ALLOC;
+    MRS_CUDA_OK(cudaMemcpy(lv.dpos, dp.data(), n * 4, cudaMemcpyHostToDevice));
+    for (int dir = 0; dir < 2; ++dir) {
+        std::vector<int32_t> order, lptr;
+        sgs_levels(n, h->row_ptr, [h](int64_t i, int64_t k) { return host_col(h, i, k); }, dir,
+                   order, lptr);
+        const int32_t nlev = (int32_t)lptr.size() - 1;
+        lv.sgs_order[dir] = dalloc<int32_t>(n, owned);
+        lv.sgs_lptr[dir] = dalloc<int32_t>(nlev + 1, owned);
+        if (!lv.sgs_order[dir] || !lv.sgs_lptr[dir]) return MRS_ERR_ALLOC;
+        MRS_CUDA_OK(cudaMemcpy(lv.sgs_order[dir], order.data(), n * 4, cudaMemcpyHostToDevice));
+        MRS_CUDA_OK(cudaMemcpy(lv.sgs_lptr[dir], lptr.data(), (nlev + 1) * 4,
+                               cudaMemcpyHostToDevice));
+        lv.sgs_nlev[dir] = nlev;
+    }
+    lv.sgs = true;
+    return MRS_OK;
+}
+
 // diagonal of a host CSR in full precision (core.py:500-510); MRS_ERR_SINGULAR
 // when a row has no structural diagonal or a zero diagonal entry.
 int host_diag(const mrs_host_csr* h, std::vector<double>& d) {
@@ -916,7 +999,14 @@ int mrs_plan_create(const mrs_plan_desc* desc, mrs_plan** out) {
     if (!desc || !out) return MRS_ERR_ARG;
     if (desc->m < 1 || desc->m > kMaxM || desc->nrows < 1) return MRS_ERR_ARG;
     if (desc->method < MRS_METHOD_CG || desc->method > MRS_METHOD_PBICGSTAB) return MRS_ERR_UNSUPPORTED;
-    if (desc->precond < MRS_PC_NONE || desc->precond > MRS_PC_MG) return MRS_ERR_UNSUPPORTED;
+    if (desc->precond < MRS_PC_NONE || desc->precond > MRS_PC_SGS) return MRS_ERR_UNSUPPORTED;
+    for (const mrs_smoother* sm : {&desc->pre, &desc->post})
+        if (desc->precond == MRS_PC_MG &&
+            (sm->kind < MRS_SMOOTH_JACOBI || sm->kind > MRS_SMOOTH_SGS ||
+             (sm->kind == MRS_SMOOTH_SGS && (sm->direction < 0 || sm->direction > 2))))
+            return MRS_ERR_UNSUPPORTED;
+    if (desc->precond == MRS_PC_SGS && (desc->pc_direction < 0 || desc->pc_direction > 2))
+        return MRS_ERR_UNSUPPORTED;
     int nl = desc->precond == MRS_PC_MG ? desc->nlevels : 1;
     if (nl < 1) return MRS_ERR_ARG;
     mrs_plan* p = new mrs_plan();
@@ -951,6 +1041,11 @@ int mrs_plan_set_level(mrs_plan* p, int32_t l, const mrs_host_csr* A, const mrs_
         if (!lv.d) return MRS_ERR_ALLOC;
         MRS_CUDA_OK(cudaMemcpy(lv.d, d.data(), d.size() * 8, cudaMemcpyHostToDevice));
     }
+    const mrs_plan_desc& ds = p->desc;
+    const bool sgs_level = (ds.precond == MRS_PC_SGS && l == 0) ||
+                           (ds.precond == MRS_PC_MG && need_diag &&
+                            (ds.pre.kind == MRS_SMOOTH_SGS || ds.post.kind == MRS_SMOOTH_SGS));
+    if (sgs_level && (rc = build_sgs_schedule(A, lv, p->owned))) return rc;
     return MRS_OK;
 }
 
@@ -1017,9 +1112,11 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
             }
             if (!lv.xa || !lv.xb || !lv.r || (l > 0 && !lv.b)) return MRS_ERR_ALLOC;
         }
-    } else if (p->desc.precond == MRS_PC_JACOBI) {
+    } else if (p->desc.precond == MRS_PC_JACOBI || p->desc.precond == MRS_PC_SGS) {
         if (!p->L[0].d) return MRS_ERR_STATE;
     }
+    for (const LevelDev& lv : p->L)
+        if (lv.sgs && p->dist) return MRS_ERR_UNSUPPORTED;   // one-leaf sweep order only
     size_t V = (size_t)p->L[0].vrows * m;   // level-0 Krylov vectors carry the A0 halo
     double** vecs[] = {&p->B, &p->X, &p->r, &p->r0, &p->p, &p->q, &p->v, &p->s,
                        &p->t, &p->ph, &p->sh, &p->z, &p->zt};

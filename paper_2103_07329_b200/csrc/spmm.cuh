@@ -80,7 +80,9 @@ struct SpArgs {
 // Zero-guess smoother seed of a right-hand-side value v at a row with
 // diagonal d: Jacobi's first sweep x = 0 + w*(v/d) (blas2.py:181) or
 // Chebyshev's first step dv = v/(d*theta) (solvers.py:551).
+// Mode 3: Gauss-Seidel starts from x = 0 (no shortcut): the seed is 0.
 __device__ __forceinline__ double seed_value(int mode, double v, double d, double w_or_theta) {
+    if (mode == 3) return 0.0;
     return mode == 1 ? mul(w_or_theta, divd(v, d)) : divd(v, mul(d, w_or_theta));
 }
 

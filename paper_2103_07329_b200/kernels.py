@@ -13,7 +13,6 @@ libmrsolve_b200.so on torch's current CUDA stream:
 * ``dot_partial`` and the fused dots return (m,) float64 CUDA tensors.
 
 There is no CPU fallback: non-CUDA inputs raise ``InvalidArgumentError``.
-``gs_sweep`` (hybrid Gauss-Seidel) is not on the device path.
 """
 
 from __future__ import annotations
@@ -24,7 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib
-from .errors import ConfigurationError, InvalidArgumentError, ShapeMismatchError
+from .errors import InvalidArgumentError, ShapeMismatchError
 
 __all__ = ["BACKEND", "MODE_ASSIGN", "MODE_ADD", "MODE_SUB", "MODE_RSUB", "DeviceCsr",
            "csr_spmv", "axpby", "add2_scaled", "dot_partial", "fused_update_dot",
@@ -217,6 +216,28 @@ def fused_update_dot2(y, u, c, w, z):
     return d1, d2
 
 
-def gs_sweep(*args, **kwargs):
-    raise ConfigurationError("gs_sweep (hybrid Gauss-Seidel) is not on the device path; "
-                             "see SURVEY.md 8(f)")
+def gs_sweep(row_ptr, col_idx, values, diag_pos, b, c, x, forward):
+    """One Gauss-Seidel half-sweep in place on x (_ckernels.pyx:60-79):
+    v = b - c, v -= a_ik x_k for k != diag_pos[i] in entry order, x_i = v / a_ii,
+    rows ascending (``forward``) or descending -- bitwise the sequential
+    sweep, run level by level on one thread-block cluster (csrc/sgs.cuh).
+    ``row_ptr`` may be a DeviceCsr (``col_idx``/``values`` then ignored)."""
+    if isinstance(row_ptr, DeviceCsr):
+        view = row_ptr.view()
+    else:
+        if row_ptr.dtype == torch.int64:
+            row_ptr = row_ptr.to(torch.int32)
+        view = _csr_view(row_ptr, col_idx, values, row_ptr.numel() - 1, row_ptr.numel() - 1)
+    for t, nm in ((b, "b"), (c, "c"), (x, "x")):
+        _vec(t, nm)
+    _same(b, c, x)
+    if x.shape[0] != view.nrows or view.nrows != view.ncols:
+        raise ShapeMismatchError(f"gs_sweep: A {view.nrows}x{view.ncols}, x {tuple(x.shape)}")
+    if not (isinstance(diag_pos, torch.Tensor) and diag_pos.is_cuda):
+        raise InvalidArgumentError("diag_pos must be a CUDA tensor")
+    dp = diag_pos.to(torch.int64).contiguous()
+    if dp.numel() != view.nrows:
+        raise ShapeMismatchError("diag_pos must have one entry per row")
+    _ck(_lib.lib().mrs_gs_sweep(C.byref(view), dp.data_ptr(), b.data_ptr(), c.data_ptr(),
+                                x.data_ptr(), x.shape[1], int(bool(forward)), _stream()),
+        "gs_sweep")

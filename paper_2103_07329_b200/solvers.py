@@ -11,9 +11,12 @@ launch (iteration loop driven on the device; see csrc/solver.cu).
 Device path: solver CG or BiCGStab in its
 three formulations -- classical, reordered (RBiCGStab), pipelined
 (PBiCGStab); merged=0/1 --, preconditioner none / Jacobi / MultiGrid V-cycle,
-smoothers Jacobi or Chebyshev.  Everything else the reference's ParamTree can
-express (Gauss-Seidel smoothing, Direct and stationary solvers) is outside
-this path and raises ConfigurationError -- there is no CPU fallback.
+smoothers Jacobi, Chebyshev or (hybrid, one-leaf) Gauss-Seidel -- the
+reference's default MultiGrid smoother, run in its exact sequential order by
+level scheduling; a Gauss-Seidel sweep preconditioner.  Everything else the
+reference's ParamTree can express (Direct and stationary solvers, Chebyshev or
+BiCGStab as a preconditioner) is outside this path and raises
+ConfigurationError -- there is no CPU fallback.
 """
 
 from __future__ import annotations
@@ -72,19 +75,29 @@ class ConfiguredSolver:
     plan_factory: object = None
 
 
+def _sgs_direction(plist) -> int:
+    d = plist.get_str("direction")
+    if d not in _lib.SGS_DIRECTIONS:          # blas2.py:125-126
+        raise InvalidArgumentError(f"unknown sweep direction {d!r}")
+    return _lib.SGS_DIRECTIONS[d]
+
+
 def _smoother(plist) -> _lib.mrs_smoother:
     if plist is None:
-        raise ConfigurationError(
-            "MultiGrid needs explicit pre/post smoothers on the device path (the reference "
-            "default, hybrid Gauss-Seidel, is not implemented here; SURVEY.md 8(f))")
+        # the reference's MultiGrid default: one symmetric hybrid Gauss-Seidel
+        # sweep (solvers.py:609-612, :630-631)
+        return _lib.mrs_smoother(_lib.SMOOTH_SGS, 1, 0.0, 0, _lib.SGS_DIRECTIONS["symmetric"])
     if plist.method == "Jacobi":
         return _lib.mrs_smoother(_lib.SMOOTH_JACOBI, plist.get_int("max_iters"),
-                                 plist.get_float("weight"), 0)
+                                 plist.get_float("weight"), 0, 0)
     if plist.method == "Chebyshev":
         order = plist.get_int("polynomial_order")
         if order < 1:
             raise InvalidArgumentError("polynomial_order must be >= 1")
-        return _lib.mrs_smoother(_lib.SMOOTH_CHEBYSHEV, 1, 0.0, order)
+        return _lib.mrs_smoother(_lib.SMOOTH_CHEBYSHEV, 1, 0.0, order, 0)
+    if plist.method == "Gauss-Seidel":
+        return _lib.mrs_smoother(_lib.SMOOTH_SGS, plist.get_int("max_iters"), 0.0, 0,
+                                 _sgs_direction(plist))
     raise ConfigurationError(f"smoother {plist.method!r} is not on the device path")
 
 
@@ -280,6 +293,11 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
         desc.precond = _lib.PC_JACOBI
         desc.pc_weight = pl.get_float("weight")
         desc.pc_sweeps = pl.get_int("max_iters")
+        levels = [(Ab, None, None, None)]
+    elif pl.method == "Gauss-Seidel":            # _SweepPrecond(sgs_sweep), solvers.py:792-797
+        desc.precond = _lib.PC_SGS
+        desc.pc_sweeps = pl.get_int("max_iters")
+        desc.pc_direction = _sgs_direction(pl)
         levels = [(Ab, None, None, None)]
     elif pl.method == "MultiGrid":
         if pl.get_str("mg_cycle") != "V":

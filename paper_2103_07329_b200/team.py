@@ -248,6 +248,11 @@ def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: 
     from .errors import ShapeMismatchError
     cfg = _configure(config, A, hierarchy, exec_mode, eig_bounds)
     desc, levels, inv, h, name, Ab = cfg
+    if _lib.PC_SGS == desc.precond or _lib.SMOOTH_SGS in (
+            (desc.pre.kind, desc.post.kind) if desc.precond == _lib.PC_MG else ()):
+        # the reference's hybrid sweep couples leaves through the pre-sweep
+        # iterate; the device sweep implements the one-leaf order only
+        raise ConfigurationError("Gauss-Seidel smoothing is single-GPU only on the device path")
     if exec_mode == "graph":
         # NCCL p2p/collectives are captured into one ordinary graph per
         # iteration (host checks convergence between launches) rather than

@@ -170,7 +170,30 @@ def test_unsupported_configs_raise():
     with pytest.raises(ConfigurationError):
         prepare(tree({"solver": {"method": "Direct"}}), A)
     with pytest.raises(ConfigurationError):
-        prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"}}), A)
+        prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "Chebyshev"}}), A)
+
+
+@pytest.mark.parametrize("mode", ["graph", "eager"])
+def test_default_gauss_seidel_multigrid_matches_oracle(mode):
+    """MultiGrid without explicit smoothers uses the reference default (one
+    symmetric hybrid Gauss-Seidel sweep, solvers.py:609-612): iterations and
+    history against the oracle restatement on a 24^3 problem."""
+    from oracle import oracle as O
+    from oracle.amg_setup import setup as osetup
+    A, _ = gen_poisson3d(24, 24, 24)
+    B = np.random.default_rng(21).uniform(-1, 1, (A.nrows, 4))
+    roles = {"solver": {"method": "CG", "rel_tolerance": "1e-9"},
+             "preconditioner": {"method": "MultiGrid"}}
+    X = BlockVector.zeros(A.nrows, 4)
+    st = prepare(tree(roles), A, exec_mode=mode).run(BlockVector.from_array(B), X)
+    Ao = O.Csr.of(A)
+    mg = O.MultiGrid(osetup(Ao), ("sgs", "symmetric", 1), ("sgs", "symmetric", 1))
+    Xo = np.zeros_like(B)
+    so = O.cg_solve(Ao, B, Xo, mg, 1e-9, 100)
+    assert st.iterations == so.iterations and st.all_converged
+    np.testing.assert_allclose(np.array(st.residual_history), np.array(so.residual_history),
+                               rtol=1e-6, atol=1e-12)
+    assert np.max(np.abs(X.data - Xo)) <= 1e-8 * np.max(np.abs(Xo))
 
 
 VARIANTS = ("BiCGStab", "RBiCGStab", "PBiCGStab")

@@ -87,13 +87,19 @@ def _solve_case(name, g):
     precond = None
     if pre and pre["method"] == "Jacobi":
         precond = O.JacobiPrecond(A, float(pre.get("weight", 1.0)), int(pre.get("max_iters", 1)))
+    elif pre and pre["method"] == "Gauss-Seidel":
+        precond = O.SgsPrecond(A, pre.get("direction", "symmetric"), int(pre.get("max_iters", 1)))
     elif pre and pre["method"] == "MultiGrid":
         h = setup(A, coarse_size=int(pre.get("mg_coarse_matrix_size", 500)),
                   agg_num_levels=int(pre.get("mg_agg_num_levels", 0)),
                   num_paths=int(pre.get("mg_num_paths", 1)),
                   mixed=bool(int(pre.get("mg_mixed_precision", 0))))
         def spec(r):
-            d = roles[r]
+            d = roles.get(r)
+            if d is None:                     # reference default: symmetric hybrid GS
+                return ("sgs", "symmetric", 1)
+            if d["method"] == "Gauss-Seidel":
+                return ("sgs", d.get("direction", "symmetric"), int(d.get("max_iters", 1)))
             if d["method"] == "Jacobi":
                 return ("jacobi", float(d.get("weight", 1.0)), int(d.get("max_iters", 1)))
             return ("chebyshev", int(d.get("polynomial_order", 2)))
