@@ -487,7 +487,7 @@ def main():
     tp = os.path.join(ROOT, "profiles", "roofline_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get(f"spmm_rsub_{args.config}_bytes_per_launch")
+            traffic = json.load(open(tp)).get(f"spmm_rsub_{args.config}_g{GRID}_bytes_per_launch")
         except Exception:
             traffic = None
     roof = {"bound": "hbm", "achieved": kbytes / kt / 1e9, "peak": peak, "unit": "GB/s",

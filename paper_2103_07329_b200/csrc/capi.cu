@@ -207,7 +207,7 @@ int mrs_gs_sweep(const mrs_csr* A, const int64_t* diag_pos, const double* b, con
     a.order = (const int32_t*)buf[0]; a.lptr = (const int32_t*)buf[1];
     a.nlev = (int)lptr.size() - 1;
     a.dpos = (const int32_t*)buf[2]; a.d = (const double*)buf[3];
-    a.b = b; a.c = c; a.x = x; a.m = (int)m;
+    a.b = b; a.c = c; a.x = x; a.m = (int)m; a.nrows = (int)n;
     cudaError_t e = launch_sgs(a, A->val_bytes, ibd, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     release();

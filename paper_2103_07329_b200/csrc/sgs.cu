@@ -35,6 +35,12 @@ static int sgs_cluster_size() {
 
 template <int CPL, typename Tv, typename Ti>
 static cudaError_t sgs_launch_t(const SgsArgs& a, cudaStream_t s) {
+    // one CTA when a schedule level averages at most one CTA pass of rows
+    const int64_t cta_rows = kSgsCta / (a.m / CPL);
+    if ((int64_t)a.nrows <= cta_rows * a.nlev) {
+        sgs_cta_kernel<CPL, Tv, Ti><<<1, kSgsCta, 0, s>>>(a);
+        return cudaGetLastError();
+    }
     const int cs = sgs_cluster_size<CPL, Tv, Ti>();
     if (cs < 1) return cudaErrorLaunchOutOfResources;
     cudaLaunchConfig_t cfg = {};

@@ -40,6 +40,7 @@ struct SgsArgs {
     const double* c;            // off-leaf coupling (plugin gs_sweep); null = 0
     double* x;
     int m;
+    int nrows;
     const int* guard;
 };
 
@@ -99,6 +100,27 @@ __global__ void __launch_bounds__(kThreads) sgs_kernel(SgsArgs a) {
             for (int idx = lo + crank * rpb + rs; idx < hi; idx += csize * rpb)
                 sgs_row<CPL, Tv, Ti>(a, __ldg(a.order + idx), cofs);
         cl.sync();
+    }
+}
+
+// Small or narrow levels (few rows per schedule level, e.g. AMG coarse
+// levels): ONE CTA of kSgsCta threads walks all schedule levels with
+// __syncthreads between them -- a block barrier instead of a cluster
+// barrier, and the level's vectors stay in this SM's L1 (coherent for the
+// block's own writes).
+constexpr int kSgsCta = 1024;
+
+template <int CPL, typename Tv, typename Ti>
+__global__ void __launch_bounds__(kSgsCta) sgs_cta_kernel(SgsArgs a) {
+    if (a.guard && *a.guard) return;
+    const int lpr = a.m / CPL, rpb = kSgsCta / lpr;
+    const int rs = threadIdx.x / lpr, cofs = (threadIdx.x % lpr) * CPL;
+    for (int lev = 0; lev < a.nlev; ++lev) {
+        const int lo = __ldg(a.lptr + lev), hi = __ldg(a.lptr + lev + 1);
+        if (rs < rpb)
+            for (int idx = lo + rs; idx < hi; idx += rpb)
+                sgs_row<CPL, Tv, Ti>(a, __ldg(a.order + idx), cofs);
+        __syncthreads();
     }
 }
 

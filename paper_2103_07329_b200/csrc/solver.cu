@@ -291,6 +291,7 @@ struct Builder {
             a.slab_base = lv.A.slab_base; a.slab_shift = lv.A.slab_shift;
             a.order = lv.sgs_order[h]; a.lptr = lv.sgs_lptr[h]; a.nlev = lv.sgs_nlev[h];
             a.dpos = lv.dpos; a.d = lv.d; a.b = b; a.x = x; a.m = (int)P->m; a.guard = guard;
+            a.nrows = (int)n;
             const int vb = lv.A.vb, ib = lv.A.ib;
             out->push_back([=](cudaStream_t s) { return launch_sgs(a, vb, ib, s); });
             bytes += lv.A.bytes() + 3 * V(n) + 16.0 * n;

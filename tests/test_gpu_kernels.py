@@ -195,15 +195,16 @@ def test_gs_sweep_vs_oracle_bitwise(m, vdt, width, forward, rng):
     np.testing.assert_array_equal(x.cpu().numpy(), ref)
 
 
-def test_gs_sweep_slab_indices_symmetric_pair(rng):
+@pytest.mark.parametrize("m", [4, 16])
+def test_gs_sweep_slab_indices_symmetric_pair(m, rng):
     """Forward + backward on a 7-point operator stored with slab-relative
-    16-bit columns (as the solver uploads it) == the oracle."""
+    16-bit columns (as the solver uploads it) == the oracle.  ~330 rows per
+    schedule level: m=4 runs the one-CTA kernel, m=16 the cluster kernel."""
     from paper_2103_07329_b200.io import gen_poisson3d
     A, _ = gen_poisson3d(20, 20, 180)          # 72k rows: slab-compressed columns
     D = K.DeviceCsr.from_block(A, slab=True)
     assert D.slab_base is not None
     dp = O.diag_positions(O.Csr.of(A))
-    m = 4
     b = rng.standard_normal((A.nrows, m))
     zero = np.zeros_like(b)
     ref = np.zeros_like(b)
