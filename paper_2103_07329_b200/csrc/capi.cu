@@ -180,23 +180,27 @@ int mrs_gs_sweep(const mrs_csr* A, const int64_t* diag_pos, const double* b, con
                                  : (double)((const float*)vals.data())[dp[i]];
     }
     sgs_levels(n, rp.data(), col, forward ? 0 : 1, order, lptr);
+    std::vector<int4> meta(n);
+    for (int64_t q = 0; q < n; ++q) {
+        const int32_t i = order[q];
+        meta[q] = make_int4(i, rp32[i], rp32[i + 1], dp32[i]);
+    }
     // temporaries: schedule, diagonal, u8 columns widened to u16
-    void* buf[5] = {nullptr, nullptr, nullptr, nullptr, nullptr};
+    void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
     auto release = [&]() { for (void* q : buf) if (q) cudaFree(q); };
-    const size_t sz[5] = {order.size() * 4, lptr.size() * 4, (size_t)n * 4, (size_t)n * 8,
+    const size_t sz[4] = {meta.size() * sizeof(int4), lptr.size() * 4, (size_t)n * 8,
                           ib == 1 ? (size_t)nnz * 2 : 0};
-    for (int q = 0; q < 5; ++q)
+    for (int q = 0; q < 4; ++q)
         if (sz[q] && cudaMalloc(&buf[q], sz[q]) != cudaSuccess) { release(); return MRS_ERR_ALLOC; }
     const void* cols = A->col_idx;
     int ibd = ib;
-    bool ok = cudaMemcpy(buf[0], order.data(), sz[0], cudaMemcpyHostToDevice) == cudaSuccess &&
+    bool ok = cudaMemcpy(buf[0], meta.data(), sz[0], cudaMemcpyHostToDevice) == cudaSuccess &&
               cudaMemcpy(buf[1], lptr.data(), sz[1], cudaMemcpyHostToDevice) == cudaSuccess &&
-              cudaMemcpy(buf[2], dp32.data(), sz[2], cudaMemcpyHostToDevice) == cudaSuccess &&
-              cudaMemcpy(buf[3], d.data(), sz[3], cudaMemcpyHostToDevice) == cudaSuccess;
+              cudaMemcpy(buf[2], d.data(), sz[2], cudaMemcpyHostToDevice) == cudaSuccess;
     if (ok && ib == 1) {
         std::vector<uint16_t> w(ci.begin(), ci.end());
-        ok = cudaMemcpy(buf[4], w.data(), sz[4], cudaMemcpyHostToDevice) == cudaSuccess;
-        cols = buf[4];
+        ok = cudaMemcpy(buf[3], w.data(), sz[3], cudaMemcpyHostToDevice) == cudaSuccess;
+        cols = buf[3];
         ibd = 2;
     }
     if (!ok) { release(); return MRS_ERR_CUDA; }
@@ -204,9 +208,9 @@ int mrs_gs_sweep(const mrs_csr* A, const int64_t* diag_pos, const double* b, con
     memset(&a, 0, sizeof(a));
     a.rp = A->row_ptr; a.ci = cols; a.vals = A->values;
     a.slab_base = A->slab_base; a.slab_shift = A->slab_shift;
-    a.order = (const int32_t*)buf[0]; a.lptr = (const int32_t*)buf[1];
+    a.meta = (const int4*)buf[0]; a.lptr = (const int32_t*)buf[1];
     a.nlev = (int)lptr.size() - 1;
-    a.dpos = (const int32_t*)buf[2]; a.d = (const double*)buf[3];
+    a.d = (const double*)buf[2];
     a.b = b; a.c = c; a.x = x; a.m = (int)m; a.nrows = (int)n;
     cudaError_t e = launch_sgs(a, A->val_bytes, ibd, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);

@@ -55,10 +55,9 @@ struct LevelDev {
     double* dva = nullptr;
     double* dvb = nullptr;
     // Gauss-Seidel: level schedules of the forward [0] / backward [1] sweep
-    int32_t* sgs_order[2] = {nullptr, nullptr};
+    int4* sgs_meta[2] = {nullptr, nullptr};   // (row, lo, hi, diag entry), schedule order
     int32_t* sgs_lptr[2] = {nullptr, nullptr};
     int sgs_nlev[2] = {0, 0};
-    int32_t* dpos = nullptr;   // diagonal entry of each row
     bool sgs = false;
 };
 
@@ -289,8 +288,8 @@ struct Builder {
             memset(&a, 0, sizeof(a));
             a.rp = lv.A.rp; a.ci = lv.A.ci; a.vals = lv.A.v;
             a.slab_base = lv.A.slab_base; a.slab_shift = lv.A.slab_shift;
-            a.order = lv.sgs_order[h]; a.lptr = lv.sgs_lptr[h]; a.nlev = lv.sgs_nlev[h];
-            a.dpos = lv.dpos; a.d = lv.d; a.b = b; a.x = x; a.m = (int)P->m; a.guard = guard;
+            a.meta = lv.sgs_meta[h]; a.lptr = lv.sgs_lptr[h]; a.nlev = lv.sgs_nlev[h];
+            a.d = lv.d; a.b = b; a.x = x; a.m = (int)P->m; a.guard = guard;
             a.nrows = (int)n;
             const int vb = lv.A.vb, ib = lv.A.ib;
             out->push_back([=](cudaStream_t s) { return launch_sgs(a, vb, ib, s); });
@@ -939,8 +938,8 @@ static inline int64_t host_col(const mrs_host_csr* h, int64_t i, int64_t k) {
     return c;
 }
 
-// Level schedules of both Gauss-Seidel sweep directions + diagonal positions
-// of a level (sgs.cuh, sgs_sched.h).
+// Level schedules of both Gauss-Seidel sweep directions of a level, as row
+// descriptors in schedule order (sgs.cuh, sgs_sched.h).
 static int build_sgs_schedule(const mrs_host_csr* h, LevelDev& lv, std::vector<void*>& owned) {
     const int64_t n = h->nrows;
     std::vector<int32_t> dp(n, -1);
@@ -949,18 +948,21 @@ static int build_sgs_schedule(const mrs_host_csr* h, LevelDev& lv, std::vector<v
             if (host_col(h, i, k) == i) { dp[i] = (int32_t)k; break; }
     for (int64_t i = 0; i < n; ++i)
         if (dp[i] < 0) return MRS_ERR_SINGULAR;
-    lv.dpos = dalloc<int32_t>(n, owned);
-    if (!lv.dpos) return MRS_ERR_ALLOC;
-    MRS_CUDA_OK(cudaMemcpy(lv.dpos, dp.data(), n * 4, cudaMemcpyHostToDevice));
     for (int dir = 0; dir < 2; ++dir) {
         std::vector<int32_t> order, lptr;
         sgs_levels(n, h->row_ptr, [h](int64_t i, int64_t k) { return host_col(h, i, k); }, dir,
                    order, lptr);
         const int32_t nlev = (int32_t)lptr.size() - 1;
-        lv.sgs_order[dir] = dalloc<int32_t>(n, owned);
+        std::vector<int4> meta(n);
+        for (int64_t q = 0; q < n; ++q) {
+            const int32_t i = order[q];
+            meta[q] = make_int4(i, (int)h->row_ptr[i], (int)h->row_ptr[i + 1], dp[i]);
+        }
+        lv.sgs_meta[dir] = dalloc<int4>(n, owned);
         lv.sgs_lptr[dir] = dalloc<int32_t>(nlev + 1, owned);
-        if (!lv.sgs_order[dir] || !lv.sgs_lptr[dir]) return MRS_ERR_ALLOC;
-        MRS_CUDA_OK(cudaMemcpy(lv.sgs_order[dir], order.data(), n * 4, cudaMemcpyHostToDevice));
+        if (!lv.sgs_meta[dir] || !lv.sgs_lptr[dir]) return MRS_ERR_ALLOC;
+        MRS_CUDA_OK(cudaMemcpy(lv.sgs_meta[dir], meta.data(), n * sizeof(int4),
+                               cudaMemcpyHostToDevice));
         MRS_CUDA_OK(cudaMemcpy(lv.sgs_lptr[dir], lptr.data(), (nlev + 1) * 4,
                                cudaMemcpyHostToDevice));
         lv.sgs_nlev[dir] = nlev;

@@ -49,7 +49,15 @@ def main():
     if len(src) > 2:
         hdr = src[1]
         si = hdr.index("Warp Stall Sampling (All Samples)")
-        data = [r for r in src[2:] if len(r) > si and r[si]]
+        def num(x):
+            try:
+                float(x)
+                return True
+            except ValueError:
+                return False
+        # (the page repeats a header block per profiled kernel: keep number rows;
+        # with several kernels the shares mix them -- profile one kernel for SASS)
+        data = [r for r in src[2:] if len(r) > si and num(r[si])]
         tot = sum(float(r[si]) for r in data) or 1.0
         print("   hottest SASS (share of warp-stall samples):")
         for r in sorted(data, key=lambda r: -float(r[si]))[:12]:
