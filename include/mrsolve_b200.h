@@ -232,6 +232,9 @@ double mrs_plan_iteration_bytes(const mrs_plan* p);
  * bracketed by CUDA events (diagnostics; call after one mrs_plan_solve). */
 int  mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32_t cap,
                       int32_t* count);
+/* Diagnostics: kernel name (mangled) of iteration-body launch `idx` (the
+ * order of mrs_plan_profile). */
+int  mrs_plan_launch_name(mrs_plan* p, int32_t idx, char* buf, int32_t len);
 int  mrs_plan_kernel_count(const mrs_plan* p);   /* kernels per outer iteration */
 int  mrs_plan_fixed_kernel_count(const mrs_plan* p); /* kernels outside the loop */
 void mrs_plan_destroy(mrs_plan* p);

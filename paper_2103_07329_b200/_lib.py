@@ -93,6 +93,7 @@ SIGNATURES = {
     "mrs_plan_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
                                    C.POINTER(C.c_int32)]),
     "mrs_plan_kernel_count": (C.c_int, [C.c_void_p]),
+    "mrs_plan_launch_name": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32]),
     "mrs_plan_fixed_kernel_count": (C.c_int, [C.c_void_p]),
     "mrs_plan_destroy": (None, [C.c_void_p]),
     "mrs_amg_setup": (C.c_int, [C.POINTER(mrs_host_csr), C.POINTER(mrs_amg_params),

@@ -1368,6 +1368,43 @@ int mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32
     cudaEventDestroy(e1);
     return MRS_OK;
 }
+// Name of the (first) kernel body launch `idx` runs, for profiles: the launch
+// is captured into a scratch graph (not executed) and its kernel node read.
+int mrs_plan_launch_name(mrs_plan* p, int32_t idx, char* buf, int32_t len) {
+    if (!p || !p->finalized || !buf || len < 2) return MRS_ERR_ARG;
+    Program pg;
+    build_program(p, true, pg);
+    if (idx < 0 || idx >= (int)pg.body.size()) return MRS_ERR_ARG;
+    cudaStream_t cs;
+    MRS_CUDA_OK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    cudaGraph_t g = nullptr;
+    MRS_CUDA_OK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
+    cudaError_t e = pg.body[idx](cs);
+    cudaError_t e2 = cudaStreamEndCapture(cs, &g);
+    cudaStreamDestroy(cs);
+    if (e != cudaSuccess || e2 != cudaSuccess) return MRS_ERR_CUDA;
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    std::string name = "(no kernel)";
+    for (auto nd : nodes) {
+        cudaGraphNodeType t;
+        cudaGraphNodeGetType(nd, &t);
+        if (t != cudaGraphNodeTypeKernel) continue;
+        cudaKernelNodeParams kp;
+        const char* nm = nullptr;
+        if (cudaGraphKernelNodeGetParams(nd, &kp) == cudaSuccess &&
+            cudaFuncGetName(&nm, kp.func) == cudaSuccess && nm)
+            name = nm;
+        break;
+    }
+    cudaGraphDestroy(g);
+    cudaGetLastError();
+    snprintf(buf, (size_t)len, "%s", name.c_str());
+    return MRS_OK;
+}
+
 int mrs_plan_kernel_count(const mrs_plan* p) { return p ? p->body_kernels : 0; }
 int mrs_plan_fixed_kernel_count(const mrs_plan* p) { return p ? p->fixed_kernels : 0; }
 

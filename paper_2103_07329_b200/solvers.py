@@ -173,6 +173,23 @@ class DevicePlan:
                                            out.ctypes.data, 512, C.byref(n)), "profile")
         return out[:n.value].copy()
 
+    def launch_names(self) -> list:
+        """Demangled kernel name of every iteration-body launch (diagnostics)."""
+        import subprocess
+        out = []
+        buf = C.create_string_buffer(512)
+        for i in range(self.kernels_per_iteration):
+            _lib.check(self.L.mrs_plan_launch_name(self.h, i, buf, 512), "launch name")
+            out.append(buf.value.decode())
+        try:
+            dem = subprocess.run(["c++filt"], input="\n".join(out), capture_output=True,
+                                 text=True, timeout=10).stdout.splitlines()
+            if len(dem) == len(out):
+                out = dem
+        except Exception:
+            pass
+        return out
+
     def kernel_launches(self, iterations: int) -> int:
         """Kernels one solve of `iterations` iterations launches."""
         return self.L.mrs_plan_fixed_kernel_count(self.h) + iterations * self.kernels_per_iteration

@@ -31,9 +31,25 @@ def main():
     plan = cs.plan_factory(bench.M)
     t = plan.profile(3)
     t = plan.profile(3)
+    import re
+    vec_ops = ["axpby", "add2", "paired", "dot", "update_dot", "update_dot2", "copy",
+               "cg_update", "cg_update_jac", "p_update", "seed", "bicg_p", "bicg_s", "dot3",
+               "bicg_xr", "dot2", "dot5", "bicg_xr0", "pbicg_qy", "pbicg_w"]
+    sp_ops = ["SPMV", "JAC_SWEEP", "CHEB_FIRST", "CHEB_STEP"]
+    names = []
+    for nm in plan.launch_names():
+        mv = re.search(r"vec_kernel<(\d+)>", nm)
+        ms = re.search(r"spmm_kernel<(\d+), (\d), ([a-z ]+), ([a-z ]+)>", nm)
+        if mv:
+            nm = f"vec {vec_ops[int(mv.group(1))]}"
+        elif ms:
+            nm = f"spmm m={ms.group(1)} {sp_ops[int(ms.group(2))]} {ms.group(3)} {ms.group(4)}"
+        names.append(nm)
     print(f"{len(t)} launches/iteration, sum {t.sum():.1f} us")
     for i, v in enumerate(t):
-        print(f"{i:3d} {v:8.2f}")
+        nm = names[i] if i < len(names) else ""
+        nm = nm.replace("mrs::", "").replace("unsigned ", "u")
+        print(f"{i:3d} {v:8.2f}  {nm[:110]}")
 
 
 if __name__ == "__main__":
