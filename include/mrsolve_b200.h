@@ -270,6 +270,8 @@ int  mrs_version(void);
 /* Tuning knobs, read when a plan captures its graph:
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
  *   "tail_rows" N  V-cycle levels with <= N rows run as one cluster kernel (0: off)
+ *   "spmm_long_rows" N  operators with <= N rows and >= 12 entries per row run the
+ *                   SpMM with 16 entries in flight per lane (default 20000; 0: off)
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

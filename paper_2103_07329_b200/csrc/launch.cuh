@@ -9,6 +9,8 @@
 
 namespace mrs {
 
+int64_t spmm_long_max_rows();   // LONG-row SpMM variant up to this many rows (knob)
+
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
@@ -77,6 +79,17 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         a.chunk = rpp * sp;
         (void)launch_ex(kern, g, s, a);
     };
+    // small operators with long rows: the LONG variant (16 entries in flight)
+    if (!generic && m <= 16 && a.nrows <= spmm_long_max_rows() && a.nnz_hint >= 12 * a.nrows) {
+        switch (m) {
+        case 1: go(spmm_kernel<1, OP, Tv, Ti, true>, Lay<1>::RPB); return cudaGetLastError();
+        case 2: go(spmm_kernel<2, OP, Tv, Ti, true>, Lay<2>::RPB); return cudaGetLastError();
+        case 4: go(spmm_kernel<4, OP, Tv, Ti, true>, Lay<4>::RPB); return cudaGetLastError();
+        case 8: go(spmm_kernel<8, OP, Tv, Ti, true>, Lay<8>::RPB); return cudaGetLastError();
+        case 16: go(spmm_kernel<16, OP, Tv, Ti, true>, Lay<16>::RPB); return cudaGetLastError();
+        default: break;
+        }
+    }
     switch (generic ? 0 : m) {
     case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
     case 2: go(spmm_kernel<2, OP, Tv, Ti>, Lay<2>::RPB); break;

@@ -314,8 +314,12 @@ template <int M, int OP> constexpr int spmm_min_blocks() {
     return (OP == OP_SPMV || OP == OP_JAC_SWEEP) ? 6 : 5;
 }
 
-template <int M, int OP, typename Tv, typename Ti>
-__global__ void __launch_bounds__(kThreads, spmm_min_blocks<M, OP>()) spmm_kernel(SpArgs a) {
+// LONG: small operators with long rows (AMG coarse levels, >= 12 nnz/row):
+// 16 entries in flight per lane -- the row's dependent chain is 4x shorter;
+// register-heavy, so only used where few CTAs run anyway.  Same order.
+template <int M, int OP, typename Tv, typename Ti, bool LONG = false>
+__global__ void __launch_bounds__(kThreads, LONG ? 1 : spmm_min_blocks<M, OP>())
+spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
     using L = Lay<M>;
@@ -330,7 +334,7 @@ __global__ void __launch_bounds__(kThreads, spmm_min_blocks<M, OP>()) spmm_kerne
     for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gridDim.x * chunk) {
         const int r1 = min(r0 + chunk, nrows);
         for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
-            do_row<OP, CPL, GSrc<Tv, Ti>, L::UNR>(a, src.at_row(a, row), row, __ldg(a.rp + row),
+            do_row<OP, CPL, GSrc<Tv, Ti>, LONG ? 16 : L::UNR>(a, src.at_row(a, row), row, __ldg(a.rp + row),
                                                   __ldg(a.rp + row + 1), M, cofs, dotp);
     }
     if (a.dot) spmm_block_dot<M>(a, dotp);
