@@ -86,6 +86,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!key) return MRS_ERR_ARG;
     if (!strcmp(key, "pdl")) { set_pdl((int)value); return MRS_OK; }
     if (!strcmp(key, "tail_rows")) { set_tail_rows(value); return MRS_OK; }
+    if (!strcmp(key, "coarse_rows")) { set_coarse_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
     return MRS_ERR_ARG;
 }

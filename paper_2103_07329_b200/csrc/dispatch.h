@@ -46,6 +46,7 @@ cudaError_t launch_tail(const TailStep* steps, int nsteps, int64_t m, const int*
 int tail_cluster_size(int64_t m);
 int tail_rows_threshold();
 void set_tail_rows(int64_t v);
+void set_coarse_rows(int64_t v);
 void set_spmm_long_rows(int64_t v);
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;

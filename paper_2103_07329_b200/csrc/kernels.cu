@@ -111,21 +111,22 @@ cudaError_t launch_vec(int op, VArgs a, cudaStream_t s) {
 }
 
 // Coarsest level: x = Ainv b (replaces scipy lu_solve, solvers.py:644-649).
-// CTA handles kRows rows; thread (ks, c) folds k = ks, ks + kpb, ... for
+// CTA handles rows_per_cta rows; thread (ks, c) folds k = ks, ks + kpb, ... for
 // column c, then the ks partials are folded in order (deterministic).
-constexpr int kCoarseRows = 4;
+static int g_coarse_rows = 1;     // rows per CTA of the coarse solve (knob coarse_rows; A/B in profiles)
+void set_coarse_rows(int64_t v) { g_coarse_rows = v < 1 ? 1 : (v > 64 ? 64 : (int)v); }
 
 __global__ void __launch_bounds__(kThreads) coarse_kernel(const double* __restrict__ inv, int64_t nc,
                                                           const double* __restrict__ b,
                                                           double* __restrict__ x, int m,
-                                                          const int* guard) {
+                                                          const int* guard, int rows_per_cta) {
     pdl_enter();
     if (guard && *guard) return;
     __shared__ double s_t[kThreads];
     const int kpb = kThreads / m;
     const int c = threadIdx.x % m, ks = threadIdx.x / m;
-    for (int rr = 0; rr < kCoarseRows; ++rr) {
-        int64_t i = (int64_t)blockIdx.x * kCoarseRows + rr;
+    for (int rr = 0; rr < rows_per_cta; ++rr) {
+        int64_t i = (int64_t)blockIdx.x * rows_per_cta + rr;
         if (i >= nc) break;
         double acc = 0.0;
         if (ks < kpb)
@@ -144,8 +145,9 @@ __global__ void __launch_bounds__(kThreads) coarse_kernel(const double* __restri
 
 cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
                           int64_t m, const int* guard, cudaStream_t s) {
-    int g = (int)((nc + kCoarseRows - 1) / kCoarseRows);
-    (void)launch_ex(coarse_kernel, g, s, inv, nc, b, x, (int)m, guard);
+    const int rpc = g_coarse_rows;
+    int g = (int)((nc + rpc - 1) / rpc);
+    (void)launch_ex(coarse_kernel, g, s, inv, nc, b, x, (int)m, guard, rpc);
     return cudaGetLastError();
 }
 
