@@ -260,13 +260,14 @@ def reference_arm(args, rank):
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": len(runs), "warmup": args.warmup, "ms_per_step": 1e3 * tot / len(runs),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference gen_poisson3d + default_rng(0).uniform(-1,1) RHS",
         "config": {"workload": WORKLOAD, "n": GRID ** 3, "m": M, "iterations": its[0],
                    "parallelism": "1 CPU core (reference kernels hold the GIL)",
                    "setup_s_excluded": res["setup"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": 1, "kind": "reference",
-                         "sample": f"{len(runs)} full C2 solves after {args.warmup} warm-up, "
+                         "sample": f"{len(runs)} full {args.config.upper()} solves after "
+                                   f"{args.warmup} warm-up, "
                                    f"1 of {ncores} host cores, mrsolve backend {res['backend']}"},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
