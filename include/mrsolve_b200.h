@@ -273,6 +273,7 @@ int  mrs_version(void);
  *   "spmm_long_rows" N  operators with <= N rows and >= 12 entries per row run the
  *                   SpMM with 16 entries in flight per lane (default 20000; 0: off)
  *   "coarse_rows" N  rows per CTA of the dense coarse solve (default 1)
+ *   "spmm_chunk_rows" N  rows per CTA chunk of the SpMM grid (default 64)
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

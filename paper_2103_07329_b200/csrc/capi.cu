@@ -88,6 +88,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "tail_rows")) { set_tail_rows(value); return MRS_OK; }
     if (!strcmp(key, "coarse_rows")) { set_coarse_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
+    if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }
     return MRS_ERR_ARG;
 }
 

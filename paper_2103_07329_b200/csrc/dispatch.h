@@ -48,6 +48,7 @@ int tail_rows_threshold();
 void set_tail_rows(int64_t v);
 void set_coarse_rows(int64_t v);
 void set_spmm_long_rows(int64_t v);
+void set_spmm_chunk_rows(int64_t v);
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;
 cudaError_t launch_sgs(const SgsArgs& a, int vb, int ib, cudaStream_t s);

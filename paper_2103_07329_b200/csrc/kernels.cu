@@ -27,6 +27,9 @@ void set_pdl(int on) { g_pdl = on ? 1 : 0; }
 static int64_t g_long_rows = 20000;   // A/B: profiles/r01_ab_experiments.txt
 int64_t spmm_long_max_rows() { return g_long_rows; }
 void set_spmm_long_rows(int64_t v) { g_long_rows = v < 0 ? 0 : v; }
+static int64_t g_chunk_rows = 64;     // A/B: profiles/r01_ab_experiments.txt
+int64_t spmm_chunk_rows() { return g_chunk_rows; }
+void set_spmm_chunk_rows(int64_t v) { g_chunk_rows = v < 1 ? 1 : v; }
 static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }

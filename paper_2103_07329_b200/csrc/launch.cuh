@@ -10,6 +10,7 @@
 namespace mrs {
 
 int64_t spmm_long_max_rows();   // LONG-row SpMM variant up to this many rows (knob)
+int64_t spmm_chunk_rows();      // rows per CTA chunk of the SpMM grid (knob)
 
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
@@ -65,12 +66,15 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     int g;
     auto go = [&](auto kern, int64_t rpp) {
         // Balanced one wave: every CTA gets the same number of passes (the
-        // slowest CTA sets the kernel time), in chunks of <= ~512 rows strided
-        // over the grid (L1 reuse inside a chunk, L2-resident band across).
+        // slowest CTA sets the kernel time), in chunks of ~64 rows strided
+        // over the grid: the active band of the matrix stays narrow (grid x 64
+        // rows), so gathered x rows shared by rows a plane apart are still in
+        // L2 when the later row reads them (scripts/probe/spmm_probe.cu:
+        // 512-row chunks 244 -> 64-row chunks 207 us on the 128^3 m=16 SpMM).
         const int64_t cap = (int64_t)blocks_per_sm((const void*)kern) * num_sms();
         const int64_t P = (a.nrows + rpp - 1) / rpp;             // passes in total
         const int64_t ppc = (P + cap - 1) / cap;                  // passes per CTA
-        const int64_t pmax = rpp >= 512 ? 1 : 512 / rpp;
+        const int64_t pmax = rpp >= spmm_chunk_rows() ? 1 : spmm_chunk_rows() / rpp;
         const int64_t sp = ppc < pmax ? ppc : pmax;               // passes per chunk
         const int64_t nchunks = (P + sp - 1) / sp;
         const int64_t cpc = (nchunks + cap - 1) / cap;            // chunks per CTA
