@@ -185,6 +185,14 @@ int  mrs_plan_set_level(mrs_plan* p, int32_t l, const mrs_host_csr* A,
                         double lmin, double lmax);
 /* Coarsest-level dense inverse, row-major nc x nc float64 (host). */
 int  mrs_plan_set_coarse_inverse(mrs_plan* p, const double* inv, int64_t nc);
+/* Collapsed V-cycle tail (MultiGrid plans, single GPU): level `l` (1 <= l <
+ * nlevels-1) and everything below it, entered with a zero guess, is the
+ * dense row-major n x n float64 operator `op` (n = rows of level l; built at
+ * setup by applying the sub-V-cycle to the unit vectors, amg.py
+ * vcycle_tail_operator).  The solve then runs x_l = op b_l as ONE launch in
+ * place of the level's smoother / residual / transfer kernels and those of
+ * every coarser level (replaces solvers.py:651-664 below level l). */
+int  mrs_plan_set_dense_tail(mrs_plan* p, int32_t l, const double* op, int64_t n);
 int  mrs_plan_finalize(mrs_plan* p, void* stream);
 
 typedef struct {

@@ -86,6 +86,7 @@ SIGNATURES = {
                                      C.POINTER(mrs_host_csr), C.POINTER(mrs_host_csr),
                                      C.c_double, C.c_double]),
     "mrs_plan_set_coarse_inverse": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int64]),
+    "mrs_plan_set_dense_tail": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64]),
     "mrs_plan_finalize": (C.c_int, [C.c_void_p, C.c_void_p]),
     "mrs_plan_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                  C.c_void_p, C.POINTER(mrs_stats), C.c_void_p, C.c_void_p]),

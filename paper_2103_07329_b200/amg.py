@@ -20,7 +20,8 @@ from . import _lib
 from .core import CsrBlock, PrecisionTag, as_csr, choose_width
 from .errors import InvalidArgumentError, SingularDiagonalError
 
-__all__ = ["AmgParams", "Level", "Hierarchy", "setup", "estimate_eig_bounds", "coarse_inverse"]
+__all__ = ["AmgParams", "Level", "Hierarchy", "setup", "estimate_eig_bounds", "coarse_inverse",
+           "vcycle_tail_operator", "dense_tail_level", "set_dense_tail_rows"]
 
 
 @dataclass(frozen=True)
@@ -174,3 +175,125 @@ def coarse_inverse(A) -> np.ndarray:
     if udiag.size and udiag.min() <= 1e-14 * scale:
         raise SingularMatrixError("matrix is singular to working precision")
     return np.ascontiguousarray(scipy.linalg.lu_solve((lu, piv), np.eye(A.nrows), check_finite=False))
+
+
+#: Largest level (rows) the V-cycle tail may be collapsed from (dense n x n
+#: operator, n^2 * 8 bytes); 0 disables.  Env MRS_DENSE_TAIL_ROWS.
+DENSE_TAIL_ROWS = int(__import__("os").environ.get("MRS_DENSE_TAIL_ROWS", "12000"))
+# cost model of the choice (microseconds; B200 measurements, profiles/r01_ab_experiments.txt):
+# a solve-path kernel costs ~_T_LAUNCH plus _T_ROUND per dependent load round of its
+# longest row (16 entries in flight); the dense product streams n^2*8 bytes at _DENSE_BW
+_T_LAUNCH, _T_ROUND, _DENSE_BW = 3.0, 1.0, 1.4e6     # us, us, bytes/us
+
+
+def set_dense_tail_rows(n: int) -> None:
+    """Row cap of the collapsed V-cycle tail (0: per-level kernels)."""
+    global DENSE_TAIL_ROWS
+    DENSE_TAIL_ROWS = max(0, int(n))
+
+
+def _kernel_us(M) -> float:
+    if M is None:
+        return 0.0
+    M = as_csr(M)
+    longest = int(np.diff(M.row_ptr).max()) if M.nrows else 0
+    return _T_LAUNCH + _T_ROUND * 2 * -(-longest // 16)
+
+
+def dense_tail_level(levels, limit=None, pre=None, post=None) -> int:
+    """Level l >= 1 (not the coarsest, at most ``limit`` rows) whose collapsed
+    tail saves the most estimated time per V-cycle, or -1 (none saves).
+
+    Saving of collapsing at l = the per-level kernels of levels l..L-2
+    (smoother + residual sweeps over A_j, the two transfers) and the coarse
+    solve, each ~ launch + dependent load rounds of its longest row;
+    cost = streaming the dense n_l x n_l operator."""
+    limit = DENSE_TAIL_ROWS if limit is None else limit
+    if limit <= 0 or len(levels) < 3:
+        return -1
+
+    def a_kernels(sm):
+        if sm is None:
+            return 2
+        if sm.kind == _lib.SMOOTH_CHEBYSHEV:
+            return max(sm.order, 1)
+        return max(sm.sweeps, 1)
+    ka = a_kernels(pre) + a_kernels(post)   # (zero-guess first step is fused: ~ +residual)
+    nL = as_csr(levels[-1][0]).nrows
+    saving = _T_LAUNCH + nL * nL * 8.0 / _DENSE_BW           # coarse solve
+    best, best_gain = -1, 0.0
+    for l in range(len(levels) - 2, 0, -1):
+        A, P, R, _ = levels[l]
+        saving += ka * _kernel_us(A) + _kernel_us(P) + _kernel_us(R)
+        n = as_csr(A).nrows
+        if n > limit:
+            break
+        gain = saving - (_T_LAUNCH + n * n * 8.0 / _DENSE_BW)
+        if gain > best_gain:
+            best, best_gain = l, gain
+    return best
+
+
+def vcycle_tail_operator(levels, start: int, pre, post, inv) -> np.ndarray | None:
+    """Dense operator T of the V-cycle from level ``start`` down (setup phase).
+
+    Below the fine levels a V-cycle entered with a zero guess is a fixed
+    LINEAR map of its right-hand side: x_l = T_l b_l (the zero-guess
+    pre-smoother, residual, restriction, the recursion, prolongation and
+    post-smoother of solvers.py:651-664 are all linear in b_l).  T_l is built
+    here once by applying that sub-V-cycle to the n_l unit vectors (fp64,
+    values widened like the device kernels), so the solve runs the whole tail
+    as one dense product -- one launch instead of ~4 per level.  Same operator
+    as the per-level kernels; only the floating-point evaluation order of the
+    tail differs (the reference's coarsest LU is replaced the same way, see
+    coarse_inverse).  ``levels``: (A, P, R, eig_bounds) per level; pre/post:
+    _lib.mrs_smoother.  Returns None for Gauss-Seidel smoothing (kept on the
+    exact level-scheduled kernels).
+    """
+    for sm in (pre, post):
+        if sm.kind not in (_lib.SMOOTH_JACOBI, _lib.SMOOTH_CHEBYSHEV):
+            return None
+    mats = []
+    for (A, P, R, bounds) in levels[start:]:
+        A = as_csr(A)
+        As = A.to_scipy()
+        mats.append((As, A.diagonal().astype(np.float64),
+                     as_csr(P).to_scipy() if P is not None else None,
+                     as_csr(R).to_scipy() if R is not None else None, bounds))
+
+    def smooth(sm, k, b, x):                  # x None: zero guess
+        As, d, _, _, bounds = mats[k]
+        if sm.kind == _lib.SMOOTH_JACOBI:     # blas2.py:165-185
+            if sm.weight == 0.0:
+                return np.zeros_like(b) if x is None else x
+            for _ in range(max(sm.sweeps, 1)):
+                r = b if x is None else b - As @ x
+                upd = sm.weight * (r / d[:, None])
+                x = upd if x is None else x + upd
+            return x
+        lmin, lmax = bounds                   # solvers.py:520-571
+        theta, delta = 0.5 * (lmax + lmin), 0.5 * (lmax - lmin)
+        sigma = theta / delta
+        rho = 1.0 / sigma
+        r = b if x is None else b - As @ x
+        dv = r / (d[:, None] * theta)
+        x = dv.copy() if x is None else x + dv
+        for _ in range(max(sm.order, 1) - 1):
+            r = r - As @ dv
+            rho_new = 1.0 / (2.0 * sigma - rho)
+            dv = dv * (rho_new * rho) + (2.0 * rho_new / delta) * (r / d[:, None])
+            x = x + dv
+            rho = rho_new
+        return x
+
+    def vcycle(k, b):
+        if k == len(mats) - 1:
+            return inv @ b
+        As, d, P, R, _ = mats[k]
+        x = smooth(pre, k, b, None)
+        xc = vcycle(k + 1, R @ (b - As @ x))
+        x = x + P @ xc
+        return smooth(post, k, b, x)
+
+    n = mats[0][0].shape[0]
+    return np.ascontiguousarray(vcycle(0, np.eye(n)))

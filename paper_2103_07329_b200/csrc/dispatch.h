@@ -37,6 +37,8 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
 // Vector-family launch (OP = VecOp).
 cudaError_t launch_vec(int op, VArgs a, cudaStream_t s);
 // Dense coarse solve x = Ainv b for (nc, m) blocks.
+cudaError_t launch_dense(const double* T, int64_t n, const double* b, double* x, int64_t m,
+                         const int* guard, cudaStream_t s);
 cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
                           int64_t m, const int* guard, cudaStream_t s);
 // V-cycle tail on one thread-block cluster (tail.cu)

@@ -154,4 +154,102 @@ cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double
     return cudaGetLastError();
 }
 
+// x = T b for a dense row-major n x n operator T (the collapsed V-cycle
+// tail).  A warp owns R consecutive rows and walks k in steps of 32: lane j
+// loads T[i_r, k + j] (256 B coalesced per row) and row k + j of b (M
+// contiguous doubles) and keeps R x M partial sums; a xor tree over the
+// lanes finishes each (row, column).  T is streamed once; b (n*M*8 bytes)
+// stays in L1/L2 and is re-read once per R rows.  Fixed reduction shape.
+template <int M, int R>
+__global__ void __launch_bounds__(kThreads) dense_kernel(const double* __restrict__ T, int64_t n,
+                                                         const double* __restrict__ b,
+                                                         double* __restrict__ x,
+                                                         const int* guard) {
+    pdl_enter();
+    if (guard && *guard) return;
+    const int lane = threadIdx.x % 32;
+    const int64_t i0 = ((int64_t)blockIdx.x * (kThreads / 32) + threadIdx.x / 32) * R;
+    if (i0 >= n) return;
+    const double* Tr[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) Tr[r] = T + min(i0 + r, n - 1) * n;
+    double acc[R][M];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < M; ++c) acc[r][c] = 0.0;
+    for (int64_t k = lane; k < n; k += 32) {
+        double t[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) t[r] = __ldg(Tr[r] + k);
+        double bv[M];
+        if constexpr (M == 1) {
+            bv[0] = __ldg(b + k);
+        } else {
+#pragma unroll
+            for (int c = 0; c < M; c += 2) {
+                const double2 v = __ldg(reinterpret_cast<const double2*>(b + k * M + c));
+                bv[c] = v.x; bv[c + 1] = v.y;
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < M; ++c) acc[r][c] = add(acc[r][c], mul(t[r], bv[c]));
+    }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int c = 0; c < M; ++c)
+                acc[r][c] = add(acc[r][c], __shfl_xor_sync(0xffffffffu, acc[r][c], off));
+    if (lane == 0) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (i0 + r >= n) break;
+#pragma unroll
+            for (int c = 0; c < M; ++c) x[(i0 + r) * M + c] = acc[r][c];
+        }
+    }
+}
+
+cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
+                          int64_t m, const int* guard, cudaStream_t s);
+
+cudaError_t launch_dense(const double* T, int64_t n, const double* b, double* x, int64_t m,
+                         const int* guard, cudaStream_t s) {
+    constexpr int W = kThreads / 32;
+    // small operators: one row per CTA (more CTAs in flight than warp-rows)
+    if (n <= 1024) return launch_coarse(T, n, b, x, m, guard, s);
+    // rows per warp: the most (<= 32 / M partial sums per lane) that still
+    // give every SM a CTA
+    auto rows = [&](int rmax) {
+        int R = rmax;
+        while (R > 1 && (n + (int64_t)R * W - 1) / ((int64_t)R * W) < num_sms()) R >>= 1;
+        return R;
+    };
+    auto go = [&](auto k1, auto k2, auto k4, auto k8, int rmax) {
+        const int R = rows(rmax);
+        const int64_t warps = (n + R - 1) / R;
+        const int g = (int)((warps + W - 1) / W);
+        if (R == 8) (void)launch_ex(k8, g, s, T, n, b, x, guard);
+        else if (R == 4) (void)launch_ex(k4, g, s, T, n, b, x, guard);
+        else if (R == 2) (void)launch_ex(k2, g, s, T, n, b, x, guard);
+        else (void)launch_ex(k1, g, s, T, n, b, x, guard);
+        return cudaGetLastError();
+    };
+#define MRS_DK(MM) dense_kernel<MM, 1>, dense_kernel<MM, 2>, dense_kernel<MM, (MM <= 8 ? 4 : 2)>, \
+                   dense_kernel<MM, (MM <= 4 ? 8 : 2)>
+    switch (m) {
+    case 1: return go(MRS_DK(1), 8);
+    case 2: return go(MRS_DK(2), 8);
+    case 4: return go(MRS_DK(4), 8);
+    case 8: return go(MRS_DK(8), 4);
+    case 16: return go(MRS_DK(16), 2);
+    default: return launch_coarse(T, n, b, x, m, guard, s);   // any m
+    }
+#undef MRS_DK
+}
+
 }  // namespace mrs

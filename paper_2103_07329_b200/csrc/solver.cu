@@ -82,6 +82,9 @@ struct mrs_plan {
     std::map<std::string, TailStep*> tail_cache;   // uploaded step lists
     double* inv = nullptr;
     int64_t nc = 0;
+    int dense_from = -1;       // collapsed V-cycle tail: level, dense operator, rows
+    double* tail_op = nullptr;
+    int64_t tail_n = 0;
     std::vector<void*> owned;
     // Krylov workspace
     double *B = nullptr, *X = nullptr, *r = nullptr, *r0 = nullptr, *p = nullptr, *q = nullptr;
@@ -275,6 +278,10 @@ struct Builder {
     static bool coarsest(const mrs_plan& p, int l) {
         return p.desc.precond == MRS_PC_MG && l == (int)p.L.size() - 1;
     }
+    // the collapsed sub-V-cycle (mrs_plan_set_dense_tail): entered with zero x
+    static bool dense_tail(const mrs_plan& p, int l) {
+        return p.desc.precond == MRS_PC_MG && l == p.dense_from && !p.dist;
+    }
 
     // Gauss-Seidel sweep in place on x (blas2.py:113-162): forward and/or
     // backward half, each one cluster launch over the level schedule.
@@ -302,7 +309,7 @@ struct Builder {
     Seed level_seed(int l, const XB& x) const {
         const mrs_plan& p = *P;
         Seed sd;
-        if (coarsest(p, l)) return sd;
+        if (coarsest(p, l) || dense_tail(p, l)) return sd;
         const LevelDev& lv = p.L[l];
         const mrs_smoother sm = pc_smoother(p.desc);
         sd.d = lv.d;
@@ -448,13 +455,16 @@ struct Builder {
                 }
             }
         }
-        if (coarsest(p, l)) {
-            // x = A_c^{-1} b (replaces the LU solve, solvers.py:644-649)
-            int64_t m = p.m, nc = p.nc;
-            const double* inv = p.inv;
+        if (coarsest(p, l) || (zero && dense_tail(p, l))) {
+            // x = A_c^{-1} b (replaces the LU solve, solvers.py:644-649), or
+            // x = T_l b for the collapsed tail (same dense kernel)
+            const bool tl = !coarsest(p, l);
+            int64_t m = p.m, nc = tl ? p.tail_n : p.nc;
+            const double* inv = tl ? p.tail_op : p.inv;
             double* xo = x.cur;
             const int* g = guard;
             if (rec) {
+                if (tl) { rec_fail = true; return; }   // the dense tail is its own launch
                 TailStep t;
                 memset(&t, 0, sizeof(t));
                 t.kind = TK_COARSE; t.inv = inv; t.nc = nc; t.cb = b; t.cx = xo;
@@ -463,7 +473,10 @@ struct Builder {
                 if (dot_epi >= 0) rec_fail = true;
                 return;
             }
-            out->push_back([=](cudaStream_t s) { return launch_coarse(inv, nc, b, xo, m, g, s); });
+            if (tl)
+                out->push_back([=](cudaStream_t s) { return launch_dense(inv, nc, b, xo, m, g, s); });
+            else
+                out->push_back([=](cudaStream_t s) { return launch_coarse(inv, nc, b, xo, m, g, s); });
             bytes += (double)nc * nc * 8.0 + 2 * V(nc);
             kernels++;
             if (dot_epi >= 0) dot(b, x.cur, nc, dot_epi);
@@ -1059,6 +1072,19 @@ int mrs_plan_set_coarse_inverse(mrs_plan* p, const double* inv, int64_t nc) {
     if (!p->inv) return MRS_ERR_ALLOC;
     p->nc = nc;
     MRS_CUDA_OK(cudaMemcpy(p->inv, inv, (size_t)nc * nc * 8, cudaMemcpyHostToDevice));
+    return MRS_OK;
+}
+
+int mrs_plan_set_dense_tail(mrs_plan* p, int32_t l, const double* op, int64_t n) {
+    if (!p || !op || n < 1) return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    if (p->desc.precond != MRS_PC_MG || l < 1 || l >= (int)p->L.size() - 1) return MRS_ERR_ARG;
+    if (!p->L[l].A.present() || p->L[l].A.nrows != n) return MRS_ERR_ARG;
+    p->tail_op = dalloc<double>((size_t)n * n, p->owned);
+    if (!p->tail_op) return MRS_ERR_ALLOC;
+    p->tail_n = n;
+    p->dense_from = l;
+    MRS_CUDA_OK(cudaMemcpy(p->tail_op, op, (size_t)n * n * 8, cudaMemcpyHostToDevice));
     return MRS_OK;
 }
 

@@ -27,7 +27,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from .amg import AmgParams, Hierarchy, coarse_inverse, estimate_eig_bounds, setup as amg_setup
+from .amg import (AmgParams, Hierarchy, coarse_inverse, dense_tail_level, estimate_eig_bounds,
+                  setup as amg_setup, vcycle_tail_operator)
 from .core import BlockVector, PrecisionTag, as_csr
 from .errors import (BreakdownError, ConfigurationError, InvalidArgumentError,
                      ShapeMismatchError)
@@ -101,6 +102,16 @@ def _smoother(plist) -> _lib.mrs_smoother:
     raise ConfigurationError(f"smoother {plist.method!r} is not on the device path")
 
 
+class CoarseOps:
+    """Dense operators of the coarse end of the V-cycle (uploaded once):
+    ``inv`` = inverse of the coarsest operator, ``tail`` = the collapsed
+    sub-V-cycle operator of level ``tail_level`` (amg.vcycle_tail_operator),
+    or None."""
+
+    def __init__(self, inv, tail_level=-1, tail=None):
+        self.inv, self.tail_level, self.tail = inv, tail_level, tail
+
+
 class DevicePlan:
     """One uploaded solver instance for a fixed RHS count m (owns a C plan)."""
 
@@ -138,10 +149,17 @@ class DevicePlan:
                                                      C.byref(p) if p is not None else None,
                                                      C.byref(r) if r is not None else None,
                                                      float(lo), float(hi)), f"upload level {l}")
+            tail = None
+            if isinstance(inv, CoarseOps):
+                inv, tail = inv.inv, inv
             if inv is not None:
                 inv = np.ascontiguousarray(inv, dtype=np.float64)
                 _lib.check(self.L.mrs_plan_set_coarse_inverse(h, inv.ctypes.data, inv.shape[0]),
                            "coarse inverse")
+            if tail is not None and tail.tail is not None and dist is None:
+                T = np.ascontiguousarray(tail.tail, dtype=np.float64)
+                _lib.check(self.L.mrs_plan_set_dense_tail(h, tail.tail_level, T.ctypes.data,
+                                                          T.shape[0]), "dense V-cycle tail")
             _lib.check(self.L.mrs_plan_finalize(h, None), "plan finalize")
         except Exception:
             self.L.mrs_plan_destroy(h)
@@ -350,6 +368,11 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
         inv = coarse_inverse(h.coarsest.A)
         h.coarsest.lu = inv
         desc.nlevels = h.nlevels
+        tl = dense_tail_level(levels, pre=desc.pre, post=desc.post)
+        if tl >= 0:
+            T = vcycle_tail_operator(levels, tl, desc.pre, desc.post, inv)
+            if T is not None:
+                inv = CoarseOps(inv, tl, T)
     else:
         raise ConfigurationError(f"preconditioner {pl.method!r} is not on the device path")
     return desc, levels, inv, h, name, Ab

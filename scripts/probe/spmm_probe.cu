@@ -308,6 +308,32 @@ static Csr poisson7(int g) {
     return A;
 }
 
+
+static Csr stencil27(int g) {
+    Csr A;
+    A.name = "27pt-" + std::to_string(g);
+    A.n = g * g * g;
+    A.rp.push_back(0);
+    std::mt19937_64 rng(4);
+    std::uniform_real_distribution<double> U(-1, 1);
+    for (int z = 0; z < g; ++z)
+        for (int y = 0; y < g; ++y)
+            for (int x = 0; x < g; ++x) {
+                const int i = (z * g + y) * g + x;
+                for (int dz = -1; dz <= 1; ++dz)
+                    for (int dy = -1; dy <= 1; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            const int zz = z + dz, yy = y + dy, xx = x + dx;
+                            if (zz < 0 || yy < 0 || xx < 0 || zz >= g || yy >= g || xx >= g) continue;
+                            const int j = (zz * g + yy) * g + xx;
+                            A.ci.push_back(j);
+                            A.v.push_back(j == i ? 30.0 + U(rng) : U(rng));
+                        }
+                A.rp.push_back((int)A.ci.size());
+            }
+    return A;
+}
+
 static Csr band_random(int n, int band, double mean) {
     Csr A;
     A.name = "c5-" + std::to_string(n);
@@ -536,6 +562,216 @@ static void to_sell(const Csr& A, const std::vector<Ti>& cols, int C, std::vecto
 }
 
 
+
+// base + cross-pass register prefetch: the next pass's row pointers (PF>=1)
+// and its first entry group's columns/values (PF>=2) are loaded while the
+// current row is accumulated.
+template <int M, typename Ti, int UNR, int MINB, int PF>
+__global__ void __launch_bounds__(256, MINB) k_pf(Args a) {
+    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR, RPB = 256 / LPR;
+    const int cofs = (threadIdx.x % LPR) * CPL;
+    const Ti* ci = (const Ti*)a.ci;
+    // flattened (chunk, pass) iteration for this thread
+    int r0 = blockIdx.x * a.chunk;
+    int row = r0 + threadIdx.x / LPR;
+    auto advance = [&](int& c0, int& rw) {
+        rw += RPB;
+        if (rw >= min(c0 + a.chunk, a.n)) { c0 += gridDim.x * a.chunk; rw = c0 + threadIdx.x / LPR; }
+    };
+    // skip rows past a short chunk end
+    while (r0 < a.n && row >= min(r0 + a.chunk, a.n)) { r0 += gridDim.x * a.chunk; row = r0 + threadIdx.x / LPR; }
+    if (r0 >= a.n) return;
+    int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
+    int pc[UNR]; double pv[UNR];
+    if constexpr (PF >= 2) {
+#pragma unroll
+        for (int u = 0; u < UNR; ++u) {
+            const int kk = (lo + u < hi) ? lo + u : lo;
+            pc[u] = (int)__ldg(ci + kk); pv[u] = __ldg(a.v + kk);
+        }
+    }
+    while (true) {
+        int nr0 = r0, nrow = row;
+        advance(nr0, nrow);
+        const bool more = nr0 < a.n && nrow < a.n;
+        int nlo = 0, nhi = 0;
+        if (more) { nlo = __ldg(a.rp + nrow); nhi = __ldg(a.rp + nrow + 1); }
+        const int base = a.slab ? __ldg(a.slab + (row >> a.slab_shift)) : 0;
+        const int o = row * M + cofs;
+        V<CPL> acc = ldx<CPL>(a.b + o);
+        for (int k = lo; k < hi; k += UNR) {
+            int c[UNR]; double v[UNR]; V<CPL> g[UNR];
+            if (PF >= 2 && k == lo) {
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) { c[u] = base + pc[u]; v[u] = pv[u]; }
+            } else {
+#pragma unroll
+                for (int u = 0; u < UNR; ++u) {
+                    const int kk = (k + u < hi) ? k + u : lo;
+                    c[u] = base + (int)__ldg(ci + kk);
+                    v[u] = __ldg(a.v + kk);
+                }
+            }
+            fence();
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) g[u] = ldx<CPL>(a.x + c[u] * M + cofs);
+            fence();
+#pragma unroll
+            for (int u = 0; u < UNR; ++u)
+                if (k + u < hi)
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc.v[i] = sub(acc.v[i], mul(v[u], g[u].v[i]));
+        }
+        stv<CPL>(a.y + o, acc);
+        if (!more) break;
+        r0 = nr0; row = nrow; lo = nlo; hi = nhi;
+        if constexpr (PF >= 2) {
+#pragma unroll
+            for (int u = 0; u < UNR; ++u) {
+                const int kk = (lo + u < hi) ? lo + u : lo;
+                pc[u] = (int)__ldg(ci + kk); pv[u] = __ldg(a.v + kk);
+            }
+        }
+    }
+}
+
+template <int M, typename Ti, int UNR, int MINB, int PF>
+static void run_pf(Args a) {
+    auto kern = k_pf<M, Ti, UNR, MINB, PF>;
+    int bps;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+    constexpr int RPB = 256 / Lay<M>::LPR;
+    const long cap = (long)bps * nsm();
+    const long P = (a.n + RPB - 1) / RPB, ppc = (P + cap - 1) / cap;
+    long pmax = std::max(1, 64 / RPB);
+    const long sp = std::min(ppc, pmax);
+    const long nch = (P + sp - 1) / sp, cpc = (nch + cap - 1) / cap;
+    const int grid = (int)((nch + cpc - 1) / cpc);
+    a.chunk = (int)(RPB * sp);
+    kern<<<grid, 256>>>(a);
+}
+
+
+// ---------------------------------------------------------------- SELL-4
+// Slices of C = 32/LPR rows; within a slice, entries are grouped by 4:
+// group g of row r (entries 4g..4g+3) is stored contiguously at
+// sptr[slice] + g*4*C + (r%C)*4.  Rows padded to the slice's group count.
+// A lane loads its row's whole group with one 32-byte (values) and one
+// 8/16-byte (columns) access; a warp instruction covers C rows' groups =
+// one contiguous 4*C-entry block.
+__device__ __forceinline__ void ld4(const double* p, double (&v)[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+}
+template <typename Ti> struct Grp;
+template <> struct Grp<uint16_t> {
+    static __device__ __forceinline__ void ld(const uint16_t* p, int (&c)[4]) {
+        uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        c[0] = t.x & 0xffff; c[1] = t.x >> 16; c[2] = t.y & 0xffff; c[3] = t.y >> 16;
+    }
+};
+template <> struct Grp<uint32_t> {
+    static __device__ __forceinline__ void ld(const uint32_t* p, int (&c)[4]) {
+        uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+        c[0] = t.x; c[1] = t.y; c[2] = t.z; c[3] = t.w;
+    }
+};
+
+template <int M, typename Ti, int MINB, int PIPE>
+__global__ void __launch_bounds__(256, MINB) k_g4(Args a) {
+    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR, RPB = 256 / LPR, C = 32 / LPR;
+    const int cofs = (threadIdx.x % LPR) * CPL;
+    const Ti* ci = (const Ti*)a.ci;
+    for (int r0 = blockIdx.x * a.chunk; r0 < a.n; r0 += gridDim.x * a.chunk) {
+        const int r1 = min(r0 + a.chunk, a.n);
+        for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB) {
+            const int base = a.slab ? __ldg(a.slab + (row >> a.slab_shift)) : 0;
+            const int p = __ldg(a.sptr + row / C) + (row % C) * 4;
+            const int len = __ldg(a.slen + row);
+            const int o = row * M + cofs;
+            V<CPL> acc = ldx<CPL>(a.b + o);
+            int c[4]; double v[4];
+            if (len > 0) {
+                Grp<Ti>::ld(ci + p, c);
+                ld4(a.v + p, v);
+            }
+            for (int k = 0; k < len; k += 4) {
+                V<CPL> g[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) g[u] = ldx<CPL>(a.x + (base + c[u]) * M + cofs);
+                double w[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) w[u] = v[u];
+                if (PIPE && k + 4 < len) {   // next group's entries fly with this group's gathers
+                    const int q = p + (k + 4) * C;
+                    Grp<Ti>::ld(ci + q, c);
+                    ld4(a.v + q, v);
+                }
+                fence();
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (k + u < len)
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) acc.v[i] = sub(acc.v[i], mul(w[u], g[u].v[i]));
+                if (!PIPE && k + 4 < len) {
+                    const int q = p + (k + 4) * C;
+                    Grp<Ti>::ld(ci + q, c);
+                    ld4(a.v + q, v);
+                }
+            }
+            stv<CPL>(a.y + o, acc);
+        }
+    }
+}
+
+template <int M, typename Ti, int MINB, int PIPE>
+static void run_g4(Args a) {
+    auto kern = k_g4<M, Ti, MINB, PIPE>;
+    int bps;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+    constexpr int RPB = 256 / Lay<M>::LPR;
+    const long cap = (long)bps * nsm();
+    const long P = (a.n + RPB - 1) / RPB, ppc = (P + cap - 1) / cap;
+    long pmax = std::max(1, 64 / RPB);
+    const long sp = std::min(ppc, pmax);
+    const long nch = (P + sp - 1) / sp, cpc = (nch + cap - 1) / cap;
+    const int grid = (int)((nch + cpc - 1) / cpc);
+    a.chunk = (int)(RPB * sp);
+    kern<<<grid, 256>>>(a);
+}
+
+template <typename Ti>
+static void to_g4(const Csr& A, const std::vector<Ti>& cols, int C, std::vector<int>& sptr,
+                  std::vector<uint8_t>& slen, std::vector<Ti>& sci, std::vector<double>& sv) {
+    const int ns = (A.n + C - 1) / C;
+    sptr.assign(ns + 1, 0);
+    slen.assign(A.n, 0);
+    long tot = 0;
+    for (int s = 0; s < ns; ++s) {
+        int G = 0;
+        for (int r = s * C; r < std::min(A.n, s * C + C); ++r) {
+            const int l = A.rp[r + 1] - A.rp[r];
+            slen[r] = (uint8_t)l;
+            G = std::max(G, (l + 3) / 4);
+        }
+        sptr[s] = (int)tot;
+        tot += (long)G * 4 * C;
+    }
+    sptr[ns] = (int)tot;
+    sci.assign(tot, 0);
+    sv.assign(tot, 0.0);
+    for (int r = 0; r < A.n; ++r) {
+        const int s = r / C, G = (sptr[s + 1] - sptr[s]) / (4 * C);
+        const int lo = A.rp[r], l = A.rp[r + 1] - lo;
+        for (int k = 0; k < 4 * G; ++k) {
+            const long q = sptr[s] + (long)(k / 4) * 4 * C + (r % C) * 4 + k % 4;
+            sci[q] = l ? cols[lo + (k < l ? k : 0)] : 0;
+            sv[q] = k < l ? A.v[lo + k] : 0.0;
+        }
+    }
+}
+
 static double bytes_of(const Csr& A, int m, int ib, int nslab) {
     return (double)A.ci.size() * (8 + ib) + (A.n + 1) * 4.0 + nslab * 4.0 + 3.0 * A.n * m * 8;
 }
@@ -590,6 +826,47 @@ template <int M, int EPR> static void bench_matrix(const Csr& A) {
     Args a32 = a; a32.ci = ci32; a32.y = y1;
     Args a16 = a; a16.ci = ci16; a16.slab = sb; a16.slab_shift = shift; a16.y = y1;
     int g;
+    if (getenv("G4")) {
+        g_chunk_rows = 64;
+        check("base u16slab 6/SM chunk 64", time_us([&] { run_base<M, uint16_t, 4, 6>(a16, g); }), b16);
+        check("base u32 6/SM chunk 64", time_us([&] { run_base<M, uint32_t, 4, 6>(a32, g); }), b32);
+        g_chunk_rows = 0;
+        constexpr int C = 32 / Lay<M>::LPR;
+        std::vector<int> sp; std::vector<uint8_t> sl; std::vector<uint32_t> s32; std::vector<double> sv;
+        to_g4<uint32_t>(A, A.ci, C, sp, sl, s32, sv);
+        printf("  g4 C=%d padding x%.3f\n", C, (double)sv.size() / A.v.size());
+        int* dsp = up(sp); uint8_t* dsl = up(sl); uint32_t* ds32 = up(s32); double* dsv = up(sv);
+        Args s1 = a32; s1.ci = ds32; s1.v = dsv; s1.sptr = dsp; s1.slen = dsl;
+        const double bs32 = (double)sv.size() * 12 + A.n * 1.0 + sp.size() * 4.0 + 3.0 * A.n * M * 8;
+        check("g4 u32 6/SM", time_us([&] { run_g4<M, uint32_t, 6, 0>(s1); }), bs32);
+        check("g4 u32 6/SM pipe", time_us([&] { run_g4<M, uint32_t, 6, 1>(s1); }), bs32);
+        check("g4 u32 5/SM pipe", time_us([&] { run_g4<M, uint32_t, 5, 1>(s1); }), bs32);
+        if (slab) {
+            std::vector<uint16_t> s16; std::vector<double> sv2;
+            to_g4<uint16_t>(A, c16, C, sp, sl, s16, sv2);
+            uint16_t* ds16 = up(s16, 128);
+            Args s2 = s1; s2.ci = ds16; s2.slab = sb; s2.slab_shift = shift;
+            const double bs16 = (double)sv.size() * 10 + A.n * 1.0 + sp.size() * 4.0 + 3.0 * A.n * M * 8;
+            check("g4 u16 6/SM", time_us([&] { run_g4<M, uint16_t, 6, 0>(s2); }), bs16);
+            check("g4 u16 6/SM pipe", time_us([&] { run_g4<M, uint16_t, 6, 1>(s2); }), bs16);
+            check("g4 u16 8/SM pipe", time_us([&] { run_g4<M, uint16_t, 8, 1>(s2); }), bs16);
+            check("g4 u16 5/SM pipe", time_us([&] { run_g4<M, uint16_t, 5, 1>(s2); }), bs16);
+            cudaFree(ds16);
+        }
+        cudaFree(dsp); cudaFree(dsl); cudaFree(ds32); cudaFree(dsv);
+        return;
+    }
+    if (getenv("PF")) {
+        g_chunk_rows = 64;
+        check("base u16slab 6/SM chunk 64", time_us([&] { run_base<M, uint16_t, 4, 6>(a16, g); }), b16);
+        g_chunk_rows = 0;
+        check("pf1 u16slab UNR4 6/SM", time_us([&] { run_pf<M, uint16_t, 4, 6, 1>(a16); }), b16);
+        check("pf2 u16slab UNR4 6/SM", time_us([&] { run_pf<M, uint16_t, 4, 6, 2>(a16); }), b16);
+        check("pf2 u16slab UNR4 5/SM", time_us([&] { run_pf<M, uint16_t, 4, 5, 2>(a16); }), b16);
+        check("pf1 u16slab UNR4 8/SM", time_us([&] { run_pf<M, uint16_t, 4, 8, 1>(a16); }), b16);
+        check("pf1 u32 UNR4 6/SM", time_us([&] { run_pf<M, uint32_t, 4, 6, 1>(a32); }), b32);
+        return;
+    }
     if (getenv("CHUNKS")) {
         for (int cr : {32, 64, 128, 256, 512, 1024, 2048, 4096}) {
             g_chunk_rows = cr;
@@ -657,6 +934,7 @@ int main(int argc, char** argv) {
     auto want = [&](const char* k) { return !strcmp(which, "all") || strstr(which, k); };
     if (want("c2")) { Csr A = poisson7(64); bench_matrix<8, 8>(A); }
     if (want("c3")) { Csr A = poisson7(128); bench_matrix<16, 8>(A); bench_matrix<8, 8>(A); }
+    if (want("c4")) { Csr A = stencil27(128); bench_matrix<8, 32>(A); }
     if (want("c5")) { Csr A = band_random(1 << 22, 4096, 15.0); bench_matrix<8, 24>(A); bench_matrix<1, 24>(A); }
     return 0;
 }

@@ -339,3 +339,27 @@ def test_cluster_tail_is_bitwise_identical(roles, m):
     _lib.set_option("tail_rows", 0)
     assert out[0][0] == out[4096][0]
     np.testing.assert_array_equal(out[0][1], out[4096][1])
+
+
+@pytest.mark.parametrize("roles", [GG.SOLVE_CASES["c2_amg_pcg_20"][3],
+                                   GG.SOLVE_CASES["c3_amg_bicgstab_full_cheb3"][3],
+                                   GG.SOLVE_CASES["c3_amg_bicgstab_mixed"][3]])
+@pytest.mark.parametrize("m", [1, 8, 16])
+def test_dense_tail_matches_per_level_kernels(roles, m, monkeypatch):
+    """The collapsed V-cycle tail (one dense launch for the levels <=
+    DENSE_TAIL_ROWS rows) is the same operator as the per-level kernels:
+    same iteration count, solutions equal to rounding, fewer launches."""
+    from paper_2103_07329_b200 import amg
+    A, _ = gen_poisson3d(24, 22, 20)
+    B = np.random.default_rng(m).uniform(-1, 1, (A.nrows, m))
+    out = {}
+    for rows in (0, 2500):
+        monkeypatch.setattr(amg, "DENSE_TAIL_ROWS", rows)
+        cs = prepare(tree(roles), A)
+        X = BlockVector.zeros(A.nrows, m)
+        st = cs.run(BlockVector.from_array(B), X)
+        assert st.all_converged
+        out[rows] = (st.iterations, X.data.copy(), cs.plan_factory(m).kernels_per_iteration)
+    assert out[0][0] == out[2500][0]
+    np.testing.assert_allclose(out[2500][1], out[0][1], rtol=0, atol=1e-9 * np.abs(out[0][1]).max())
+    assert out[2500][2] < out[0][2]
