@@ -69,6 +69,12 @@ typedef struct {
     const int32_t* slab_base; /* NULL: plain indices */
     int32_t slab_shift;
     int32_t pad_;
+    /* Optional (NULL / 0: none): rows with more than long_thr entries, done by
+     * whole CTAs instead of lane groups (same bits; the lane path skips them).
+     * Device int32 array of n_long row indices. */
+    const int32_t* long_rows;
+    int32_t n_long;
+    int32_t long_thr;
 } mrs_csr;
 
 /* Host CSR (the reference CsrBlock layout, core.py:146-254). */
@@ -282,6 +288,8 @@ int  mrs_version(void);
  *                   SpMM with 16 entries in flight per lane (default 20000; 0: off)
  *   "coarse_rows" N  rows per CTA of the dense coarse solve (default 1)
  *   "spmm_chunk_rows" N  rows per CTA chunk of the SpMM grid (default 64)
+ *   "spmm_long_split" 0/1  rows far longer than their operator's mean run on
+ *                   whole CTAs (default 1; solver levels only)
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

@@ -29,7 +29,8 @@ class mrs_csr(C.Structure):
     _fields_ = [("nrows", C.c_int64), ("ncols", C.c_int64), ("nnz", C.c_int64),
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
                 ("idx_bytes", C.c_int32), ("val_bytes", C.c_int32),
-                ("slab_base", C.c_void_p), ("slab_shift", C.c_int32), ("pad_", C.c_int32)]
+                ("slab_base", C.c_void_p), ("slab_shift", C.c_int32), ("pad_", C.c_int32),
+                ("long_rows", C.c_void_p), ("n_long", C.c_int32), ("long_thr", C.c_int32)]
 
 
 class mrs_host_csr(C.Structure):

@@ -89,6 +89,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "coarse_rows")) { set_coarse_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }
+    if (!strcmp(key, "spmm_long_split")) { set_spmm_long_split(value); return MRS_OK; }
     return MRS_ERR_ARG;
 }
 
@@ -128,6 +129,12 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_
         if (A->idx_bytes != 2 || A->slab_shift < 0 || A->slab_shift > 30) return MRS_ERR_ARG;
         D.slab_base = const_cast<int32_t*>(A->slab_base);
         D.slab_shift = A->slab_shift;
+    }
+    if (A->long_rows && A->n_long > 0) {
+        if (A->long_thr < 1) return MRS_ERR_ARG;
+        D.long_rows = const_cast<int32_t*>(A->long_rows);
+        D.n_long = A->n_long;
+        D.long_thr = A->long_thr;
     }
     SpArgs a;
     memset(&a, 0, sizeof(a));

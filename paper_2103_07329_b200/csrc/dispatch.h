@@ -23,6 +23,8 @@ struct DevCsr {
     void* ci = nullptr;
     void* v = nullptr;
     int ib = 4, vb = 8;
+    int32_t* long_rows = nullptr; // rows with > long_thr entries (spmm.cuh long_row_cta)
+    int n_long = 0, long_thr = 0;
     bool present() const { return rp != nullptr; }
     // algorithmic bytes of one pass over the CSR arrays
     double bytes() const {
@@ -51,6 +53,8 @@ void set_tail_rows(int64_t v);
 void set_coarse_rows(int64_t v);
 void set_spmm_long_rows(int64_t v);
 void set_spmm_chunk_rows(int64_t v);
+void set_spmm_long_split(int64_t v);
+int64_t spmm_long_split();
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;
 cudaError_t launch_sgs(const SgsArgs& a, int vb, int ib, cudaStream_t s);

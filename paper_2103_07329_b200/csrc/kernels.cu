@@ -30,6 +30,9 @@ void set_spmm_long_rows(int64_t v) { g_long_rows = v < 0 ? 0 : v; }
 static int64_t g_chunk_rows = 64;     // A/B: profiles/r01_ab_experiments.txt
 int64_t spmm_chunk_rows() { return g_chunk_rows; }
 void set_spmm_chunk_rows(int64_t v) { g_chunk_rows = v < 1 ? 1 : v; }
+static int64_t g_long_split = 1;      // long rows by whole CTAs (0: lane path only)
+int64_t spmm_long_split() { return g_long_split; }
+void set_spmm_long_split(int64_t v) { g_long_split = v ? 1 : 0; }
 static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
@@ -50,6 +53,10 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
     a.ncols_hint = A.ncols;
     a.slab_base = A.slab_base;
     a.slab_shift = A.slab_shift;
+    a.long_rows = A.long_rows;
+    a.n_long = spmm_long_split() ? A.n_long : 0;
+    a.long_thr = A.long_thr;
+    a.long_ctas = 0;
     if (A.nrows == 0) return cudaSuccess;
     // the SpMM engine indexes with 32 bits (rows, entries, element offsets)
     if ((A.nrows + 1) * m >= (int64_t)INT32_MAX || (A.ncols + 1) * m >= (int64_t)INT32_MAX ||

@@ -2,6 +2,7 @@
 // (occupancy-sized one-wave grids, PDL launch attribute).
 #pragma once
 
+#include <algorithm>
 #include <mutex>
 #include <unordered_map>
 
@@ -81,7 +82,9 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         g = (int)((nchunks + cpc - 1) / cpc);
         if (g < 1) g = 1;
         a.chunk = rpp * sp;
-        (void)launch_ex(kern, g, s, a);
+        if (generic) a.n_long = 0;                               // lane path only
+        a.long_ctas = a.n_long ? (int)std::min<int64_t>(a.n_long, 4LL * num_sms()) : 0;
+        (void)launch_ex(kern, g + a.long_ctas, s, a);
     };
     // small operators with long rows: the LONG variant (16 entries in flight)
     if (!generic && m <= 16 && a.nrows <= spmm_long_max_rows() && a.nnz_hint >= 12 * a.nrows) {

@@ -931,6 +931,21 @@ int upload_csr(const mrs_host_csr* h, DevCsr& d, std::vector<void*>& owned) {
         MRS_CUDA_OK(cudaMemcpy(d.ci, h->col_idx, (size_t)h->nnz * d.ib, cudaMemcpyHostToDevice));
     }
     MRS_CUDA_OK(cudaMemcpy(d.v, h->values, (size_t)h->nnz * d.vb, cudaMemcpyHostToDevice));
+    // rows far longer than the mean (AMG coarse operators): whole-CTA path
+    if (h->nrows > 0 && h->nnz > 0) {
+        const int64_t mean = (h->nnz + h->nrows - 1) / h->nrows;
+        const int64_t thr = std::max<int64_t>(64, 4 * mean);
+        std::vector<int32_t> lr;
+        for (int64_t i = 0; i < h->nrows; ++i)
+            if (rp[i + 1] - rp[i] > thr) lr.push_back((int32_t)i);
+        if (!lr.empty() && (int64_t)lr.size() * 8 <= h->nrows) {
+            d.long_rows = dalloc<int32_t>(lr.size(), owned);
+            if (!d.long_rows) return MRS_ERR_ALLOC;
+            MRS_CUDA_OK(cudaMemcpy(d.long_rows, lr.data(), lr.size() * 4, cudaMemcpyHostToDevice));
+            d.n_long = (int)lr.size();
+            d.long_thr = (int)thr;
+        }
+    }
     if (h->slab_base) {
         if (h->idx_bytes != 2 || h->slab_shift < 0 || h->slab_shift > 30) return MRS_ERR_ARG;
         const int64_t ns = ((h->nrows - 1) >> h->slab_shift) + 1;

@@ -17,11 +17,14 @@
 //   LPR : 1  1  2  4   8   8   8
 //
 // Grid: one wave of resident CTAs (occupancy-sized, never more than the rows
-// need) striding over chunks of ~512 consecutive rows.  Inside a chunk the
+// need) striding over chunks of ~64 consecutive rows.  Inside a chunk the
 // CTA walks passes of RPB rows, so x rows shared by neighbouring passes are
 // reused from L1; across CTAs the active chunks form one narrow band of the
 // matrix, so the gathered x window of a banded matrix stays L2-resident.
 // The reduction shape of the fused dots is fixed by (n, grid): deterministic.
+// Rows much longer than the operator's mean (AMG coarse levels) are taken
+// out of the lane path and done by trailing CTAs, one row each
+// (long_row_cta), so one long row no longer sets the kernel's duration.
 #pragma once
 
 #include "reduce.cuh"
@@ -74,8 +77,12 @@ struct SpArgs {
     const int32_t* slab_base;  // non-null: column = slab_base[row >> slab_shift] + col16
     int slab_shift;
     int64_t ncols_hint;     // matrix columns
+    const int32_t* long_rows;  // rows with more than long_thr entries (one CTA each)
+    int n_long, long_thr, long_ctas;   // long_ctas: trailing CTAs of the grid doing them
     RedArgs red;
 };
+// shared-memory products per chunk of a long row (long_row_cta)
+constexpr int kLongProducts = 2048;
 
 // Zero-guess smoother seed of a right-hand-side value v at a row with
 // diagonal d: Jacobi's first sweep x = 0 + w*(v/d) (blas2.py:181) or
@@ -185,14 +192,13 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
     }
 }
 
-// One (row, column-slice) of work for every op.  `dotp` accumulates the fused
-// dot (OP_SPMV with a.dot: x_own . y).
-template <int OP, int CPL, class Src, int UNR = 4, bool NC = true>
-__device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row, int lo,
-                                       int hi, int ld, int cofs, double (&dotp)[CPL]) {
-    // 32-bit indices: rows, entries and element offsets < 2^31 (launch checks)
-    const int o = row * ld + cofs;
-    double acc[CPL];
+// One (row, column-slice) of work for every op, in three parts so that the
+// long-row path (long_row_cta) can run the same prologue / epilogue around a
+// CTA-cooperative accumulation.  row_begin loads the accumulator's start
+// value (and operands the epilogue reuses); `sub` = entries are subtracted.
+template <int OP, int CPL, bool NC = true>
+__device__ __forceinline__ void row_begin(const SpArgs& a, int o, double (&acc)[CPL],
+                                          Vec<CPL>& keep, bool& subtract) {
     if constexpr (OP == OP_SPMV) {
         const int mode = a.mode;
         if (mode == MRS_MODE_ASSIGN) {
@@ -207,10 +213,24 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row,
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         }
-        if (mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD)
-            row_accumulate<OP, CPL, false, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
-        else
-            row_accumulate<OP, CPL, true, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
+        subtract = !(mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD);
+    } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
+        // r = b - A x  (RSUB order: start at b, subtract in entry order)
+        keep = ldv<CPL, NC>(a.b + o);
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = keep.v[i];
+        subtract = true;
+    } else {  // OP_CHEB_STEP: tmp = A dv from 0
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
+        subtract = false;
+    }
+}
+
+template <int OP, int CPL, bool NC = true>
+__device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double (&acc)[CPL],
+                                        const Vec<CPL>& keep, double (&dotp)[CPL]) {
+    if constexpr (OP == OP_SPMV) {
         Vec<CPL> out;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
@@ -228,11 +248,6 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row,
             for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
         }
     } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
-        // r = b - A x  (RSUB order: start at b, subtract in entry order)
-        Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
-        row_accumulate<OP, CPL, true, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
         const double dd = __ldg(a.d + row);
         Vec<CPL> xo = ldv<CPL, NC>(a.x + o);
         if constexpr (OP == OP_CHEB_FIRST) {
@@ -253,12 +268,9 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row,
         store_vec<CPL>(a.x_out + o, xo);
         if (a.dot) {
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(keep.v[i], xo.v[i]));
         }
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
-#pragma unroll
-        for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
-        row_accumulate<OP, CPL, false, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);   // tmp = A dv
         const double dd = __ldg(a.d + row);
         Vec<CPL> r = ldv<CPL, NC>(a.r_in + o);
         Vec<CPL> dv = ldv<CPL, NC>(a.x + o);
@@ -279,6 +291,67 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row,
             for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
         }
     }
+}
+
+template <int OP, int CPL, class Src, int UNR = 4, bool NC = true>
+__device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row, int lo,
+                                       int hi, int ld, int cofs, double (&dotp)[CPL]) {
+    // 32-bit indices: rows, entries and element offsets < 2^31 (launch checks)
+    const int o = row * ld + cofs;
+    double acc[CPL];
+    Vec<CPL> keep;
+    bool subtract;
+    row_begin<OP, CPL, NC>(a, o, acc, keep, subtract);
+    if (subtract)
+        row_accumulate<OP, CPL, true, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
+    else
+        row_accumulate<OP, CPL, false, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
+    row_end<OP, CPL, NC>(a, row, o, acc, keep, dotp);
+}
+
+// A long row (more than a.long_thr entries: AMG coarse operators carry rows
+// of ~1000 entries among rows of ~60) by a whole CTA: all threads gather and
+// multiply a chunk of the row's entries into shared memory (entry e, column
+// c), then the row's LPR lane-threads fold the products in entry order --
+// the same separately rounded mul then add/sub sequence as row_accumulate,
+// so the result is bitwise that of the lane path, but the row's gathers run
+// in parallel instead of as ceil(len/UNR) dependent rounds.
+template <int M, int OP, typename Tv, typename Ti>
+__device__ __forceinline__ void long_row_cta(const SpArgs& a, const GSrc<Tv, Ti>& src0, int row,
+                                             double (&dotp)[Lay<M>::CPL]) {
+    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR;
+    constexpr int EPC = kLongProducts / M;          // entries per chunk
+    __shared__ double s_p[kLongProducts];
+    const int q = threadIdx.x;
+    const GSrc<Tv, Ti> src = src0.at_row(a, row);
+    const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
+    const int o = row * M + q * CPL;
+    double acc[CPL];
+    Vec<CPL> keep;
+    bool subtract = false;
+    if (q < LPR) row_begin<OP, CPL>(a, o, acc, keep, subtract);
+    for (int k0 = lo; k0 < hi; k0 += EPC) {
+        const int ne = min(EPC, hi - k0);
+#pragma unroll 4
+        for (int t = threadIdx.x; t < ne * M; t += kThreads) {
+            const int e = t / M, c = t % M;
+            s_p[t] = mul(src.val(k0 + e), __ldg(a.x + src.col(k0 + e) * M + c));
+        }
+        __syncthreads();
+        if (q < LPR) {
+            if (subtract) {
+                for (int e = 0; e < ne; ++e)
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc[i] = sub(acc[i], s_p[e * M + q * CPL + i]);
+            } else {
+                for (int e = 0; e < ne; ++e)
+#pragma unroll
+                    for (int i = 0; i < CPL; ++i) acc[i] = add(acc[i], s_p[e * M + q * CPL + i]);
+            }
+        }
+        __syncthreads();
+    }
+    if (q < LPR) row_end<OP, CPL>(a, row, o, acc, keep, dotp);
 }
 
 // CTA-level fixed-shape reduction of the fused-dot partials (warp xor tree
@@ -331,11 +404,22 @@ spmm_kernel(SpArgs a) {
 #pragma unroll
     for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
     const int nrows = (int)a.nrows, chunk = (int)a.chunk;
-    for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gridDim.x * chunk) {
-        const int r1 = min(r0 + chunk, nrows);
-        for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB)
-            do_row<OP, CPL, GSrc<Tv, Ti>, LONG ? 16 : L::UNR>(a, src.at_row(a, row), row, __ldg(a.rp + row),
-                                                  __ldg(a.rp + row + 1), M, cofs, dotp);
+    const int gl = (int)gridDim.x - a.long_ctas;   // CTAs of the lane path
+    if ((int)blockIdx.x >= gl) {
+        // long rows: one CTA each (long_row_cta), strided over the long CTAs
+        for (int j = (int)blockIdx.x - gl; j < a.n_long; j += a.long_ctas)
+            long_row_cta<M, OP, Tv, Ti>(a, src, __ldg(a.long_rows + j), dotp);
+    } else {
+        const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
+        for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
+            const int r1 = min(r0 + chunk, nrows);
+            for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB) {
+                const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
+                if (hi - lo > lthr) continue;            // done by a long-row CTA
+                do_row<OP, CPL, GSrc<Tv, Ti>, LONG ? 16 : L::UNR>(a, src.at_row(a, row), row, lo, hi,
+                                                                  M, cofs, dotp);
+            }
+        }
     }
     if (a.dot) spmm_block_dot<M>(a, dotp);
 }

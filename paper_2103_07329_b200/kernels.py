@@ -86,6 +86,8 @@ class DeviceCsr:
         self.values = torch.as_tensor(np.asarray(values)).to(dev)
         self.nrows, self.ncols = int(nrows), int(ncols)
         self.nnz = int(self.col_idx.numel())
+        # rows far longer than the mean run on whole CTAs (same bits)
+        self.long_rows, self.long_thr = long_row_split(row_ptr, dev)
 
     @classmethod
     def from_block(cls, blk, device=None, slab=False):
@@ -96,7 +98,27 @@ class DeviceCsr:
         if self.slab_base is not None:
             v.slab_base = self.slab_base.data_ptr()
             v.slab_shift = self.slab_shift
+        if self.long_rows is not None:
+            v.long_rows = self.long_rows.data_ptr()
+            v.n_long = int(self.long_rows.numel())
+            v.long_thr = self.long_thr
         return v
+
+
+def long_row_split(row_ptr, device):
+    """Rows with more than max(64, 4 * ceil(mean)) entries, when they are
+    outliers (at most 1/8 of the rows) -- the same rule as the solver's level
+    upload (csrc/solver.cu upload_csr).  Returns (device int32 rows, thr) or
+    (None, 0)."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    n = rp.size - 1
+    if n <= 0 or rp[-1] <= 0:
+        return None, 0
+    thr = max(64, 4 * (-(-int(rp[-1]) // n)))
+    rows = np.flatnonzero(np.diff(rp) > thr).astype(np.int32)
+    if rows.size == 0 or rows.size * 8 > n:
+        return None, 0
+    return torch.from_numpy(rows).to(device), thr
 
 
 def _csr_view(row_ptr, col_idx, values, nrows, ncols):

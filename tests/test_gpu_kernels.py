@@ -214,3 +214,35 @@ def test_gs_sweep_slab_indices_symmetric_pair(m, rng):
         K.gs_sweep(D, None, None, T(dp), T(b), T(zero), x, fwd)
     torch.cuda.synchronize()
     np.testing.assert_array_equal(x.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("m", [1, 2, 3, 4, 8, 16, 32, 64])
+@pytest.mark.parametrize("vdt", [np.float64, np.float32])
+@pytest.mark.parametrize("slab", [False, True])
+def test_spmv_long_rows_bitwise(m, vdt, slab, rng):
+    """Rows far longer than the mean (the AMG coarse-level pattern) run on
+    whole CTAs (kernels.long_row_split): still bitwise the reference order."""
+    import scipy.sparse as sp
+    n = 6000
+    base = sp.random(n, n, density=8.0 / n, random_state=7, format="csr")
+    rows, cols = [], []
+    for i in rng.choice(n, 40, replace=False):
+        L = int(rng.integers(300, 3000))             # > one 2048-product chunk at m = 1
+        js = np.sort(rng.choice(n, L, replace=False))
+        rows += [i] * L
+        cols += list(js)
+    M = (base + sp.csr_matrix((rng.standard_normal(len(rows)), (rows, cols)), shape=(n, n))).tocsr()
+    M.sort_indices()
+    blk = CsrBlock.from_scipy(M)
+    vals = blk.values.astype(vdt)
+    D = K.DeviceCsr(blk.row_ptr, blk.col_idx, vals, n, n, slab=slab)
+    assert D.long_rows is not None and D.long_rows.numel() >= 40
+    x = rng.standard_normal((n, m))
+    b = rng.standard_normal((n, m))
+    y0 = rng.standard_normal((n, m))
+    for mode in range(4):
+        y = T(y0)
+        K.csr_spmv(D, None, None, T(x), y, mode, T(b) if mode == 3 else None)
+        ref = y0.copy()
+        O.csr_spmv(blk.row_ptr, blk.col_idx, vals, x, ref, mode, b if mode == 3 else None)
+        np.testing.assert_array_equal(y.cpu().numpy(), ref, err_msg=f"mode {mode}")

@@ -363,3 +363,53 @@ def test_dense_tail_matches_per_level_kernels(roles, m, monkeypatch):
     assert out[0][0] == out[2500][0]
     np.testing.assert_allclose(out[2500][1], out[0][1], rtol=0, atol=1e-9 * np.abs(out[0][1]).max())
     assert out[2500][2] < out[0][2]
+
+
+def _arrowhead_system(g=16, nlong=12, width=400, seed=5):
+    """SPD Poisson-plus-arrowhead matrix: `nlong` rows coupled to `width`
+    random columns each (symmetrised, diagonally dominant), so level 0 (and
+    the coarse operators built from it) carry rows far longer than the mean."""
+    import scipy.sparse as sp
+    A, _ = gen_poisson3d(g, g, g)
+    n = A.nrows
+    rng = np.random.default_rng(seed)
+    rows, cols = [], []
+    for i in rng.choice(n, nlong, replace=False):
+        js = rng.choice(n, width, replace=False)
+        js = js[js != i]
+        rows += [i] * len(js)
+        cols += list(js)
+    E = sp.csr_matrix((rng.uniform(-0.5, 0.5, len(rows)), (rows, cols)), shape=(n, n))
+    E = E + E.T
+    M = A.to_scipy() + E
+    M = M + sp.diags(np.abs(E).sum(axis=1).A1)
+    return CsrBlock.from_scipy(sp.csr_matrix(M))
+
+
+@pytest.mark.parametrize("roles", [GG.SOLVE_CASES["c2_amg_pcg_20"][3],
+                                   GG.SOLVE_CASES["c3_amg_bicgstab_full_cheb3"][3],
+                                   GG.SOLVE_CASES["c3_amg_bicgstab_mixed"][3]])
+@pytest.mark.parametrize("m", [1, 4, 8, 16, 3])
+def test_long_row_ctas_bitwise(roles, m):
+    """Rows far longer than their operator's mean are accumulated by whole
+    CTAs (products in parallel, in-order fold; the SpMM itself is bitwise the
+    lane path, test_gpu_kernels.py::test_spmv_long_rows_bitwise).  In a solve
+    only the fused dots' CTA partition changes: same iterations, solutions
+    equal to the last bits."""
+    from paper_2103_07329_b200 import _lib
+    A = _arrowhead_system()
+    lens = np.diff(A.row_ptr)
+    assert lens.max() > max(64, 4 * lens.mean())
+    B = np.random.default_rng(m).uniform(-1, 1, (A.nrows, m))
+    out = {}
+    try:
+        for split in (0, 1):
+            _lib.set_option("spmm_long_split", split)
+            cs = prepare(tree(roles), A)
+            X = BlockVector.zeros(A.nrows, m)
+            st = cs.run(BlockVector.from_array(B), X)
+            out[split] = (st.iterations, X.data.copy(), np.array(st.residual_history))
+    finally:
+        _lib.set_option("spmm_long_split", 1)
+    assert out[0][0] == out[1][0]
+    np.testing.assert_allclose(out[1][1], out[0][1], rtol=0, atol=1e-12 * np.abs(out[0][1]).max())
