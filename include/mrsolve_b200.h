@@ -290,6 +290,9 @@ int  mrs_version(void);
  *   "spmm_chunk_rows" N  rows per CTA chunk of the SpMM grid (default 64)
  *   "spmm_long_split" 0/1  rows far longer than their operator's mean run on
  *                   whole CTAs (default 1; solver levels only)
+ *   "spmm_coop" 0/1  operators with >= 12 entries per row (outside the LONG range)
+ *                   load a row's entries once per lane group and shuffle them
+ *                   (default 1)
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

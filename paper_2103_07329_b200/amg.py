@@ -179,7 +179,7 @@ def coarse_inverse(A) -> np.ndarray:
 
 #: Largest level (rows) the V-cycle tail may be collapsed from (dense n x n
 #: operator, n^2 * 8 bytes); 0 disables.  Env MRS_DENSE_TAIL_ROWS.
-DENSE_TAIL_ROWS = int(__import__("os").environ.get("MRS_DENSE_TAIL_ROWS", "12000"))
+DENSE_TAIL_ROWS = int(__import__("os").environ.get("MRS_DENSE_TAIL_ROWS", "8000"))
 # cost model of the choice (microseconds; B200 measurements, profiles/r01_ab_experiments.txt):
 # a solve-path kernel costs ~_T_LAUNCH plus _T_ROUND per dependent load round of its
 # longest row (16 entries in flight); the dense product streams n^2*8 bytes at _DENSE_BW

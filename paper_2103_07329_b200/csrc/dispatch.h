@@ -54,6 +54,7 @@ void set_coarse_rows(int64_t v);
 void set_spmm_long_rows(int64_t v);
 void set_spmm_chunk_rows(int64_t v);
 void set_spmm_long_split(int64_t v);
+void set_spmm_coop(int64_t v);
 int64_t spmm_long_split();
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;

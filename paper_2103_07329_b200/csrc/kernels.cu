@@ -33,6 +33,9 @@ void set_spmm_chunk_rows(int64_t v) { g_chunk_rows = v < 1 ? 1 : v; }
 static int64_t g_long_split = 1;      // long rows by whole CTAs (0: lane path only)
 int64_t spmm_long_split() { return g_long_split; }
 void set_spmm_long_split(int64_t v) { g_long_split = v ? 1 : 0; }
+static int64_t g_coop = 0;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
+int64_t spmm_coop() { return g_coop; }
+void set_spmm_coop(int64_t v) { g_coop = v ? 1 : 0; }
 static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }

@@ -12,6 +12,7 @@ namespace mrs {
 
 int64_t spmm_long_max_rows();   // LONG-row SpMM variant up to this many rows (knob)
 int64_t spmm_chunk_rows();      // rows per CTA chunk of the SpMM grid (knob)
+int64_t spmm_coop();            // cooperative entry loads for long-row operators (knob)
 
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
@@ -94,6 +95,15 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         case 4: go(spmm_kernel<4, OP, Tv, Ti, true>, Lay<4>::RPB); return cudaGetLastError();
         case 8: go(spmm_kernel<8, OP, Tv, Ti, true>, Lay<8>::RPB); return cudaGetLastError();
         case 16: go(spmm_kernel<16, OP, Tv, Ti, true>, Lay<16>::RPB); return cudaGetLastError();
+        default: break;
+        }
+    }
+    // large operators with long rows: cooperative entry loads (coop_accumulate)
+    if (!generic && spmm_coop() && a.nnz_hint >= 12 * a.nrows) {
+        switch (m) {
+        case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB); return cudaGetLastError();
+        case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB); return cudaGetLastError();
+        case 16: go(spmm_kernel<16, OP, Tv, Ti, false, true>, Lay<16>::RPB); return cudaGetLastError();
         default: break;
         }
     }

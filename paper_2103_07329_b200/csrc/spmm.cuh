@@ -387,10 +387,59 @@ template <int M, int OP> constexpr int spmm_min_blocks() {
     return (OP == OP_SPMV || OP == OP_JAC_SWEEP) ? 6 : 5;
 }
 
+// Operators with long rows on average (27-point stencils, the banded random
+// C5 matrix: >= 12 entries per row): the LPR lanes of a row load LPR
+// consecutive entries with ONE load each and exchange (column, value) by
+// shuffles, instead of every lane loading every entry -- the replicated
+// value loads were half of the kernel's L1 wavefronts (a warp's 8 rows sit
+// in 8 different lines per entry).  Same entry order, same bits.  The trip
+// count is warp-uniform (the warp's longest row); `live` rows accumulate.
+template <int CPL, int LPR, class Src>
+__device__ __forceinline__ void coop_accumulate(const SpArgs& a, const Src& src, int lo, int len,
+                                                int ld, int cofs, bool live, bool subtract,
+                                                double (&acc)[CPL]) {
+    const int l = threadIdx.x % LPR;
+    const int gbase = (threadIdx.x % 32) & ~(LPR - 1);
+    const int wlen = __reduce_max_sync(0xffffffffu, len);
+    for (int k = 0; k < wlen; k += LPR) {
+        const int e = k + l;
+        const int kk = e < len ? lo + e : lo;
+        const int cm = len > 0 ? src.col(kk) : 0;
+        const double vm = len > 0 ? src.val(kk) : 0.0;
+        int c[LPR];
+        double v[LPR];
+#pragma unroll
+        for (int u = 0; u < LPR; ++u) {
+            c[u] = __shfl_sync(0xffffffffu, cm, gbase + u);
+            v[u] = __shfl_sync(0xffffffffu, vm, gbase + u);
+        }
+        if (live && k < len) {
+            Vec<CPL> g[LPR];
+#pragma unroll
+            for (int u = 0; u < LPR; ++u) g[u] = load_vec<CPL>(a.x + c[u] * ld + cofs);
+            compiler_fence();
+            if (subtract) {
+#pragma unroll
+                for (int u = 0; u < LPR; ++u)
+                    if (k + u < len)
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) acc[i] = sub(acc[i], mul(v[u], g[u].v[i]));
+            } else {
+#pragma unroll
+                for (int u = 0; u < LPR; ++u)
+                    if (k + u < len)
+#pragma unroll
+                        for (int i = 0; i < CPL; ++i) acc[i] = add(acc[i], mul(v[u], g[u].v[i]));
+            }
+        }
+    }
+}
+
 // LONG: small operators with long rows (AMG coarse levels, >= 12 nnz/row):
 // 16 entries in flight per lane -- the row's dependent chain is 4x shorter;
 // register-heavy, so only used where few CTAs run anyway.  Same order.
-template <int M, int OP, typename Tv, typename Ti, bool LONG = false>
+// COOP: large operators with long rows (coop_accumulate), M in {4, 8, 16}.
+template <int M, int OP, typename Tv, typename Ti, bool LONG = false, bool COOP = false>
 __global__ void __launch_bounds__(kThreads, LONG ? 1 : spmm_min_blocks<M, OP>())
 spmm_kernel(SpArgs a) {
     pdl_enter();
@@ -409,6 +458,29 @@ spmm_kernel(SpArgs a) {
         // long rows: one CTA each (long_row_cta), strided over the long CTAs
         for (int j = (int)blockIdx.x - gl; j < a.n_long; j += a.long_ctas)
             long_row_cta<M, OP, Tv, Ti>(a, src, __ldg(a.long_rows + j), dotp);
+    } else if constexpr (COOP) {
+        const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
+        for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
+            const int r1 = min(r0 + chunk, nrows);
+            for (int rb = r0; rb < r1; rb += RPB) {            // warp-uniform passes
+                const int row = rb + threadIdx.x / LPR;
+                int lo = 0, len = 0;
+                bool live = row < r1;
+                if (live) {
+                    lo = __ldg(a.rp + row);
+                    len = __ldg(a.rp + row + 1) - lo;
+                    if (len > lthr) { live = false; len = 0; }  // done by a long-row CTA
+                }
+                const GSrc<Tv, Ti> rs = live ? src.at_row(a, row) : src;
+                const int o = row * M + cofs;
+                double acc[CPL];
+                Vec<CPL> keep;
+                bool subtract = false;
+                if (live) row_begin<OP, CPL>(a, o, acc, keep, subtract);
+                coop_accumulate<CPL, LPR>(a, rs, lo, len, M, cofs, live, subtract, acc);
+                if (live) row_end<OP, CPL>(a, row, o, acc, keep, dotp);
+            }
+        }
     } else {
         const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
         for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {

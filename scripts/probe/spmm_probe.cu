@@ -77,7 +77,7 @@ template <int CPL> __device__ __forceinline__ void stv(double* p, const V<CPL>& 
 // ---------------------------------------------------------------- baseline
 // replica of the library's spmm_kernel<M, OP_SPMV RSUB>: lanes over columns,
 // groups of UNR entries, chunk-strided one-wave grid.
-template <int M, typename Ti, int UNR, int MINB>
+template <int M, typename Ti, int UNR, int MINB, int OWN = 0>
 __global__ void __launch_bounds__(256, MINB) k_base(Args a) {
     constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR, RPB = 256 / LPR;
     const int cofs = (threadIdx.x % LPR) * CPL;
@@ -98,6 +98,10 @@ __global__ void __launch_bounds__(256, MINB) k_base(Args a) {
                     v[u] = __ldg(a.v + kk);
                 }
                 fence();
+                if (OWN == 1) {
+#pragma unroll
+                    for (int u = 0; u < UNR; ++u) c[u] = (c[u] & 0) + row;   // keep the dependency, hit own row
+                }
 #pragma unroll
                 for (int u = 0; u < UNR; ++u) g[u] = ldx<CPL>(a.x + c[u] * M + cofs);
                 fence();
@@ -413,6 +417,20 @@ static void flush_l2() {
     CK(cudaMemsetAsync(g_flush, 0, 256u << 20));
 }
 
+template <class F> static float time_b2b_us(F&& f, int reps = 40) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    f();
+    flush_l2();
+    cudaEventRecord(e0);
+    for (int r = 0; r < reps; ++r) f();
+    cudaEventRecord(e1);
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    return ms * 1e3f / reps;
+}
 template <class F> static float time_us(F&& f, int reps = 15) {
     std::vector<float> ts;
     cudaEvent_t e0, e1;
@@ -435,9 +453,9 @@ template <class F> static float time_us(F&& f, int reps = 15) {
 
 static int nsm() { int v; cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, 0); return v; }
 
-template <int M, typename Ti, int UNR, int MINB>
+template <int M, typename Ti, int UNR, int MINB, int OWN = 0>
 static void run_base(Args a, int& grid) {
-    auto kern = k_base<M, Ti, UNR, MINB>;
+    auto kern = k_base<M, Ti, UNR, MINB, OWN>;
     int bps;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
     constexpr int RPB = 256 / Lay<M>::LPR;
@@ -772,6 +790,81 @@ static void to_g4(const Csr& A, const std::vector<Ti>& cols, int C, std::vector<
     }
 }
 
+
+// cooperative entry loads: the LPR lanes of a row load LPR consecutive
+// entries (one each) and exchange them by shuffles, instead of every lane
+// loading every entry.  Warp-uniform trip count (max row length in the warp).
+template <int M, typename Ti, int MINB, int G2 = 1>
+__global__ void __launch_bounds__(256, MINB) k_coop(Args a) {
+    constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR, RPB = 256 / LPR;
+    constexpr int G = LPR * G2;                 // entries per group
+    const int l = threadIdx.x % LPR;
+    const int cofs = l * CPL;
+    const int gbase = (threadIdx.x % 32) & ~(LPR - 1);
+    const Ti* ci = (const Ti*)a.ci;
+    for (int r0 = blockIdx.x * a.chunk; r0 < a.n; r0 += gridDim.x * a.chunk) {
+        const int r1 = min(r0 + a.chunk, a.n);
+        for (int rb = r0; rb < r1; rb += RPB) {        // warp-uniform pass loop
+            const int row = rb + threadIdx.x / LPR;
+            const bool live = row < r1;
+            const int base = (live && a.slab) ? __ldg(a.slab + (row >> a.slab_shift)) : 0;
+            const int lo = live ? __ldg(a.rp + row) : 0, hi = live ? __ldg(a.rp + row + 1) : 0;
+            const int len = hi - lo;
+            const int wlen = __reduce_max_sync(0xffffffffu, len);
+            const int o = row * M + cofs;
+            V<CPL> acc;
+            if (live) acc = ldx<CPL>(a.b + o);
+            for (int k = 0; k < wlen; k += G) {
+                int cm[G2]; double vm[G2];
+#pragma unroll
+                for (int j = 0; j < G2; ++j) {
+                    const int e = k + j * LPR + l;
+                    const int kk = e < len ? lo + e : lo;
+                    cm[j] = (len > 0) ? base + (int)__ldg(ci + kk) : 0;
+                    vm[j] = (len > 0) ? __ldg(a.v + kk) : 0.0;
+                }
+                V<CPL> g[G];
+                const bool act = live && k < len;
+#pragma unroll
+                for (int j = 0; j < G2; ++j)
+#pragma unroll
+                    for (int u = 0; u < LPR; ++u) {
+                        const int cu = __shfl_sync(0xffffffffu, cm[j], gbase + u);
+                        if (act) g[j * LPR + u] = ldx<CPL>(a.x + cu * M + cofs);
+                    }
+                fence();
+#pragma unroll
+                for (int j = 0; j < G2; ++j)
+#pragma unroll
+                    for (int u = 0; u < LPR; ++u) {
+                        const double vu = __shfl_sync(0xffffffffu, vm[j], gbase + u);
+                        if (act && k + j * LPR + u < len)
+#pragma unroll
+                            for (int i = 0; i < CPL; ++i)
+                                acc.v[i] = sub(acc.v[i], mul(vu, g[j * LPR + u].v[i]));
+                    }
+            }
+            if (live) stv<CPL>(a.y + o, acc);
+        }
+    }
+}
+
+template <int M, typename Ti, int MINB, int G2>
+static void run_coop(Args a) {
+    auto kern = k_coop<M, Ti, MINB, G2>;
+    int bps;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, 256, 0);
+    constexpr int RPB = 256 / Lay<M>::LPR;
+    const long cap = (long)bps * nsm();
+    const long P = (a.n + RPB - 1) / RPB, ppc = (P + cap - 1) / cap;
+    long pmax = std::max(1, 64 / RPB);
+    const long sp = std::min(ppc, pmax);
+    const long nch = (P + sp - 1) / sp, cpc = (nch + cap - 1) / cap;
+    const int grid = (int)((nch + cpc - 1) / cpc);
+    a.chunk = (int)(RPB * sp);
+    kern<<<grid, 256>>>(a);
+}
+
 static double bytes_of(const Csr& A, int m, int ib, int nslab) {
     return (double)A.ci.size() * (8 + ib) + (A.n + 1) * 4.0 + nslab * 4.0 + 3.0 * A.n * m * 8;
 }
@@ -826,6 +919,29 @@ template <int M, int EPR> static void bench_matrix(const Csr& A) {
     Args a32 = a; a32.ci = ci32; a32.y = y1;
     Args a16 = a; a16.ci = ci16; a16.slab = sb; a16.slab_shift = shift; a16.y = y1;
     int g;
+    if (getenv("COOP")) {
+        g_chunk_rows = 64;
+        check("base u16slab 6/SM", time_us([&] { run_base<M, uint16_t, 4, 6>(a16, g); }), b16);
+        g_chunk_rows = 0;
+        if constexpr (M > 1) {
+            check("coop u16slab G=LPR 6/SM", time_us([&] { run_coop<M, uint16_t, 6, 1>(a16); }), b16);
+            check("coop u16slab G=LPR 5/SM", time_us([&] { run_coop<M, uint16_t, 5, 1>(a16); }), b16);
+            check("coop u16slab G=2LPR 5/SM", time_us([&] { run_coop<M, uint16_t, 5, 2>(a16); }), b16);
+            check("coop u16slab G=2LPR 4/SM", time_us([&] { run_coop<M, uint16_t, 4, 2>(a16); }), b16);
+            check("coop u32 G=LPR 6/SM", time_us([&] { run_coop<M, uint32_t, 6, 1>(a32); }), b32);
+        }
+        return;
+    }
+    if (getenv("OWN")) {
+        g_chunk_rows = 64;
+        check("base u16slab (cold)", time_us([&] { run_base<M, uint16_t, 4, 6>(a16, g); }), b16);
+        check("base u16slab (b2b, L2-warm)", time_b2b_us([&] { run_base<M, uint16_t, 4, 6>(a16, g); }), b16);
+        const float t = time_us([&] { run_base<M, uint16_t, 4, 6, 1>(a16, g); });
+        printf("  %-40s %9.2f us  %6.0f GB/s\n", "own-row gather (cold, no real gather)", t, b16 / t / 1e3);
+        CK(cudaMemset(y1, 0, hx.size() * 8));
+        g_chunk_rows = 0;
+        return;
+    }
     if (getenv("G4")) {
         g_chunk_rows = 64;
         check("base u16slab 6/SM chunk 64", time_us([&] { run_base<M, uint16_t, 4, 6>(a16, g); }), b16);

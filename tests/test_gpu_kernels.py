@@ -246,3 +246,28 @@ def test_spmv_long_rows_bitwise(m, vdt, slab, rng):
         ref = y0.copy()
         O.csr_spmv(blk.row_ptr, blk.col_idx, vals, x, ref, mode, b if mode == 3 else None)
         np.testing.assert_array_equal(y.cpu().numpy(), ref, err_msg=f"mode {mode}")
+
+
+@pytest.mark.parametrize("m", [4, 8, 16])
+@pytest.mark.parametrize("vdt", [np.float64, np.float32])
+@pytest.mark.parametrize("coop", [0, 1])
+def test_spmv_coop_entry_loads_bitwise(m, vdt, coop, rng):
+    """Operators with >= 12 entries per row (beyond the LONG range) load each
+    entry once per lane group and shuffle it (spmm_coop): still bitwise."""
+    from mrs_testutil import random_csr
+    from paper_2103_07329_b200 import _lib
+    n = 40000
+    blk = random_csr(n, n, 20.0, rng)
+    vals = blk.values.astype(vdt)
+    x = rng.standard_normal((n, m))
+    b = rng.standard_normal((n, m))
+    y0 = rng.standard_normal((n, m))
+    try:
+        _lib.set_option("spmm_coop", coop)
+        for mode in range(4):
+            y = spmv_dev(blk.row_ptr, blk.col_idx, vals, x, y0, mode, b if mode == 3 else None)
+            ref = y0.copy()
+            O.csr_spmv(blk.row_ptr, blk.col_idx, vals, x, ref, mode, b if mode == 3 else None)
+            np.testing.assert_array_equal(y, ref, err_msg=f"mode {mode}")
+    finally:
+        _lib.set_option("spmm_coop", 0)
