@@ -12,6 +12,7 @@ hierarchy built by the reference itself is accepted too (duck-typed).
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -179,7 +180,7 @@ def coarse_inverse(A) -> np.ndarray:
 
 #: Largest level (rows) the V-cycle tail may be collapsed from (dense n x n
 #: operator, n^2 * 8 bytes); 0 disables.  Env MRS_DENSE_TAIL_ROWS.
-DENSE_TAIL_ROWS = int(__import__("os").environ.get("MRS_DENSE_TAIL_ROWS", "8000"))
+DENSE_TAIL_ROWS = int(os.environ.get("MRS_DENSE_TAIL_ROWS", "8000"))
 # cost model of the choice (microseconds; B200 measurements, profiles/r01_ab_experiments.txt):
 # a solve-path kernel costs ~_T_LAUNCH plus _T_ROUND per dependent load round of its
 # longest row (16 entries in flight); the dense product streams n^2*8 bytes at _DENSE_BW
@@ -295,5 +296,13 @@ def vcycle_tail_operator(levels, start: int, pre, post, inv) -> np.ndarray | Non
         x = x + P @ xc
         return smooth(post, k, b, x)
 
+    # columns in blocks: host memory stays O(n * block) however large n_l is
     n = mats[0][0].shape[0]
-    return np.ascontiguousarray(vcycle(0, np.eye(n)))
+    T = np.empty((n, n))
+    block = 512
+    for j0 in range(0, n, block):
+        j1 = min(n, j0 + block)
+        E = np.zeros((n, j1 - j0))
+        E[np.arange(j0, j1), np.arange(j1 - j0)] = 1.0
+        T[:, j0:j1] = vcycle(0, E)
+    return T

@@ -1044,10 +1044,37 @@ done:
     if (sb) cudaFree(sb);
 }
 
+
+__global__ void k_empty(int* p) { if (p && threadIdx.x == 1023) p[0] = 1; }
+
+static void graph_gap() {
+    cudaStream_t st;
+    cudaStreamCreate(&st);
+    for (int grid : {1, 148, 888}) {
+        cudaGraph_t g;
+        cudaGraphExec_t ge;
+        CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal));
+        for (int i = 0; i < 200; ++i) k_empty<<<grid, 256, 0, st>>>(nullptr);
+        CK(cudaStreamEndCapture(st, &g));
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        CK(cudaGraphLaunch(ge, st));
+        CK(cudaStreamSynchronize(st));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        cudaEventRecord(e0, st);
+        for (int r = 0; r < 10; ++r) CK(cudaGraphLaunch(ge, st));
+        cudaEventRecord(e1, st);
+        CK(cudaEventSynchronize(e1));
+        float ms; cudaEventElapsedTime(&ms, e0, e1);
+        printf("graph of 200 empty kernels, grid %d: %.3f us per kernel\n", grid, ms * 1e3 / 2000);
+    }
+}
+
 int main(int argc, char** argv) {
     CK(cudaMalloc(&g_flush, 256u << 20));
     const char* which = argc > 1 ? argv[1] : "all";
     auto want = [&](const char* k) { return !strcmp(which, "all") || strstr(which, k); };
+    if (!strcmp(which, "gap")) { graph_gap(); return 0; }
     if (want("c2")) { Csr A = poisson7(64); bench_matrix<8, 8>(A); }
     if (want("c3")) { Csr A = poisson7(128); bench_matrix<16, 8>(A); bench_matrix<8, 8>(A); }
     if (want("c4")) { Csr A = stencil27(128); bench_matrix<8, 32>(A); }
