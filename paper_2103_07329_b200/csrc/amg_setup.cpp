@@ -18,10 +18,14 @@
 // Compiled with -ffp-contract=off and no -march flags: every multiply-add is
 // separately rounded, like the x86-64 baseline builds of numpy/scipy.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <thread>
 #include <vector>
 
 #include "../../include/mrsolve_b200.h"
@@ -37,6 +41,52 @@ struct Csr {
 };
 
 constexpr int8_t U = 0, C = 1, F = 2;
+
+// Row-parallel phases (strength, Galerkin products, row sorts) run on host
+// threads: every output row is computed by one thread with the same
+// per-row operation order as the sequential code, so the hierarchy is
+// bitwise the same for any thread count.  MRS_SETUP_THREADS overrides.
+int setup_threads() {
+    static int t = 0;
+    if (!t) {
+        const char* e = getenv("MRS_SETUP_THREADS");
+        t = e ? atoi(e) : (int)std::thread::hardware_concurrency();
+        t = std::max(1, std::min(t, 16));
+    }
+    return t;
+}
+
+// fn(lo, hi, part) over `parts` contiguous row ranges of [0, n).
+template <class Fn> void for_row_parts(int64_t n, int parts, Fn fn) {
+    if (parts <= 1 || n < 4096) { fn(0, n, 0); return; }
+    std::vector<std::thread> th;
+    for (int p = 0; p < parts; ++p) {
+        const int64_t lo = n * p / parts, hi = n * (p + 1) / parts;
+        th.emplace_back([=, &fn] { fn(lo, hi, p); });
+    }
+    for (auto& t : th) t.join();
+}
+
+// Rows built per part (count, columns, values), concatenated in row order.
+struct RowParts {
+    std::vector<std::vector<int64_t>> len, ci;
+    std::vector<std::vector<double>> v;
+    explicit RowParts(int parts) : len(parts), ci(parts), v(parts) {}
+    void into(Csr& out) {
+        out.rp.assign(out.nrows + 1, 0);
+        int64_t row = 0, total = 0;
+        for (size_t p = 0; p < len.size(); ++p)
+            for (int64_t l : len[p]) { total += l; out.rp[++row] = total; }
+        out.ci.clear(); out.v.clear();
+        out.ci.reserve(total); out.v.reserve(total);
+        for (size_t p = 0; p < len.size(); ++p) {
+            out.ci.insert(out.ci.end(), ci[p].begin(), ci[p].end());
+            out.v.insert(out.v.end(), v[p].begin(), v[p].end());
+            std::vector<int64_t>().swap(ci[p]);
+            std::vector<double>().swap(v[p]);
+        }
+    }
+};
 
 // numpy's pairwise summation (loops_utils.h, PW_BLOCKSIZE 128) for a
 // contiguous float64 array: what `arr.sum()` computes.
@@ -83,42 +133,53 @@ Csr transpose(const Csr& A) {
 Csr matmat(const Csr& A, const Csr& B) {
     Csr Cm;
     Cm.nrows = A.nrows; Cm.ncols = B.ncols;
-    Cm.rp.assign(A.nrows + 1, 0);
-    std::vector<int64_t> next(B.ncols, -1);
-    std::vector<double> sums(B.ncols, 0.0);
-    for (int64_t i = 0; i < A.nrows; ++i) {
-        int64_t head = -2, length = 0;
-        for (int64_t jj = A.rp[i]; jj < A.rp[i + 1]; ++jj) {
-            const int64_t j = A.ci[jj];
-            const double v = A.v[jj];
-            for (int64_t kk = B.rp[j]; kk < B.rp[j + 1]; ++kk) {
-                const int64_t k = B.ci[kk];
-                sums[k] += v * B.v[kk];
-                if (next[k] == -1) { next[k] = head; head = k; ++length; }
+    // dense per-thread scratch of B.ncols entries: cap the threads by memory
+    const int parts = std::max<int>(1, std::min<int64_t>(setup_threads(),
+                                                         (int64_t)(2e9 / (16.0 * (B.ncols + 1)))));
+    RowParts rows(parts);
+    for_row_parts(A.nrows, parts, [&](int64_t r0, int64_t r1, int part) {
+        std::vector<int64_t> next(B.ncols, -1);
+        std::vector<double> sums(B.ncols, 0.0);
+        auto& len = rows.len[part];
+        auto& oc = rows.ci[part];
+        auto& ov = rows.v[part];
+        for (int64_t i = r0; i < r1; ++i) {
+            int64_t head = -2, length = 0, kept = 0;
+            for (int64_t jj = A.rp[i]; jj < A.rp[i + 1]; ++jj) {
+                const int64_t j = A.ci[jj];
+                const double v = A.v[jj];
+                for (int64_t kk = B.rp[j]; kk < B.rp[j + 1]; ++kk) {
+                    const int64_t k = B.ci[kk];
+                    sums[k] += v * B.v[kk];
+                    if (next[k] == -1) { next[k] = head; head = k; ++length; }
+                }
             }
+            for (int64_t jj = 0; jj < length; ++jj) {
+                if (sums[head] != 0) { oc.push_back(head); ov.push_back(sums[head]); ++kept; }
+                int64_t tmp = head;
+                head = next[head];
+                next[tmp] = -1;
+                sums[tmp] = 0;
+            }
+            len.push_back(kept);
         }
-        for (int64_t jj = 0; jj < length; ++jj) {
-            if (sums[head] != 0) { Cm.ci.push_back(head); Cm.v.push_back(sums[head]); }
-            int64_t tmp = head;
-            head = next[head];
-            next[tmp] = -1;
-            sums[tmp] = 0;
-        }
-        Cm.rp[i + 1] = Cm.nnz();
-    }
+    });
+    rows.into(Cm);
     return Cm;
 }
 
 void sort_rows(Csr& A) {
-    std::vector<std::pair<int64_t, double>> row;
-    for (int64_t i = 0; i < A.nrows; ++i) {
-        int64_t lo = A.rp[i], hi = A.rp[i + 1];
-        row.clear();
-        for (int64_t k = lo; k < hi; ++k) row.emplace_back(A.ci[k], A.v[k]);
-        std::sort(row.begin(), row.end(),
-                  [](const auto& a, const auto& b) { return a.first < b.first; });
-        for (int64_t k = lo; k < hi; ++k) { A.ci[k] = row[k - lo].first; A.v[k] = row[k - lo].second; }
-    }
+    for_row_parts(A.nrows, setup_threads(), [&](int64_t r0, int64_t r1, int) {
+        std::vector<std::pair<int64_t, double>> row;
+        for (int64_t i = r0; i < r1; ++i) {
+            int64_t lo = A.rp[i], hi = A.rp[i + 1];
+            row.clear();
+            for (int64_t k = lo; k < hi; ++k) row.emplace_back(A.ci[k], A.v[k]);
+            std::sort(row.begin(), row.end(),
+                      [](const auto& a, const auto& b) { return a.first < b.first; });
+            for (int64_t k = lo; k < hi; ++k) { A.ci[k] = row[k - lo].first; A.v[k] = row[k - lo].second; }
+        }
+    });
 }
 
 // strength_graph (amg.py:55-78): S[i,j] iff j != i and
@@ -126,18 +187,27 @@ void sort_rows(Csr& A) {
 Csr strength(const Csr& A, double theta) {
     Csr S;
     S.nrows = A.nrows; S.ncols = A.ncols;
-    S.rp.assign(A.nrows + 1, 0);
-    for (int64_t i = 0; i < A.nrows; ++i) {
-        double rowmax = 0.0;
-        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
-            if (A.ci[k] != i) rowmax = std::max(rowmax, -A.v[k]);
-        if (rowmax > 0) {
-            const double thr = theta * rowmax;
+    const int parts = setup_threads();
+    RowParts rows(parts);
+    for_row_parts(A.nrows, parts, [&](int64_t r0, int64_t r1, int part) {
+        for (int64_t i = r0; i < r1; ++i) {
+            double rowmax = 0.0;
+            int64_t kept = 0;
             for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
-                if (A.ci[k] != i && -A.v[k] >= thr) { S.ci.push_back(A.ci[k]); S.v.push_back(1.0); }
+                if (A.ci[k] != i) rowmax = std::max(rowmax, -A.v[k]);
+            if (rowmax > 0) {
+                const double thr = theta * rowmax;
+                for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k)
+                    if (A.ci[k] != i && -A.v[k] >= thr) {
+                        rows.ci[part].push_back(A.ci[k]);
+                        rows.v[part].push_back(1.0);
+                        ++kept;
+                    }
+            }
+            rows.len[part].push_back(kept);
         }
-        S.rp[i + 1] = S.nnz();
-    }
+    });
+    rows.into(S);
     return S;
 }
 
@@ -273,26 +343,42 @@ int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarc
     chain.push_back(from_host(Ah));
     sort_rows(chain.back());
     std::vector<Csr> Ps;
+    const bool timing = getenv("MRS_SETUP_TIMING") != nullptr;
+    double tphase[6] = {0, 0, 0, 0, 0, 0};
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
     while (chain.back().nrows > prm->coarse_matrix_size && (int)chain.size() < prm->max_levels) {
         const Csr& M = chain.back();
+        auto t0 = now();
         Csr S = strength(M, prm->strength_threshold);
+        auto t1 = now();
         const bool agg = (int)chain.size() - 1 < prm->agg_num_levels;
         std::vector<int8_t> st = split(S, agg, prm->num_paths);
+        auto t2 = now();
         Csr P;
         std::vector<int64_t> bad;
         if (!interp(M, S, st, P, bad)) {
             for (int64_t r : bad) st[r] = C;
             if (!interp(M, S, st, P, bad)) return MRS_ERR_DEGENERATE;
         }
+        auto t3 = now();
         const int64_t ncoarse = P.ncols;
         if (ncoarse == 0 || (double)ncoarse > prm->stall_ratio * (double)M.nrows) break;
         Csr R = transpose(P);
         Csr RA = matmat(R, M);
+        auto t4 = now();
         Csr Ac = matmat(RA, P);
+        auto t5 = now();
         sort_rows(Ac);
+        auto t6 = now();
+        tphase[0] += secs(t0, t1); tphase[1] += secs(t1, t2); tphase[2] += secs(t2, t3);
+        tphase[3] += secs(t3, t4); tphase[4] += secs(t4, t5); tphase[5] += secs(t5, t6);
         Ps.push_back(std::move(P));
         chain.push_back(std::move(Ac));
     }
+    if (timing)
+        fprintf(stderr, "[mrs_amg_setup] strength %.2fs split %.2fs interp %.2fs RA %.2fs RAP %.2fs sort %.2fs (%d threads)\n",
+                tphase[0], tphase[1], tphase[2], tphase[3], tphase[4], tphase[5], setup_threads());
     mrs_hierarchy* h = new mrs_hierarchy();
     h->levels.resize(chain.size());
     for (size_t l = 0; l < chain.size(); ++l) {
