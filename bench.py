@@ -380,6 +380,13 @@ def main():
             print(f"[bench] distributed path failed ({dist_error}); running replicas",
                   file=sys.stderr)
             partitioned = False
+        if dist is not None:
+            # every rank takes the same path: replicas as soon as any rank failed
+            flag = torch.tensor([0 if partitioned else 1], device="cuda")
+            dist.all_reduce(flag, op=dist.ReduceOp.MAX)
+            if int(flag.item()) and partitioned:
+                partitioned = False
+                dist_error = dist_error or "another rank's distributed path failed"
     if not partitioned:
         cs = prepare(tree(ROLES), A, exec_mode=args.exec)
     lo, hi = getattr(cs, "row_range", (0, nglob)) if partitioned else (0, nglob)
