@@ -185,6 +185,7 @@ DENSE_TAIL_ROWS = int(os.environ.get("MRS_DENSE_TAIL_ROWS", "8000"))
 # a solve-path kernel costs ~_T_LAUNCH plus _T_ROUND per dependent load round of its
 # longest row (16 entries in flight); the dense product streams n^2*8 bytes at _DENSE_BW
 _T_LAUNCH, _T_ROUND, _DENSE_BW = 3.0, 1.0, 1.4e6     # us, us, bytes/us
+_SGS_KERNEL_FACTOR = 10     # a Gauss-Seidel half-sweep ~ 10 SpMM launches (schedule barriers)
 
 
 def set_dense_tail_rows(n: int) -> None:
@@ -218,6 +219,9 @@ def dense_tail_level(levels, limit=None, pre=None, post=None) -> int:
             return 2
         if sm.kind == _lib.SMOOTH_CHEBYSHEV:
             return max(sm.order, 1)
+        if sm.kind == _lib.SMOOTH_SGS:        # level-scheduled half-sweeps: one
+            halves = 2 if sm.direction == 0 else 1      # barrier per schedule level
+            return _SGS_KERNEL_FACTOR * halves * max(sm.sweeps, 1)
         return max(sm.sweeps, 1)
     ka = a_kernels(pre) + a_kernels(post)   # (zero-guess first step is fused: ~ +residual)
     nL = as_csr(levels[-1][0]).nrows
@@ -252,7 +256,7 @@ def vcycle_tail_operator(levels, start: int, pre, post, inv) -> np.ndarray | Non
     exact level-scheduled kernels).
     """
     for sm in (pre, post):
-        if sm.kind not in (_lib.SMOOTH_JACOBI, _lib.SMOOTH_CHEBYSHEV):
+        if sm.kind not in (_lib.SMOOTH_JACOBI, _lib.SMOOTH_CHEBYSHEV, _lib.SMOOTH_SGS):
             return None
     mats = []
     for (A, P, R, bounds) in levels[start:]:
@@ -262,8 +266,33 @@ def vcycle_tail_operator(levels, start: int, pre, post, inv) -> np.ndarray | Non
                      as_csr(P).to_scipy() if P is not None else None,
                      as_csr(R).to_scipy() if R is not None else None, bounds))
 
+    gs_rows = {}
+
+    def gs_half(k, b, x, forward):            # _ckernels.pyx:60-79, in place on x
+        if k not in gs_rows:
+            As = mats[k][0]
+            rows = []
+            for i in range(As.shape[0]):
+                lo, hi = As.indptr[i], As.indptr[i + 1]
+                cols, vals = As.indices[lo:hi], As.data[lo:hi]
+                off = cols != i
+                rows.append((cols[off], vals[off], vals[~off][0]))
+            gs_rows[k] = rows
+        rows = gs_rows[k]
+        order = range(len(rows)) if forward else range(len(rows) - 1, -1, -1)
+        for i in order:
+            cols, vals, dii = rows[i]
+            x[i] = (b[i] - vals @ x[cols]) / dii
+
     def smooth(sm, k, b, x):                  # x None: zero guess
         As, d, _, _, bounds = mats[k]
+        if sm.kind == _lib.SMOOTH_SGS:        # blas2.sgs_sweep at one leaf (blas2.py:113-162)
+            x = np.zeros_like(b) if x is None else x
+            halves = {0: (True, False), 1: (True,), 2: (False,)}[sm.direction]
+            for _ in range(max(sm.sweeps, 1)):
+                for fwd in halves:
+                    gs_half(k, b, x, fwd)
+            return x
         if sm.kind == _lib.SMOOTH_JACOBI:     # blas2.py:165-185
             if sm.weight == 0.0:
                 return np.zeros_like(b) if x is None else x

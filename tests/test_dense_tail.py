@@ -25,7 +25,7 @@ def _cheb(order):
 
 
 @pytest.mark.parametrize("mixed", [False, True])
-@pytest.mark.parametrize("smoother", ["jacobi", "jacobi2", "cheb2", "cheb3"])
+@pytest.mark.parametrize("smoother", ["jacobi", "jacobi2", "cheb2", "cheb3", "sgs", "sgs_fwd2"])
 def test_tail_operator_matches_oracle_vcycle(mixed, smoother):
     A, _ = gen_poisson3d(18, 17, 16)
     h = setup(A, AmgParams(coarse_matrix_size=40), mixed_precision=mixed)
@@ -36,7 +36,10 @@ def test_tail_operator_matches_oracle_vcycle(mixed, smoother):
     levels = [(lv.A, lv.P, lv.R, bounds[l]) for l, lv in enumerate(h.levels)]
     inv = coarse_inverse(h.coarsest.A)
     spec = {"jacobi": (_jac(0.8), ("jacobi", 0.8, 1)), "jacobi2": (_jac(0.7, 2), ("jacobi", 0.7, 2)),
-            "cheb2": (_cheb(2), ("chebyshev", 2)), "cheb3": (_cheb(3), ("chebyshev", 3))}[smoother]
+            "cheb2": (_cheb(2), ("chebyshev", 2)), "cheb3": (_cheb(3), ("chebyshev", 3)),
+            "sgs": (_lib.mrs_smoother(_lib.SMOOTH_SGS, 1, 0.0, 0, 0), ("sgs", "symmetric", 1)),
+            "sgs_fwd2": (_lib.mrs_smoother(_lib.SMOOTH_SGS, 2, 0.0, 0, 1), ("sgs", "forward", 2)),
+            }[smoother]
     ho = osetup(O.Csr.of(A), coarse_size=40, mixed=mixed)
     for l, lv in enumerate(ho.levels):
         lv.eig_bounds = bounds[l]
@@ -66,5 +69,5 @@ def test_tail_level_choice_and_sgs():
     assert sizes[dense_tail_level(levels, 10 ** 9)] < 5000
     assert dense_tail_level(levels, 0) == -1
     assert dense_tail_level(levels, sizes[-1]) == -1      # only the coarsest fits: nothing to collapse
-    sgs = _lib.mrs_smoother(_lib.SMOOTH_SGS, 1, 0.0, 0, 0)
-    assert vcycle_tail_operator(levels, l, sgs, sgs, coarse_inverse(h.coarsest.A)) is None
+    bad = _lib.mrs_smoother(99, 1, 0.0, 0, 0)                 # unknown smoother kind
+    assert vcycle_tail_operator(levels, l, bad, bad, coarse_inverse(h.coarsest.A)) is None
