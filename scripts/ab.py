@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--config", default="c2")
     ap.add_argument("--rounds", type=int, default=3)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--grid", type=int, default=None)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -28,7 +29,7 @@ def main():
     from paper_2103_07329_b200 import _lib, gen_poisson3d
     from paper_2103_07329_b200.params import tree
     from paper_2103_07329_b200.solvers import prepare
-    bench.select(a.config)
+    bench.select(a.config, a.grid)
     A = bench.make_matrix()
     B = torch.from_numpy(np.random.default_rng(0).uniform(-1, 1, (A.nrows, bench.M))).cuda()
     X = torch.zeros_like(B)
