@@ -280,7 +280,9 @@ struct Builder {
     }
     // the collapsed sub-V-cycle (mrs_plan_set_dense_tail): entered with zero x
     static bool dense_tail(const mrs_plan& p, int l) {
-        return p.desc.precond == MRS_PC_MG && l == p.dense_from && !p.dist;
+        // distributed plans: only where the level is replicated (agglomerated)
+        return p.desc.precond == MRS_PC_MG && l == p.dense_from &&
+               (!p.dist || p.L[l].replicated);
     }
 
     // Gauss-Seidel sweep in place on x (blas2.py:113-162): forward and/or

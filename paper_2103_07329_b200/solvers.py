@@ -156,7 +156,8 @@ class DevicePlan:
                 inv = np.ascontiguousarray(inv, dtype=np.float64)
                 _lib.check(self.L.mrs_plan_set_coarse_inverse(h, inv.ctypes.data, inv.shape[0]),
                            "coarse inverse")
-            if tail is not None and tail.tail is not None and dist is None:
+            if tail is not None and tail.tail is not None and (
+                    dist is None or dist[1][tail.tail_level].replicated):
                 T = np.ascontiguousarray(tail.tail, dtype=np.float64)
                 _lib.check(self.L.mrs_plan_set_dense_tail(h, tail.tail_level, T.ctypes.data,
                                                           T.shape[0]), "dense V-cycle tail")

@@ -58,3 +58,22 @@ def test_team_of_one_matches_single_gpu(name, force, monkeypatch):
     np.testing.assert_array_equal(Xd.data, Xs.data)
     np.testing.assert_array_equal(sd.final_rel_residual, ss.final_rel_residual)
     team.close()
+
+
+@pytest.mark.parametrize("name", ["amg_pcg", "amg_pbicgstab", "amg_bicgstab_mixed"])
+def test_team_of_one_dense_tail_on_replicated_levels(name):
+    """The collapsed V-cycle tail also runs in distributed plans when its level
+    is replicated (agglomerated): a 1-rank team replicating from level 1 gives
+    the single-GPU bits."""
+    A, _ = gen_poisson3d(14, 13, 12)
+    B = np.random.default_rng(4).uniform(-1, 1, (A.nrows, 4))
+    roles = CASES[name]
+    Xs = BlockVector.zeros(A.nrows, 4)
+    ss = prepare(tree(roles), A).run(BlockVector.from_array(B), Xs)
+    team = GpuTeam(agg_rows_per_rank=1, force_replicate_from=1)
+    cs = prepare(tree(roles), A, team=team)
+    Xd = BlockVector.zeros(A.nrows, 4)
+    sd = cs.run(BlockVector.from_array(B), Xd)
+    assert sd.iterations == ss.iterations and sd.all_converged
+    np.testing.assert_array_equal(Xd.data, Xs.data)
+    team.close()
