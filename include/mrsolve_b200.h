@@ -133,11 +133,20 @@ int mrs_gs_sweep(const mrs_csr* A, const int64_t* diag_pos, const double* b,
 #define MRS_METHOD_BICGSTAB  1   /* classical van der Vorst, solvers.py:219-293 */
 #define MRS_METHOD_RBICGSTAB 2   /* reordered, two reduction groups, solvers.py:296-364 */
 #define MRS_METHOD_PBICGSTAB 3   /* pipelined (op = A M, drift check), solvers.py:367-479 */
+#define MRS_METHOD_STATIONARY 4  /* repeat one step of `precond` on X until the true residual
+                                    meets rel_tol: MultiGrid (one V-cycle, multigrid_solve,
+                                    solvers.py:683-710), Jacobi (one sweep, weight pc_weight) or
+                                    Gauss-Seidel (one sweep, pc_direction) (_stationary_solve,
+                                    solvers.py:962-978) */
+#define MRS_METHOD_DIRECT    5   /* X = A^-1 B with the dense inverse given as the "coarse
+                                    inverse" (n x n), precond NONE (direct_solve, :588-604) */
 
 #define MRS_PC_NONE     0
 #define MRS_PC_JACOBI   1        /* _SweepPrecond(jacobi), solvers.py:716-726,782-788 */
 #define MRS_PC_MG       2        /* MultiGrid V-cycle, solvers.py:615-675 */
 #define MRS_PC_SGS      3        /* _SweepPrecond(sgs_sweep), solvers.py:792-797 */
+#define MRS_PC_CHEB     4        /* _SweepPrecond(chebyshev_apply), solvers.py:796-802: order in
+                                    desc.pre.order, bounds = level 0 lmin/lmax */
 
 #define MRS_SMOOTH_JACOBI     0  /* blas2.jacobi_sweep, blas2.py:165-185 */
 #define MRS_SMOOTH_CHEBYSHEV  1  /* solvers.chebyshev_apply, solvers.py:520-571 */

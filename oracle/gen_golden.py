@@ -169,6 +169,31 @@ SOLVE_CASES = {
     "sgs_precond_cg": ((10, 10, 10), 2, 11, {
         "solver": {"method": "CG", "rel_tolerance": "1e-9"},
         "preconditioner": {"method": "Gauss-Seidel"}}),
+    # the other solver families of prepare (solvers.py:891-953) and the
+    # Chebyshev preconditioner (:796-802)
+    "mg_solver_jacobi": ((12, 12, 12), 2, 12, {
+        "solver": {"method": "MultiGrid", "rel_tolerance": "1e-8", "max_iters": "60"},
+        "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+        "post_smoother": {"method": "Jacobi", "weight": "0.8"}}),
+    "mg_solver_default_sgs": ((10, 10, 10), 2, 13, {
+        "solver": {"method": "MultiGrid", "rel_tolerance": "1e-8", "max_iters": "40",
+                   "mg_coarse_matrix_size": "100"}}),
+    "jacobi_solver": ((6, 6, 6), 2, 14, {
+        "solver": {"method": "Jacobi", "rel_tolerance": "1e-4", "max_iters": "400",
+                   "weight": "0.9"}}),
+    "gs_solver": ((8, 8, 8), 3, 15, {
+        "solver": {"method": "Gauss-Seidel", "rel_tolerance": "1e-6", "max_iters": "300"}}),
+    "gs_solver_forward": ((6, 6, 6), 2, 16, {
+        "solver": {"method": "Gauss-Seidel", "rel_tolerance": "1e-6", "max_iters": "300",
+                   "direction": "forward"}}),
+    "direct": ((6, 6, 6), 3, 17, {
+        "solver": {"method": "Direct"}}),
+    "cheb_precond_cg": ((12, 12, 12), 2, 18, {
+        "solver": {"method": "CG", "rel_tolerance": "1e-9"},
+        "preconditioner": {"method": "Chebyshev", "polynomial_order": "3"}}),
+    "cheb_precond_bicgstab": ((10, 10, 10), 2, 19, {
+        "solver": {"method": "BiCGStab", "rel_tolerance": "1e-9"},
+        "preconditioner": {"method": "Chebyshev", "polynomial_order": "2"}}),
 }
 
 

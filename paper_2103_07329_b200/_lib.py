@@ -20,7 +20,8 @@ MRS_ERR_BREAKDOWN, MRS_ERR_SINGULAR, MRS_ERR_DEGENERATE, MRS_ERR_STATE = 5, 6, 7
 MRS_ERR_INSTABILITY = 9
 
 METHOD_CG, METHOD_BICGSTAB, METHOD_RBICGSTAB, METHOD_PBICGSTAB = 0, 1, 2, 3
-PC_NONE, PC_JACOBI, PC_MG, PC_SGS = 0, 1, 2, 3
+METHOD_STATIONARY, METHOD_DIRECT = 4, 5
+PC_NONE, PC_JACOBI, PC_MG, PC_SGS, PC_CHEB = 0, 1, 2, 3, 4
 SMOOTH_JACOBI, SMOOTH_CHEBYSHEV, SMOOTH_SGS = 0, 1, 2
 SGS_DIRECTIONS = {"symmetric": 0, "forward": 1, "backward": 2}
 

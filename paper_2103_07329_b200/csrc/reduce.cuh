@@ -71,6 +71,7 @@ enum Epilogue : int {
     EPI_PBICG_RHO,     // out = (r0.r, r0.w, r0.s, r0.z, r.r) -> rnorm, history, beta,
                        //   alpha, rho, stop, drift-check flag
     EPI_PBICG_DRIFT,   // out = chk.chk       -> instability check
+    EPI_STAT_RNORM,    // out = r.r (true residual) -> it++, rnorm, history, stop
 };
 constexpr int kMaxK = 5;   // reduced values per column of one reduction
 
@@ -146,8 +147,13 @@ static __device__ void run_epilogue(int epi, SolveState* st, const double* v, in
         }
         if (threadIdx.x == 0) st->it += 1;
         break;
+    case EPI_STAT_RNORM:
     case EPI_CG_RNORM: {
         bool conv = true;
+        if (epi == EPI_STAT_RNORM) {
+            if (threadIdx.x == 0) st->it += 1;
+            __syncthreads();
+        }
         if (act) {
             double rn = sqrt(v[c]);
             st->rnorm[c] = rn;

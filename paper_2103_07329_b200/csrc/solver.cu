@@ -364,7 +364,7 @@ struct Builder {
     static mrs_smoother pc_smoother(const mrs_plan_desc& d) {
         if (d.precond == MRS_PC_JACOBI) return mrs_smoother{MRS_SMOOTH_JACOBI, d.pc_sweeps, d.pc_weight, 0, 0};
         if (d.precond == MRS_PC_SGS) return mrs_smoother{MRS_SMOOTH_SGS, d.pc_sweeps, 0.0, 0, d.pc_direction};
-        return d.pre;
+        return d.pre;   // MultiGrid pre-smoother; Chebyshev preconditioner (pre.order)
     }
 
     // Smoother on a NONZERO x (post-smoothing; pre-smoothing of later cycles).
@@ -533,7 +533,8 @@ PCPlan plan_precond(mrs_plan* P, const int* guard, const double* r, double* want
         if (d.precond == MRS_PC_NONE) {
             pc.out = const_cast<double*>(r);
             if (dot_epi >= 0) bd.dot(r, r, P->n, dot_epi);
-        } else if (d.precond == MRS_PC_JACOBI || d.precond == MRS_PC_SGS) {
+        } else if (d.precond == MRS_PC_JACOBI || d.precond == MRS_PC_SGS ||
+                   d.precond == MRS_PC_CHEB) {
             LevelDev& lv = P->L[0];
             pc.seed = bd.level_seed(0, x);
             if (!producer_seeds) bd.seed_kernel(r, P->n, pc.seed);
@@ -827,8 +828,75 @@ void build_pbicgstab(mrs_plan* P, bool x_zero, Program& pg) {
     }
 }
 
+// _stationary_solve / multigrid_solve (solvers.py:962-978, :683-710): one
+// step of the configured sweep (or one V-cycle) on X per iteration, then the
+// TRUE residual and its norm decide convergence; the final relative residual
+// is that last norm (recomputed by the epilogue from the same X).
+void build_stationary(mrs_plan* P, bool x_zero, Program& pg) {
+    const int64_t n = P->n;
+    const DevCsr& A = P->L[0].A;
+    const mrs_plan_desc& d = P->desc;
+    {
+        Builder b{P, &pg.pro, nullptr};
+        b.dot(P->B, P->B, n, EPI_BSCALE);
+        if (x_zero) b.copy(P->B, P->r, n);
+        else b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_RNORM_INIT);
+    }
+    {
+        Builder b{P, &pg.body, nullptr};
+        LevelDev& lv = P->L[0];
+        // the step runs on a NONZERO x: on the zero first guess this is the
+        // reference's zero-flag short-cut value (0 + w*(b/d) == w*(b/d), ...)
+        XB x{P->X, P->zt};
+        if (d.precond == MRS_PC_SGS) {
+            b.sgs_sweep(lv, P->B, P->X, d.pc_direction);
+        } else if (d.precond == MRS_PC_JACOBI) {
+            if (d.pc_weight != 0.0) b.jacobi_sweep(lv, P->B, d.pc_weight, x, -1);
+        } else {
+            b.vcycle(0, P->B, false, false, x, -1);
+        }
+        if (x.cur != P->X) b.copy(x.cur, P->X, n);
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_STAT_RNORM);
+        pg.body_bytes = b.bytes;
+        pg.body_kernels = b.kernels;
+    }
+    {
+        Builder b{P, &pg.epi, nullptr};
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_FINAL);
+    }
+}
+
+// direct_solve (solvers.py:588-604): X = A^-1 B with the uploaded dense
+// inverse, then the relative residual; no iterations (max_iters 0).
+void build_direct(mrs_plan* P, bool, Program& pg) {
+    const int64_t n = P->n;
+    const DevCsr& A = P->L[0].A;
+    {
+        Builder b{P, &pg.pro, nullptr};
+        b.dot(P->B, P->B, n, EPI_BSCALE);
+        b.dot(P->B, P->B, n, EPI_RNORM_INIT);     // stop = 1 (max_iters 0)
+        const double* inv = P->inv;
+        const double* B = P->B;
+        double* X = P->X;
+        const int64_t m = P->m;
+        pg.pro.push_back([=](cudaStream_t s) { return launch_dense(inv, n, B, X, m, nullptr, s); });
+        b.bytes += (double)n * n * 8.0 + 2 * b.V(n);
+        b.kernels++;
+    }
+    {
+        Builder b{P, &pg.epi, nullptr};
+        b.spmv(A, P->X, P->r, MRS_MODE_RSUB, P->B);
+        b.dot(P->r, P->r, n, EPI_FINAL);
+    }
+}
+
 void build_program(mrs_plan* P, bool x_zero, Program& pg) {
     switch (P->desc.method) {
+    case MRS_METHOD_STATIONARY: build_stationary(P, x_zero, pg); break;
+    case MRS_METHOD_DIRECT: build_direct(P, x_zero, pg); break;
     case MRS_METHOD_CG: build_cg(P, x_zero, pg); break;
     case MRS_METHOD_BICGSTAB: build_bicgstab(P, x_zero, pg); break;
     case MRS_METHOD_RBICGSTAB: build_rbicgstab(P, x_zero, pg); break;
@@ -885,20 +953,25 @@ int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s) {
         MRS_CUDA_OK(cudaGraphNodeGetDependentNodes(nd, nullptr, &ndep));
         if (ndep == 0) sinks.push_back(nd);
     }
-    // 2) WHILE node with the iteration body
-    cudaGraphNodeParams cp = {};
-    cp.type = cudaGraphNodeTypeConditional;
-    cp.conditional.handle = h;
-    cp.conditional.type = cudaGraphCondTypeWhile;
-    cp.conditional.size = 1;
-    cudaGraphNode_t wnode;
-    MRS_CUDA_OK(cudaGraphAddNode(&wnode, g, sinks.data(), sinks.size(), &cp));
-    cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
-    MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-    if (run_list(pg.body, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
-    MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
+    // 2) WHILE node with the iteration body (none for a loop-free program)
+    std::vector<cudaGraphNode_t> after = sinks;
+    if (!pg.body.empty()) {
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        MRS_CUDA_OK(cudaGraphAddNode(&wnode, g, sinks.data(), sinks.size(), &cp));
+        cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+        MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        if (run_list(pg.body, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
+        MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
+        after.assign(1, wnode);
+    }
     // 3) epilogue after the loop
-    MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
+    MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, g, after.data(), nullptr, after.size(),
+                                              cudaStreamCaptureModeRelaxed));
     if (run_list(pg.epi, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
     MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
     cudaStreamDestroy(cs);
@@ -1031,8 +1104,13 @@ extern "C" {
 int mrs_plan_create(const mrs_plan_desc* desc, mrs_plan** out) {
     if (!desc || !out) return MRS_ERR_ARG;
     if (desc->m < 1 || desc->m > kMaxM || desc->nrows < 1) return MRS_ERR_ARG;
-    if (desc->method < MRS_METHOD_CG || desc->method > MRS_METHOD_PBICGSTAB) return MRS_ERR_UNSUPPORTED;
-    if (desc->precond < MRS_PC_NONE || desc->precond > MRS_PC_SGS) return MRS_ERR_UNSUPPORTED;
+    if (desc->method < MRS_METHOD_CG || desc->method > MRS_METHOD_DIRECT) return MRS_ERR_UNSUPPORTED;
+    if (desc->precond < MRS_PC_NONE || desc->precond > MRS_PC_CHEB) return MRS_ERR_UNSUPPORTED;
+    if (desc->method == MRS_METHOD_STATIONARY &&
+        !(desc->precond == MRS_PC_JACOBI || desc->precond == MRS_PC_SGS || desc->precond == MRS_PC_MG))
+        return MRS_ERR_UNSUPPORTED;
+    if (desc->method == MRS_METHOD_DIRECT && desc->precond != MRS_PC_NONE) return MRS_ERR_UNSUPPORTED;
+    if (desc->precond == MRS_PC_CHEB && desc->pre.order < 1) return MRS_ERR_ARG;
     for (const mrs_smoother* sm : {&desc->pre, &desc->post})
         if (desc->precond == MRS_PC_MG &&
             (sm->kind < MRS_SMOOTH_JACOBI || sm->kind > MRS_SMOOTH_SGS ||
@@ -1160,7 +1238,17 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
         }
     } else if (p->desc.precond == MRS_PC_JACOBI || p->desc.precond == MRS_PC_SGS) {
         if (!p->L[0].d) return MRS_ERR_STATE;
+    } else if (p->desc.precond == MRS_PC_CHEB) {
+        LevelDev& lv = p->L[0];
+        if (!lv.d) return MRS_ERR_STATE;
+        if (!(lv.lmin > 0.0 && lv.lmin < lv.lmax)) return MRS_ERR_ARG;
+        const int64_t nl = lv.vrows;
+        lv.r = dalloc<double>(nl * m, o);
+        lv.dva = dalloc<double>(nl * m, o);
+        lv.dvb = dalloc<double>(nl * m, o);
+        if (!lv.r || !lv.dva || !lv.dvb) return MRS_ERR_ALLOC;
     }
+    if (p->desc.method == MRS_METHOD_DIRECT && (!p->inv || p->nc != n)) return MRS_ERR_STATE;
     for (const LevelDev& lv : p->L)
         if (lv.sgs && p->dist) return MRS_ERR_UNSUPPORTED;   // one-leaf sweep order only
     size_t V = (size_t)p->L[0].vrows * m;   // level-0 Krylov vectors carry the A0 halo

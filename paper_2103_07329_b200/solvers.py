@@ -227,6 +227,8 @@ class DevicePlan:
         it = int(st.iterations)
         history = [hist[i * m:(i + 1) * m].copy() for i in range(it + 1)]
         tol = float(self.desc.rel_tol)
+        if int(self.desc.method) == _lib.METHOD_DIRECT:   # solvers.py:598-604
+            return SolveStats(1, rel <= 1e-8, rel, [rel.copy()], self.method, float(st.device_ms))
         return SolveStats(it, rel <= tol, rel, history, self.method, float(st.device_ms))
 
 
@@ -298,21 +300,32 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
     sp = config.role("solver")
     method = sp.method
     family = METHOD_FAMILIES[method]
-    if family not in ("CG", "BiCGStab"):
-        raise ConfigurationError(
-            f"solver {method!r} is not on the device solve path (CG and the three BiCGStab "
-            "formulations are; see SURVEY.md 8(f))")
-    tol = sp.get_float("rel_tolerance")
-    iters = sp.get_int("max_iters")
+    if family not in ("CG", "BiCGStab", "MultiGrid", "Jacobi", "Gauss-Seidel", "Direct"):
+        raise ConfigurationError(f"method {method!r} cannot act as a solver")   # solvers.py:953
+    if family == "Direct":            # no iteration keys (direct_solve tests rel <= 1e-8)
+        tol, iters = 1e-8, 0
+    else:
+        tol = sp.get_float("rel_tolerance")
+        iters = sp.get_int("max_iters")
     merged = bool(sp.get_int("merged")) if family == "BiCGStab" else False
-    # SolveStats.method as the reference names it (solvers.py:292, :363, :478)
-    name = "CG" if family == "CG" else (method + ("/merged" if merged else ""))
+    # SolveStats.method as the reference names it (solvers.py:292, :363, :478;
+    # the stationary and direct families report the configured method)
+    name = ("CG" if family == "CG" else
+            method + ("/merged" if merged else "") if family == "BiCGStab" else method)
 
     pl = config.role("preconditioner")
+    if family == "MultiGrid":
+        if pl is not None:                       # solvers.py:904-905
+            raise ConfigurationError("MultiGrid solver takes no preconditioner")
+        pl = sp                                  # the solver role carries the mg_* keys
+    elif family in ("Jacobi", "Gauss-Seidel", "Direct"):
+        pl = None                                # built but unused by the reference
     desc = _lib.mrs_plan_desc()
     desc.method = {"CG": _lib.METHOD_CG, "BiCGStab": _lib.METHOD_BICGSTAB,
-                   "RBiCGStab": _lib.METHOD_RBICGSTAB,
-                   "PBiCGStab": _lib.METHOD_PBICGSTAB}[method if family == "BiCGStab" else "CG"]
+                   "RBiCGStab": _lib.METHOD_RBICGSTAB, "PBiCGStab": _lib.METHOD_PBICGSTAB,
+                   "MultiGrid": _lib.METHOD_STATIONARY, "Jacobi": _lib.METHOD_STATIONARY,
+                   "Gauss-Seidel": _lib.METHOD_STATIONARY,
+                   "Direct": _lib.METHOD_DIRECT}[method if family == "BiCGStab" else family]
     desc.drift_limit = DRIFT_LIMIT
     desc.nrows = Ab.nrows
     desc.rel_tol = tol
@@ -322,9 +335,35 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
     desc.mg_cycles = 1
     desc.nlevels = 1
     levels, inv, h = None, None, None
-    if pl is None:
+    if family == "Direct":                       # direct_solve (solvers.py:588-604)
+        desc.precond = _lib.PC_NONE
+        desc.max_iters = 0
+        levels = [(Ab, None, None, None)]
+        inv = coarse_inverse(Ab)
+    elif family == "Jacobi":                     # _stationary_solve with one sweep per step
+        desc.precond = _lib.PC_JACOBI
+        desc.pc_weight = sp.get_float("weight")
+        desc.pc_sweeps = 1
+        levels = [(Ab, None, None, None)]
+    elif family == "Gauss-Seidel":
+        desc.precond = _lib.PC_SGS
+        desc.pc_sweeps = 1
+        desc.pc_direction = _sgs_direction(sp)
+        levels = [(Ab, None, None, None)]
+    elif pl is None:
         desc.precond = _lib.PC_NONE
         levels = [(Ab, None, None, None)]
+    elif pl.method == "Chebyshev":               # _SweepPrecond(chebyshev_apply), :796-802
+        desc.precond = _lib.PC_CHEB
+        order = pl.get_int("polynomial_order")
+        if order < 1:
+            raise InvalidArgumentError("polynomial_order must be >= 1")
+        desc.pre = _lib.mrs_smoother(_lib.SMOOTH_CHEBYSHEV, 1, 0.0, order, 0)
+        bounds = tuple(eig_bounds[0]) if eig_bounds is not None else estimate_eig_bounds(Ab)
+        if not (0.0 < bounds[0] < bounds[1]):
+            raise InvalidArgumentError(
+                f"eigenvalue bounds must satisfy 0 < lmin < lmax, got {bounds}")
+        levels = [(Ab, None, None, bounds)]
     elif pl.method == "Jacobi":
         desc.precond = _lib.PC_JACOBI
         desc.pc_weight = pl.get_float("weight")
@@ -339,7 +378,8 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
         if pl.get_str("mg_cycle") != "V":
             raise ConfigurationError("only the V cycle is implemented")
         desc.precond = _lib.PC_MG
-        desc.mg_cycles = max(pl.get_int("max_iters"), 1)
+        # preconditioner: max_iters V-cycles per application; solver: one per step
+        desc.mg_cycles = 1 if family == "MultiGrid" else max(pl.get_int("max_iters"), 1)
         desc.pre = _smoother(config.role("pre_smoother"))
         desc.post = _smoother(config.role("post_smoother"))
         if hierarchy is None:

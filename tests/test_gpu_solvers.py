@@ -167,10 +167,17 @@ def test_device_tensor_run_matches_host_run():
 
 def test_unsupported_configs_raise():
     A, _ = gen_poisson3d(4, 4, 4)
+    # a Krylov solver as preconditioner / smoother is not on the device path
     with pytest.raises(ConfigurationError):
-        prepare(tree({"solver": {"method": "Direct"}}), A)
+        prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "BiCGStab"}}), A)
     with pytest.raises(ConfigurationError):
-        prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "Chebyshev"}}), A)
+        prepare(tree({"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"},
+                      "pre_smoother": {"method": "BiCGStab"}}), A)
+    # as in the reference (solvers.py:904-905, :953)
+    with pytest.raises(ConfigurationError):
+        prepare(tree({"solver": {"method": "MultiGrid"}, "preconditioner": {"method": "Jacobi"}}), A)
+    with pytest.raises(ConfigurationError):
+        prepare(tree({"solver": {"method": "Chebyshev"}}), A)
 
 
 @pytest.mark.parametrize("mode", ["graph", "eager"])

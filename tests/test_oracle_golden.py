@@ -104,10 +104,37 @@ def _solve_case(name, g):
                 return ("jacobi", float(d.get("weight", 1.0)), int(d.get("max_iters", 1)))
             return ("chebyshev", int(d.get("polynomial_order", 2)))
         precond = O.MultiGrid(h, spec("pre_smoother"), spec("post_smoother"))
+    elif pre and pre["method"] == "Chebyshev":
+        precond = O.ChebPrecond(A, int(pre.get("polynomial_order", 2)))
+    method = sp_["method"]
+    iters = int(sp_.get("max_iters", 100))
+    if method == "Direct":
+        return O.direct_solve(A, B, X), X
+    if method in ("MultiGrid", "Jacobi", "Gauss-Seidel"):
+        if method == "MultiGrid":
+            h = setup(A, coarse_size=int(sp_.get("mg_coarse_matrix_size", 500)))
+            step = O.mg_step(O.MultiGrid(h, _spec(roles, "pre_smoother"),
+                                         _spec(roles, "post_smoother")))
+        elif method == "Jacobi":
+            step = O.jacobi_step(A, float(sp_.get("weight", 1.0)))
+        else:
+            step = O.sgs_step(A, sp_.get("direction", "symmetric"))
+        return O.stationary_solve(A, B, X, step, tol, iters), X
     drv = {"CG": O.cg_solve, "BiCGStab": O.bicgstab_solve, "RBiCGStab": O.rbicgstab_solve,
-           "PBiCGStab": O.pbicgstab_solve}[sp_["method"]]
-    st = drv(A, B, X, precond, tol, int(sp_.get("max_iters", 100)))
+           "PBiCGStab": O.pbicgstab_solve}[method]
+    st = drv(A, B, X, precond, tol, iters)
     return st, X
+
+
+def _spec(roles, r):
+    d = roles.get(r)
+    if d is None:                     # reference default: symmetric hybrid GS
+        return ("sgs", "symmetric", 1)
+    if d["method"] == "Gauss-Seidel":
+        return ("sgs", d.get("direction", "symmetric"), int(d.get("max_iters", 1)))
+    if d["method"] == "Jacobi":
+        return ("jacobi", float(d.get("weight", 1.0)), int(d.get("max_iters", 1)))
+    return ("chebyshev", int(d.get("polynomial_order", 2)))
 
 
 def _cases():
