@@ -599,13 +599,20 @@ def main():
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
-        res, errs = run_reference_cpu(steps=1, warmup=0, timeout=600)
+        try:
+            usable = len(os.sched_getaffinity(0))
+        except Exception:
+            usable = os.cpu_count() or 1
+        res, errs = run_reference_cpu(steps=1, warmup=1, timeout=600, nproc=min(M, usable))
         if res is not None:
             r = res["runs"][0]
-            cpu = {"value": r[1] / r[0], "unit": UNIT, "cores": 1, "kind": "reference",
-                   "sample": f"1 full C2 solve ({r[2]} iterations, {r[0]:.2f} s) after a "
-                             f"{res['setup']:.1f} s reference setup; 1 of {os.cpu_count()} "
-                             f"host cores, mrsolve {res['backend']} kernels"}
+            P = res["nproc"]
+            cpu = {"value": r[1] / r[0], "unit": UNIT, "cores": P, "kind": "reference",
+                   "sample": f"1 full {args.config.upper()} solve ({r[2]} iterations, {r[0]:.2f} s) "
+                             f"after a warm-up solve and a {res['setup']:.1f} s reference setup; "
+                             f"the m={M} columns over {P} concurrent single-core processes "
+                             f"({P} of {os.cpu_count()} host cores), mrsolve {res['backend']} "
+                             f"kernels (see --impl reference for the 1-process comparison)"}
         else:
             cpu = {"value": None, "unit": UNIT, "cores": 1, "kind": "reference",
                    "sample": f"unavailable: {errs}"}
