@@ -17,11 +17,12 @@ int64_t spmm_coop();            // cooperative entry loads for long-row operator
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
 template <typename... KArgs, typename... Args>
-inline cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, Args... args) {
+inline cudaError_t launch_ex_smem(void (*kern)(KArgs...), int grid, size_t smem, cudaStream_t s,
+                                  Args... args) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -29,6 +30,11 @@ inline cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, A
     cfg.attrs = attr;
     cfg.numAttrs = pdl_enabled() ? 1 : 0;
     return cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_ex(void (*kern)(KArgs...), int grid, cudaStream_t s, Args... args) {
+    return launch_ex_smem(kern, grid, 0, s, args...);
 }
 
 // Resident CTAs per SM of a kernel (cached per function).
@@ -85,7 +91,8 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         a.chunk = rpp * sp;
         if (generic) a.n_long = 0;                               // lane path only
         a.long_ctas = a.n_long ? (int)std::min<int64_t>(a.n_long, 4LL * num_sms()) : 0;
-        (void)launch_ex(kern, g + a.long_ctas, s, a);
+        (void)launch_ex_smem(kern, g + a.long_ctas,
+                             a.long_ctas ? kLongProducts * sizeof(double) : 0, s, a);
     };
     // small operators with long rows: the LONG variant (16 entries in flight)
     if (!generic && m <= 16 && a.nrows <= spmm_long_max_rows() && a.nnz_hint >= 12 * a.nrows) {

@@ -321,7 +321,9 @@ __device__ __forceinline__ void long_row_cta(const SpArgs& a, const GSrc<Tv, Ti>
                                              double (&dotp)[Lay<M>::CPL]) {
     constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR;
     constexpr int EPC = kLongProducts / M;          // entries per chunk
-    __shared__ double s_p[kLongProducts];
+    // dynamic shared memory: launches without long rows reserve none, so the
+    // lane path keeps its whole L1 for the gathered x rows
+    extern __shared__ double s_p[];
     const int q = threadIdx.x;
     const GSrc<Tv, Ti> src = src0.at_row(a, row);
     const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
