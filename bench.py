@@ -339,6 +339,36 @@ def reference_arm(args, rank):
 # B200 arm
 # ---------------------------------------------------------------------------
 
+def roofline_at_scale(torch, K, peak, grid=128):
+    from paper_2103_07329_b200 import gen_poisson3d
+    A = gen_poisson3d(grid, grid, grid)[0]
+    D = K.DeviceCsr.from_block(A, slab=True)
+    n = A.nrows
+    x = torch.rand(n, M, dtype=torch.float64, device="cuda")
+    b = torch.rand(n, M, dtype=torch.float64, device="cuda")
+    y = torch.empty_like(b)
+    for _ in range(3):
+        K.csr_spmv(D, None, None, x, y, K.MODE_RSUB, b)
+    reps, ts = 20, []
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _r in range(reps):
+            K.csr_spmv(D, None, None, x, y, K.MODE_RSUB, b)
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1) * 1e-3 / reps)
+    t = sorted(ts)[1]
+    nslab = 0 if D.slab_base is None else D.slab_base.numel()
+    byts = (A.nnz * (A.values.itemsize + D.col_idx.element_size()) + (n + 1) * 4 + 4 * nslab
+            + 3 * n * M * 8)
+    return {"kernel": f"spmm_kernel<{M}, OP_SPMV(RSUB), double, uint16(slab)> on the "
+                      f"{grid}^3 7-pt operator", "algorithmic_bytes": byts,
+            "us_per_launch": t * 1e6, "achieved": byts / t / 1e9, "frac": byts / t / 1e9 / peak,
+            "timing": "back-to-back launches (each streams the operands from HBM: "
+                      f"{byts / 1e6:.0f} MB >> L2), median of 3 rounds of {reps}"}
+
+
 def spmm_sweep(torch, K, quick: bool):
     """Config 5: blocked SpMM GB/s against the HBM roofline (ASSIGN mode)."""
     from paper_2103_07329_b200.io import gen_random_sdd
@@ -596,6 +626,14 @@ def main():
     sweep = None
     if not args.no_spmm and rank == 0:
         sweep = spmm_sweep(torch, K, args.quick)
+        # the same kernel (fine-level RSUB SpMM of the 7-pt family, m = M, slab
+        # indices) where HBM is the binding bound: the 128^3 operator (C3's grid;
+        # ~0.5-1 GB per launch >> L2, so back-to-back launches read cold operands)
+        if args.config == "c2":
+            try:
+                roof["at_scale"] = roofline_at_scale(torch, K, peak)
+            except Exception as e:       # informational only
+                roof["at_scale"] = {"error": f"{type(e).__name__}: {e}"[:200]}
 
     cpu = None
     if not args.no_cpu and rank == 0 and world == 1:
