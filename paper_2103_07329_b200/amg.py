@@ -184,7 +184,8 @@ DENSE_TAIL_ROWS = int(os.environ.get("MRS_DENSE_TAIL_ROWS", "8000"))
 # cost model of the choice (microseconds; B200 measurements, profiles/r01_ab_experiments.txt):
 # a solve-path kernel costs ~_T_LAUNCH plus _T_ROUND per dependent load round of its
 # longest row (16 entries in flight); the dense product streams n^2*8 bytes at _DENSE_BW
-_T_LAUNCH, _T_ROUND, _DENSE_BW = 3.0, 1.0, 1.4e6     # us, us, bytes/us
+_T_LAUNCH, _T_ROUND = 3.0, 1.0                           # us, us
+_DENSE_BW = float(os.environ.get("MRS_DENSE_BW", "3e6"))     # bytes/us (DMMA kernel)
 _SGS_KERNEL_FACTOR = 10     # a Gauss-Seidel half-sweep ~ 10 SpMM launches (schedule barriers)
 
 

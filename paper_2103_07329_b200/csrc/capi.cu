@@ -91,6 +91,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_split")) { set_spmm_long_split(value); return MRS_OK; }
     if (!strcmp(key, "spmm_coop")) { set_spmm_coop(value); return MRS_OK; }
+    if (!strcmp(key, "dense_mma")) { set_dense_mma(value); return MRS_OK; }
     return MRS_ERR_ARG;
 }
 

@@ -55,6 +55,8 @@ void set_spmm_long_rows(int64_t v);
 void set_spmm_chunk_rows(int64_t v);
 void set_spmm_long_split(int64_t v);
 void set_spmm_coop(int64_t v);
+bool dense_mma_enabled();
+void set_dense_mma(int64_t v);
 int64_t spmm_long_split();
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;

@@ -33,6 +33,9 @@ void set_spmm_chunk_rows(int64_t v) { g_chunk_rows = v < 1 ? 1 : v; }
 static int64_t g_long_split = 1;      // long rows by whole CTAs (0: lane path only)
 int64_t spmm_long_split() { return g_long_split; }
 void set_spmm_long_split(int64_t v) { g_long_split = v ? 1 : 0; }
+static int64_t g_dense_mma = 1;       // FP64 tensor-core dense tail (dense_mma_kernel)
+bool dense_mma_enabled() { return g_dense_mma != 0; }
+void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }
 static int64_t g_coop = 0;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v ? 1 : 0; }
@@ -227,9 +230,78 @@ __global__ void __launch_bounds__(kThreads) dense_kernel(const double* __restric
 cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
                           int64_t m, const int* guard, cudaStream_t s);
 
+// x = T b on the FP64 tensor cores (mma.sync m8n8k4 f64), m = 8 * NT columns.
+// A CTA owns 8 rows of T; its 8 warps split k and each accumulates the 8 x 8
+// (x NT) output block over its k range with DMMA (A fragment = T[8 rows][4 k],
+// B fragment = b[4 k][8 columns]); the 8 partial blocks are folded in warp
+// order through shared memory.  T is streamed once; b (n x m) is re-read once
+// per 8 rows from L2.  Products are fused multiply-adds (dense tail only: the
+// reference-order SpMM kernels never use this).
+template <int NT>
+__global__ void __launch_bounds__(kThreads) dense_mma_kernel(const double* __restrict__ T, int64_t n,
+                                                             const double* __restrict__ b,
+                                                             double* __restrict__ x,
+                                                             const int* guard) {
+    pdl_enter();
+    if (guard && *guard) return;
+    constexpr int M = 8 * NT;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int64_t row0 = (int64_t)blockIdx.x * 8;
+    const int64_t arow = min(row0 + g, n - 1);
+    const double* Ta = T + arow * n;
+    // k range of this warp: multiples of 4
+    const int64_t nk4 = (n + 3) / 4;
+    const int64_t per = (nk4 + 7) / 8;
+    const int64_t k0 = (int64_t)warp * per * 4, k1 = min(k0 + per * 4, n);
+    double c[NT][2];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
+    constexpr int U = 4;   // k-steps in flight
+    for (int64_t k = k0; k < k1; k += 4 * U) {
+        double av[U], bv[U][NT];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t kk = k + 4 * u + t4;
+            const bool ok = kk < k1;
+            av[u] = ok ? __ldg(Ta + kk) : 0.0;
+#pragma unroll
+            for (int j = 0; j < NT; ++j) bv[u][j] = ok ? __ldg(b + kk * M + 8 * j + g) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+            for (int j = 0; j < NT; ++j)
+                asm volatile(
+                    "mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+                    : "+d"(c[j][0]), "+d"(c[j][1])
+                    : "d"(av[u]), "d"(bv[u][j]));
+    }
+    __shared__ double s_c[kThreads / 32][8 * M];
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+        s_c[warp][g * M + 8 * j + 2 * t4] = c[j][0];
+        s_c[warp][g * M + 8 * j + 2 * t4 + 1] = c[j][1];
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < 8 * M; e += kThreads) {
+        const int r = e / M;
+        if (row0 + r >= n) continue;
+        double acc = s_c[0][e];
+        for (int w = 1; w < kThreads / 32; ++w) acc = add(acc, s_c[w][e]);
+        x[(row0 + r) * M + (e % M)] = acc;
+    }
+}
+
 cudaError_t launch_dense(const double* T, int64_t n, const double* b, double* x, int64_t m,
                          const int* guard, cudaStream_t s) {
     constexpr int W = kThreads / 32;
+    if (n > 1024 && dense_mma_enabled() && (m == 8 || m == 16)) {
+        const int g = (int)((n + 7) / 8);
+        if (m == 8) (void)launch_ex(dense_mma_kernel<1>, g, s, T, n, b, x, guard);
+        else (void)launch_ex(dense_mma_kernel<2>, g, s, T, n, b, x, guard);
+        return cudaGetLastError();
+    }
     // small operators: one row per CTA (more CTAs in flight than warp-rows)
     if (n <= 1024) return launch_coarse(T, n, b, x, m, guard, s);
     // rows per warp: the most (<= 32 / M partial sums per lane) that still

@@ -43,6 +43,9 @@ def main():
             if a.knob == "dense_tail_rows":        # setup-phase (Python) knob
                 from paper_2103_07329_b200 import amg
                 amg.set_dense_tail_rows(v)
+            elif a.knob == "dense_bw":              # cost-model bandwidth (GB/s)
+                from paper_2103_07329_b200 import amg
+                amg._DENSE_BW = float(v) * 1e3
             else:
                 _lib.set_option(a.knob, v)
             cs = prepare(tree(bench.ROLES), A, hierarchy=h)

@@ -420,3 +420,22 @@ def test_long_row_ctas_bitwise(roles, m):
         _lib.set_option("spmm_long_split", 1)
     assert out[0][0] == out[1][0]
     np.testing.assert_allclose(out[1][1], out[0][1], rtol=0, atol=1e-12 * np.abs(out[0][1]).max())
+
+
+@pytest.mark.parametrize("m", [8, 16, 3])
+@pytest.mark.parametrize("mma", [0, 1])
+def test_direct_solver_dense_kernels(m, mma):
+    """Direct (dense inverse) solves through the dense-apply kernels: the FP64
+    tensor-core kernel (n > 1024, m = 8 / 16) and the CUDA-core ones."""
+    from paper_2103_07329_b200 import _lib
+    A, _ = gen_poisson3d(12, 12, 12)
+    B = np.random.default_rng(m).uniform(-1, 1, (A.nrows, m))
+    try:
+        _lib.set_option("dense_mma", mma)
+        X = BlockVector.zeros(A.nrows, m)
+        st = prepare(tree({"solver": {"method": "Direct"}}), A).run(BlockVector.from_array(B), X)
+    finally:
+        _lib.set_option("dense_mma", 1)
+    ref = np.linalg.solve(A.to_dense(), B)
+    np.testing.assert_allclose(X.data, ref, rtol=0, atol=1e-11 * np.abs(ref).max())
+    assert st.iterations == 1 and np.all(st.converged)
