@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--matrix", default="c2", choices=["c2", "c3", "c4", "c5", "c2l1"])
+    ap.add_argument("--matrix", default="c2", choices=["c2", "c3", "c4", "c5", "c2l1", "c3l1"])
     ap.add_argument("--m", type=int, default=8)
     ap.add_argument("--mode", default="rsub", choices=["assign", "rsub"])
     ap.add_argument("--reps", type=int, default=20)
@@ -36,6 +36,9 @@ def main():
     elif a.matrix == "c2l1":
         from paper_2103_07329_b200.amg import setup
         A = setup(gen_poisson3d(64, 64, 64)[0]).levels[1].A
+    elif a.matrix == "c3l1":          # C3's level 1 (mixed precision: f32 values)
+        from paper_2103_07329_b200.amg import setup
+        A = setup(gen_poisson3d(128, 128, 128)[0], mixed_precision=True).levels[1].A
     else:
         g = 64 if a.matrix == "c2" else 128
         A = gen_poisson3d(g, g, g)[0]
