@@ -215,10 +215,12 @@ __device__ __forceinline__ void row_begin(const SpArgs& a, int o, double (&acc)[
         }
         subtract = !(mode == MRS_MODE_ASSIGN || mode == MRS_MODE_ADD);
     } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
-        // r = b - A x  (RSUB order: start at b, subtract in entry order)
-        keep = ldv<CPL, NC>(a.b + o);
+        // r = b - A x  (RSUB order: start at b, subtract in entry order); b
+        // is re-read by row_end for the fused dot rather than held across
+        // the accumulation (4 fewer live registers in the gather loop)
+        Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
 #pragma unroll
-        for (int i = 0; i < CPL; ++i) acc[i] = keep.v[i];
+        for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
         subtract = true;
     } else {  // OP_CHEB_STEP: tmp = A dv from 0
 #pragma unroll
@@ -267,8 +269,9 @@ __device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double 
         }
         store_vec<CPL>(a.x_out + o, xo);
         if (a.dot) {
+            const Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(keep.v[i], xo.v[i]));
+            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
         }
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
         const double dd = __ldg(a.d + row);
