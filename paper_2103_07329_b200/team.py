@@ -253,6 +253,8 @@ def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: 
         # the reference's hybrid sweep couples leaves through the pre-sweep
         # iterate; the device sweep implements the one-leaf order only
         raise ConfigurationError("Gauss-Seidel smoothing is single-GPU only on the device path")
+    if desc.method == _lib.METHOD_DIRECT:
+        raise ConfigurationError("the Direct solver (dense inverse) is single-GPU only")
     if exec_mode == "graph":
         # NCCL p2p/collectives are captured into one ordinary graph per
         # iteration (host checks convergence between launches) rather than

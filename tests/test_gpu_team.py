@@ -77,3 +77,38 @@ def test_team_of_one_dense_tail_on_replicated_levels(name):
     assert sd.iterations == ss.iterations and sd.all_converged
     np.testing.assert_array_equal(Xd.data, Xs.data)
     team.close()
+
+
+def test_team_single_gpu_only_configs_raise():
+    from paper_2103_07329_b200.errors import ConfigurationError
+    A, _ = gen_poisson3d(6, 6, 6)
+    team = GpuTeam()
+    for roles in ({"solver": {"method": "Direct"}},
+                  {"solver": {"method": "Gauss-Seidel"}},
+                  {"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"}}):
+        with pytest.raises(ConfigurationError):
+            prepare(tree(roles), A, team=team)
+    team.close()
+
+
+@pytest.mark.parametrize("roles", [
+    {"solver": {"method": "MultiGrid", "rel_tolerance": "1e-8", "max_iters": "60"},
+     "pre_smoother": JAC, "post_smoother": JAC},
+    {"solver": {"method": "Jacobi", "rel_tolerance": "1e-3", "max_iters": "300", "weight": "0.9"}},
+    {"solver": {"method": "CG", "rel_tolerance": "1e-9"},
+     "preconditioner": {"method": "Chebyshev", "polynomial_order": "3"}},
+])
+def test_team_of_one_other_families(roles):
+    """MultiGrid-as-solver, stationary Jacobi and the Chebyshev preconditioner
+    through the distributed code path (1-rank NCCL team) equal the single-GPU
+    bits."""
+    A, _ = gen_poisson3d(10, 9, 8)
+    B = np.random.default_rng(6).uniform(-1, 1, (A.nrows, 2))
+    Xs = BlockVector.zeros(A.nrows, 2)
+    ss = prepare(tree(roles), A).run(BlockVector.from_array(B), Xs)
+    team = GpuTeam(agg_rows_per_rank=1, force_replicate_from=1)
+    Xd = BlockVector.zeros(A.nrows, 2)
+    sd = prepare(tree(roles), A, team=team).run(BlockVector.from_array(B), Xd)
+    assert sd.iterations == ss.iterations
+    np.testing.assert_array_equal(Xd.data, Xs.data)
+    team.close()
