@@ -56,6 +56,8 @@ void set_spmm_chunk_rows(int64_t v);
 void set_spmm_long_split(int64_t v);
 void set_spmm_coop(int64_t v);
 bool dense_mma_enabled();
+int64_t loop_unroll();
+void set_loop_unroll(int64_t v);
 void set_dense_mma(int64_t v);
 int64_t spmm_long_split();
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)

@@ -33,6 +33,9 @@ void set_spmm_chunk_rows(int64_t v) { g_chunk_rows = v < 1 ? 1 : v; }
 static int64_t g_long_split = 1;      // long rows by whole CTAs (0: lane path only)
 int64_t spmm_long_split() { return g_long_split; }
 void set_spmm_long_split(int64_t v) { g_long_split = v ? 1 : 0; }
+static int64_t g_loop_unroll = 4;     // CG bodies of <= 4 kernels: iterations per WHILE trip
+int64_t loop_unroll() { return g_loop_unroll; }
+void set_loop_unroll(int64_t v) { g_loop_unroll = v < 1 ? 1 : (v > 8 ? 8 : v); }
 static int64_t g_dense_mma = 1;       // FP64 tensor-core dense tail (dense_mma_kernel)
 bool dense_mma_enabled() { return g_dense_mma != 0; }
 void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }

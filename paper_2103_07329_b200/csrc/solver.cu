@@ -82,6 +82,7 @@ struct mrs_plan {
     std::map<std::string, TailStep*> tail_cache;   // uploaded step lists
     double* inv = nullptr;
     int64_t nc = 0;
+    const int* body_guard = nullptr;   // capture of unrolled loop-body copies (&st->stop)
     int dense_from = -1;       // collapsed V-cycle tail: level, dense operator, rows
     double* tail_op = nullptr;
     int64_t tail_n = 0;
@@ -576,7 +577,8 @@ void append(std::vector<Launch>& dst, std::vector<Launch>& src) {
 
 void build_cg(mrs_plan* P, bool x_zero, Program& pg) {
     const int64_t n = P->n;
-    const int* skip = &P->st->skip;
+    // unrolled body copies are guarded by `stop` (skip implies stop)
+    const int* skip = P->body_guard ? P->body_guard : &P->st->skip;
     const DevCsr& A = P->L[0].A;
     const mrs_plan_desc& d = P->desc;
     const bool pc_on = d.precond != MRS_PC_NONE;
@@ -966,6 +968,18 @@ int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s) {
         cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
         MRS_CUDA_OK(cudaStreamBeginCaptureToGraph(cs, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
         if (run_list(pg.body, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
+        // short CG bodies: more iterations per trip of the WHILE node (each
+        // trip costs ~4 us of conditional relaunch); the extra copies run
+        // only while `stop` is clear, so iterations and results are unchanged
+        const int copies = (P->desc.method == MRS_METHOD_CG && pg.body.size() <= 4)
+                               ? (int)loop_unroll() : 1;
+        for (int u = 1; u < copies; ++u) {
+            P->body_guard = &P->st->stop;
+            Program pg2;
+            build_program(P, x_zero, pg2);
+            P->body_guard = nullptr;
+            if (run_list(pg2.body, cs) != cudaSuccess) { cudaStreamEndCapture(cs, &gg); return MRS_ERR_CUDA; }
+        }
         MRS_CUDA_OK(cudaStreamEndCapture(cs, &gg));
         after.assign(1, wnode);
     }

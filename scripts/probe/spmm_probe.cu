@@ -1070,11 +1070,64 @@ static void graph_gap() {
     }
 }
 
+
+__global__ void k_loopctl(cudaGraphConditionalHandle h, int* cnt, int iters) {
+    int c = ++cnt[0];
+    cudaGraphSetConditional(h, c < iters ? 1u : 0u);
+}
+
+static void while_gap() {
+    cudaStream_t st;
+    cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
+    int* cnt;
+    CK(cudaMalloc(&cnt, 4));
+    for (int body : {1, 16}) {
+        const int iters = 200 / body;
+        cudaGraph_t g;
+        CK(cudaGraphCreate(&g, 0));
+        cudaGraphConditionalHandle h;
+        CK(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams cp = {};
+        cp.type = cudaGraphNodeTypeConditional;
+        cp.conditional.handle = h;
+        cp.conditional.type = cudaGraphCondTypeWhile;
+        cp.conditional.size = 1;
+        cudaGraphNode_t wnode;
+        CK(cudaGraphAddNode(&wnode, g, nullptr, 0, &cp));
+        cudaGraph_t bodyg = cp.conditional.phGraph_out[0];
+        CK(cudaStreamBeginCaptureToGraph(st, bodyg, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+        for (int i = 0; i < body - 1; ++i) k_empty<<<888, 256, 0, st>>>(nullptr);
+        k_loopctl<<<1, 1, 0, st>>>(h, cnt, iters);
+        cudaGraph_t tmp;
+        CK(cudaStreamEndCapture(st, &tmp));
+        cudaGraphExec_t ge;
+        CK(cudaGraphInstantiate(&ge, g, 0));
+        CK(cudaMemset(cnt, 0, 4));
+        CK(cudaGraphLaunch(ge, st));
+        CK(cudaStreamSynchronize(st));
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0); cudaEventCreate(&e1);
+        const int R = 5;
+        float tot = 0;
+        for (int r = 0; r < R; ++r) {
+            CK(cudaMemset(cnt, 0, 4));
+            CK(cudaStreamSynchronize(st));
+            cudaEventRecord(e0, st);
+            CK(cudaGraphLaunch(ge, st));
+            cudaEventRecord(e1, st);
+            CK(cudaEventSynchronize(e1));
+            float ms; cudaEventElapsedTime(&ms, e0, e1); tot += ms;
+        }
+        printf("WHILE loop, body of %d kernels (grid 888 + 1-thread control), %d iterations: %.3f us per iteration, %.3f us per kernel\n",
+               body, iters, tot / R * 1e3 / iters, tot / R * 1e3 / (iters * body));
+    }
+}
+
 int main(int argc, char** argv) {
     CK(cudaMalloc(&g_flush, 256u << 20));
     const char* which = argc > 1 ? argv[1] : "all";
     auto want = [&](const char* k) { return !strcmp(which, "all") || strstr(which, k); };
-    if (!strcmp(which, "gap")) { graph_gap(); return 0; }
+    if (!strcmp(which, "gap")) { graph_gap(); while_gap(); return 0; }
     if (want("c2")) { Csr A = poisson7(64); bench_matrix<8, 8>(A); }
     if (want("c3")) { Csr A = poisson7(128); bench_matrix<16, 8>(A); bench_matrix<8, 8>(A); }
     if (want("c4")) { Csr A = stencil27(128); bench_matrix<8, 32>(A); }

@@ -439,3 +439,33 @@ def test_direct_solver_dense_kernels(m, mma):
     ref = np.linalg.solve(A.to_dense(), B)
     np.testing.assert_allclose(X.data, ref, rtol=0, atol=1e-11 * np.abs(ref).max())
     assert st.iterations == 1 and np.all(st.converged)
+
+
+@pytest.mark.parametrize("pc", [None, {"method": "Jacobi"}])
+@pytest.mark.parametrize("max_iters", ["7", "500"])
+def test_cg_loop_unroll_bitwise(pc, max_iters):
+    """Short CG bodies are captured U times per trip of the WHILE node, the
+    extra copies guarded by `stop`: iterations (also when max_iters cuts a
+    trip short), history and X bitwise those of one copy per trip."""
+    from paper_2103_07329_b200 import _lib
+    A, _ = gen_poisson3d(16, 15, 14)
+    B = np.random.default_rng(11).uniform(-1, 1, (A.nrows, 4))
+    roles = {"solver": {"method": "CG", "rel_tolerance": "1e-9", "max_iters": max_iters}}
+    if pc is not None:
+        roles["preconditioner"] = pc
+    out = {}
+    try:
+        for u in (1, 4, 3):
+            _lib.set_option("loop_unroll", u)
+            cs = prepare(tree(roles), A)
+            X = BlockVector.zeros(A.nrows, 4)
+            st = cs.run(BlockVector.from_array(B), X)
+            out[u] = (st.iterations, X.data.copy(), np.array(st.residual_history))
+    finally:
+        _lib.set_option("loop_unroll", 4)
+    for u in (4, 3):
+        assert out[u][0] == out[1][0]
+        np.testing.assert_array_equal(out[u][1], out[1][1])
+        np.testing.assert_array_equal(out[u][2], out[1][2])
+    if max_iters == "7":
+        assert out[1][0] == 7
