@@ -260,7 +260,7 @@ __global__ void __launch_bounds__(kThreads) dense_mma_kernel(const double* __res
     double c[NT][2];
 #pragma unroll
     for (int j = 0; j < NT; ++j) c[j][0] = c[j][1] = 0.0;
-    constexpr int U = 4;   // k-steps in flight
+    constexpr int U = 16;  // k-steps in flight (ncu: 4 left the kernel at 26% occupancy, latency-bound)
     for (int64_t k = k0; k < k1; k += 4 * U) {
         double av[U], bv[U][NT];
 #pragma unroll
