@@ -299,9 +299,10 @@ int  mrs_version(void);
  *   "spmm_chunk_rows" N  rows per CTA chunk of the SpMM grid (default 64)
  *   "spmm_long_split" 0/1  rows far longer than their operator's mean run on
  *                   whole CTAs (default 1; solver levels only)
- *   "spmm_coop" 0/1  operators with >= 12 entries per row (outside the LONG range)
- *                   load a row's entries once per lane group and shuffle them
- *                   (default 1)
+ *   "spmm_coop" 0/1/2  load a row's entries once per lane group and shuffle them:
+ *                   1 = operators with >= 12 entries per row (outside the LONG range),
+ *                   2 = (default) only long uniform rows (>= 20 per row, max <= 1.1 x mean;
+ *                   27-point stencils), 0 = off
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

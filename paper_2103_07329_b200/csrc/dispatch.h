@@ -25,6 +25,7 @@ struct DevCsr {
     int ib = 4, vb = 8;
     int32_t* long_rows = nullptr; // rows with > long_thr entries (spmm.cuh long_row_cta)
     int n_long = 0, long_thr = 0;
+    int max_row = 0;              // longest row (solver levels; 0 = unknown)
     bool present() const { return rp != nullptr; }
     // algorithmic bytes of one pass over the CSR arrays
     double bytes() const {

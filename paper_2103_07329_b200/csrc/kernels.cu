@@ -39,9 +39,9 @@ void set_loop_unroll(int64_t v) { g_loop_unroll = v < 1 ? 1 : (v > 8 ? 8 : v); }
 static int64_t g_dense_mma = 1;       // FP64 tensor-core dense tail (dense_mma_kernel)
 bool dense_mma_enabled() { return g_dense_mma != 0; }
 void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }
-static int64_t g_coop = 0;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
+static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
-void set_spmm_coop(int64_t v) { g_coop = v ? 1 : 0; }
+void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
 static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
 int tail_rows_threshold() { return (int)g_tail_rows; }
 void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
@@ -62,6 +62,7 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
     a.ncols_hint = A.ncols;
     a.slab_base = A.slab_base;
     a.slab_shift = A.slab_shift;
+    a.max_row_hint = A.max_row;
     a.long_rows = A.long_rows;
     a.n_long = spmm_long_split() ? A.n_long : 0;
     a.long_thr = A.long_thr;

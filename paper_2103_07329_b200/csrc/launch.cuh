@@ -106,7 +106,13 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         }
     }
     // large operators with long rows: cooperative entry loads (coop_accumulate)
-    if (!generic && spmm_coop() && a.nnz_hint >= 12 * a.nrows) {
+    // spmm_coop: 1 = every operator with >= 12 entries per row; 2 (default) =
+    // only long AND uniform rows (27-point stencils: mean >= 20, no row more
+    // than ~10 % above it), where the warp-uniform trip count wastes nothing
+    const int64_t coop = spmm_coop();
+    const bool uniform_long = a.nnz_hint >= 20 * a.nrows && a.max_row_hint > 0 &&
+                              (int64_t)a.max_row_hint * 10 * a.nrows <= 11 * a.nnz_hint + 10 * a.nrows;
+    if (!generic && ((coop == 1 && a.nnz_hint >= 12 * a.nrows) || (coop == 2 && uniform_long))) {
         switch (m) {
         case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB); return cudaGetLastError();
         case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB); return cudaGetLastError();

@@ -1020,6 +1020,8 @@ int upload_csr(const mrs_host_csr* h, DevCsr& d, std::vector<void*>& owned) {
         MRS_CUDA_OK(cudaMemcpy(d.ci, h->col_idx, (size_t)h->nnz * d.ib, cudaMemcpyHostToDevice));
     }
     MRS_CUDA_OK(cudaMemcpy(d.v, h->values, (size_t)h->nnz * d.vb, cudaMemcpyHostToDevice));
+    for (int64_t i = 0; i < h->nrows; ++i)
+        d.max_row = std::max<int>(d.max_row, (int)(rp[i + 1] - rp[i]));
     // rows far longer than the mean (AMG coarse operators): whole-CTA path
     if (h->nrows > 0 && h->nnz > 0) {
         const int64_t mean = (h->nnz + h->nrows - 1) / h->nrows;

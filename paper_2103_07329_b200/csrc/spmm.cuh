@@ -79,6 +79,7 @@ struct SpArgs {
     int64_t ncols_hint;     // matrix columns
     const int32_t* long_rows;  // rows with more than long_thr entries (one CTA each)
     int n_long, long_thr, long_ctas;   // long_ctas: trailing CTAs of the grid doing them
+    int max_row_hint;          // longest row (0: unknown) -- layout choice
     RedArgs red;
 };
 // shared-memory products per chunk of a long row (long_row_cta)

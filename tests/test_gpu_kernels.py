@@ -270,4 +270,4 @@ def test_spmv_coop_entry_loads_bitwise(m, vdt, coop, rng):
             O.csr_spmv(blk.row_ptr, blk.col_idx, vals, x, ref, mode, b if mode == 3 else None)
             np.testing.assert_array_equal(y, ref, err_msg=f"mode {mode}")
     finally:
-        _lib.set_option("spmm_coop", 0)
+        _lib.set_option("spmm_coop", 2)
