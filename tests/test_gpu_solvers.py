@@ -469,3 +469,29 @@ def test_cg_loop_unroll_bitwise(pc, max_iters):
         np.testing.assert_array_equal(out[u][2], out[1][2])
     if max_iters == "7":
         assert out[1][0] == 7
+
+
+def test_coop_auto_on_27_point_operator():
+    """The 27-point fine level (long uniform rows) takes the cooperative
+    entry-load SpMM by default (spmm_coop = 2); same iterations and solution
+    as the lane path."""
+    from paper_2103_07329_b200 import _lib
+    from paper_2103_07329_b200.io import gen_stencil27_aniso
+    A = gen_stencil27_aniso(24, seed=4)
+    B = np.random.default_rng(2).uniform(-1, 1, (A.nrows, 8))
+    roles = {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+             "preconditioner": {"method": "MultiGrid"},
+             "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+             "post_smoother": {"method": "Jacobi", "weight": "0.8"}}
+    out = {}
+    try:
+        for mode in (0, 2):
+            _lib.set_option("spmm_coop", mode)
+            X = BlockVector.zeros(A.nrows, 8)
+            st = prepare(tree(roles), A).run(BlockVector.from_array(B), X)
+            assert st.all_converged
+            out[mode] = (st.iterations, X.data.copy())
+    finally:
+        _lib.set_option("spmm_coop", 2)
+    assert out[0][0] == out[2][0]
+    np.testing.assert_allclose(out[2][1], out[0][1], rtol=0, atol=1e-9 * np.abs(out[0][1]).max())
