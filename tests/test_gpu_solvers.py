@@ -350,7 +350,13 @@ def test_cluster_tail_is_bitwise_identical(roles, m):
 
 @pytest.mark.parametrize("roles", [GG.SOLVE_CASES["c2_amg_pcg_20"][3],
                                    GG.SOLVE_CASES["c3_amg_bicgstab_full_cheb3"][3],
-                                   GG.SOLVE_CASES["c3_amg_bicgstab_mixed"][3]])
+                                   GG.SOLVE_CASES["c3_amg_bicgstab_mixed"][3],
+                                   GG.SOLVE_CASES["amg_pcg_default_sgs"][3],
+                                   {"solver": {"method": "CG", "rel_tolerance": "1e-9"},
+                                    "preconditioner": {"method": "MultiGrid", "max_iters": "2"},
+                                    "pre_smoother": {"method": "Jacobi", "weight": "0.7"},
+                                    "post_smoother": {"method": "Chebyshev",
+                                                      "polynomial_order": "2"}}])
 @pytest.mark.parametrize("m", [1, 8, 16])
 def test_dense_tail_matches_per_level_kernels(roles, m, monkeypatch):
     """The collapsed V-cycle tail (one dense launch for the levels <=
