@@ -62,3 +62,12 @@ def test_cli_run_on_gpu(tmp_path):
     rows = out.read_text().strip().splitlines()
     assert rows[0].split(",") == list(cli.CSV_COLUMNS)
     assert len(rows) == 3 and rows[2].split(",")[1] == "4"
+
+
+def test_report_stats_format():
+    from paper_2103_07329_b200.solvers import SolveStats
+    st = SolveStats(3, np.array([True, False]), np.array([1e-9, 2e-3]),
+                    [np.array([1.0, 1.0]), np.array([1e-3, 1e-2]), np.array([1e-9, 2e-3])], "CG")
+    out = cli.report_stats(st)
+    assert "iterations: 3" in out and "converged: NO (1/2 columns)" in out
+    assert "max relative residual: 2.000000e-03" in out
