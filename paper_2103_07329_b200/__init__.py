@@ -14,6 +14,8 @@ Layout:
   solvers   prepare / ConfiguredSolver / SolveStats (device-driven solve)
   team      multi-GPU row partition over NCCL (halo exchange, allreduce)
   io        seeded generators for the BASELINE.json configurations
+  sysfile   XAMGBIN1 system files and YAML run configurations
+  cli       the batch driver (python -m paper_2103_07329_b200.cli)
 """
 
 from .core import (SUPPORTED_NRHS, BlockVector, CsrBlock, IndexWidth, PrecisionTag,
@@ -23,6 +25,7 @@ from .errors import (BreakdownError, CapacityError, ConfigurationError, DeviceEr
                      SetupDegeneracyError, ShapeMismatchError, SingularDiagonalError,
                      SingularMatrixError)
 from .io import gen_poisson3d, gen_random_sdd, gen_stencil27_aniso, seeded_rhs
+from .sysfile import parse_run_config, read_system, write_system
 from .params import ParamList, ParamTree
 from .amg import AmgParams, Hierarchy, Level, estimate_eig_bounds, setup
 
@@ -34,7 +37,7 @@ def __getattr__(name):
     if name in ("prepare", "solve", "SolveStats", "ConfiguredSolver"):
         from . import solvers
         return getattr(solvers, name)
-    if name in ("kernels", "solvers", "team"):
+    if name in ("kernels", "solvers", "team", "cli"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     raise AttributeError(name)
