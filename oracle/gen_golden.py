@@ -18,7 +18,12 @@ import hashlib
 import os
 import sys
 
-import numpy as np
+# the reference's LAPACK coarse solve (scipy lu_solve) on ONE thread: threaded
+# getrs rounds differently, and the oracle replays the 1-thread order
+for _v in ("OPENBLAS_NUM_THREADS", "OMP_NUM_THREADS", "MKL_NUM_THREADS"):
+    os.environ.setdefault(_v, "1")
+
+import numpy as np  # noqa: E402
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
@@ -312,8 +317,120 @@ def gen_sysfile(ms):
     write_system(os.path.join(OUT, "xamgbin1_ref.bin"), A, rhs, guess)
 
 
+_JAC08 = {"method": "Jacobi", "weight": "0.8"}
+_CHEB2 = {"method": "Chebyshev", "polynomial_order": "2"}
+#: BASELINE.json configs at their FULL sizes (C1-C3 on the reference generator)
+#: and the builder-defined C4 operator family (27-pt anisotropic) at sizes the
+#: reference finishes in minutes: (kind, grid, m, seed, roles)
+FULL_CASES = {
+    "c1": ("p7", 32, 4, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8",
+                                       "max_iters": "1000"},
+                            "preconditioner": {"method": "Jacobi"}}),
+    "c2": ("p7", 64, 8, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+                            "preconditioner": {"method": "MultiGrid"},
+                            "pre_smoother": _JAC08, "post_smoother": _JAC08}),
+    "c3": ("p7", 128, 16, 0, {"solver": {"method": "BiCGStab", "rel_tolerance": "1e-8"},
+                              "preconditioner": {"method": "MultiGrid",
+                                                 "mg_mixed_precision": "1"},
+                              "pre_smoother": _CHEB2, "post_smoother": _CHEB2}),
+    "c4_24": ("s27", 24, 8, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+                                "preconditioner": {"method": "MultiGrid"},
+                                "pre_smoother": _JAC08, "post_smoother": _JAC08}),
+    "c4_32": ("s27", 32, 8, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+                                "preconditioner": {"method": "MultiGrid"},
+                                "pre_smoother": _JAC08, "post_smoother": _JAC08}),
+    "c4_64": ("s27", 64, 8, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+                                "preconditioner": {"method": "MultiGrid"},
+                                "pre_smoother": _JAC08, "post_smoother": _JAC08}),
+    "c4_128": ("s27", 128, 8, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+                                  "preconditioner": {"method": "MultiGrid"},
+                                  "pre_smoother": _JAC08, "post_smoother": _JAC08}),
+    # BASELINE.json config 4 at its full size (449 M nnz; ~30 min, ~40 GB)
+    "c4_256": ("s27", 256, 8, 0, {"solver": {"method": "CG", "rel_tolerance": "1e-8"},
+                                  "preconditioner": {"method": "MultiGrid"},
+                                  "pre_smoother": _JAC08, "post_smoother": _JAC08}),
+}
+#: rows of X stored per case (strided sample; the full X hash is stored too)
+SAMPLE_ROWS = 4096
+
+
+def sample_rows(n: int) -> np.ndarray:
+    """Strided row sample of an n-row solution (first and last row included)."""
+    if n <= SAMPLE_ROWS:
+        return np.arange(n)
+    return np.unique(np.concatenate([np.linspace(0, n - 1, SAMPLE_ROWS).astype(np.int64),
+                                     [n - 1]]))
+
+
+def gen_fullsize(ms, names=None):
+    """Reference outputs at BASELINE.json's full sizes (C1-C3) and for the C4
+    operator family: iterations, residual history, final relative residuals,
+    a strided X sample + the full-X hash, and per-level (rows, nnz, SHA) of
+    the reference hierarchy with its Chebyshev eigenvalue bounds.  One file
+    per case (tests/golden/full_<case>.npz) so cases can be regenerated alone.
+    C3 takes ~3 min and c4_64 a few minutes on one core."""
+    import time
+    from mrsolve.core import BlockVector, CsrBlock
+    from mrsolve.io import gen_poisson3d
+    sys.path.insert(0, ROOT)
+    from paper_2103_07329_b200.io import gen_stencil27_aniso
+    for name, (kind, g, m, seed, roles) in FULL_CASES.items():
+        if names and name not in names:
+            continue
+        if kind == "p7":
+            A, _ = gen_poisson3d(g, g, g)
+        else:
+            G = gen_stencil27_aniso(g, seed=4)
+            A = CsrBlock(G.nrows, G.ncols, G.row_ptr, G.col_idx, G.values)
+        n = A.nrows
+        B = np.random.default_rng(seed).uniform(-1.0, 1.0, (n, m))
+        t0 = time.perf_counter()
+        cs = ms.prepare(tree(ms, roles), A)
+        t_setup = time.perf_counter() - t0
+        X = BlockVector.zeros(n, m)
+        t0 = time.perf_counter()
+        st = cs.run(BlockVector.from_array(B), X)
+        t_solve = time.perf_counter() - t0
+        rows = sample_rows(n)
+        out = {"kind": np.array(kind), "grid": np.int64(g), "m": np.int64(m),
+               "seed": np.int64(seed), "iters": np.int64(st.iterations),
+               "rel": st.final_rel_residual, "hist": np.array(st.residual_history),
+               "rows": rows, "X_rows": X.data[rows], "X_sha": np.array(sha(X.data)),
+               "X_norm": np.linalg.norm(X.data, axis=0), "B_sha": np.array(sha(B)),
+               "t_setup": np.float64(t_setup), "t_solve": np.float64(t_solve)}
+        h = cs.hierarchy
+        if h is not None:
+            out["nlevels"] = np.int64(h.nlevels)
+            for l, lv in enumerate(h.levels):
+                Ag = lv.A.blocks[0].diag
+                out[f"L{l}_A_shape"] = np.array([Ag.nrows, Ag.nnz])
+                out[f"L{l}_eig"] = np.array(lv.eig_bounds if lv.eig_bounds else [np.nan, np.nan])
+                for tag, blk in (("A", Ag), ("P", lv.P), ("R", lv.R)):
+                    if blk is None:
+                        continue
+                    out[f"L{l}_{tag}_sha"] = np.array(
+                        [sha(blk.row_ptr.astype(np.int64)), sha(blk.col_idx.astype(np.int64)),
+                         sha(blk.values)])
+                    out[f"L{l}_{tag}_dtype"] = np.array(str(blk.values.dtype))
+        np.savez_compressed(os.path.join(OUT, f"full_{name}.npz"), **out)
+        print(f"full {name}: n={n} m={m} iters={st.iterations} "
+              f"levels={h.nlevels if h is not None else '-'} "
+              f"maxrel={st.final_rel_residual.max():.3e} setup {t_setup:.1f}s "
+              f"solve {t_solve:.1f}s", flush=True)
+
+
 def main():
-    """All fixtures, or only the named groups (e.g. ``gen_golden.py solves``)."""
+    """All fixtures, or only the named groups (e.g. ``gen_golden.py solves``;
+    ``gen_golden.py fullsize[:c2,c4_24]`` for the full-size reference runs)."""
+    args = sys.argv[1:]
+    full = [a for a in args if a.startswith("fullsize")]
+    if full:
+        ms = import_reference()
+        assert ms.kernels.BACKEND == "cython", ms.kernels.BACKEND
+        os.makedirs(OUT, exist_ok=True)
+        sel = full[0].split(":", 1)[1].split(",") if ":" in full[0] else None
+        gen_fullsize(ms, sel)
+        return
     ms = import_reference()
     assert ms.kernels.BACKEND == "cython", ms.kernels.BACKEND
     os.makedirs(OUT, exist_ok=True)
