@@ -292,7 +292,6 @@ const char* mrs_status_string(int32_t status);
 int  mrs_version(void);
 /* Tuning knobs, read when a plan captures its graph:
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
- *   "tail_rows" N  V-cycle levels with <= N rows run as one cluster kernel (0: off)
  *   "spmm_long_rows" N  operators with <= N rows and >= 12 entries per row run the
  *                   SpMM with 16 entries in flight per lane (default 20000; 0: off)
  *   "coarse_rows" N  rows per CTA of the dense coarse solve (default 1)

@@ -7,6 +7,9 @@
 // the caller's stream.
 #include <cstdint>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "dispatch.h"
@@ -28,18 +31,21 @@ struct Scratch {
     int cap = 0;
 };
 
-// One reduction scratch per device per thread (plugin calls are stream-ordered;
-// concurrent use from several host threads needs distinct streams AND is
-// serialised here by thread_local ownership).
-thread_local Scratch t_scratch[16];
+// One reduction scratch (CTA partials + last-CTA ticket) per (device,
+// stream): calls on one stream are ordered, so they can share it; calls on
+// different streams may run concurrently and must not (the ticket protocol of
+// finish_reduction assumes one reduction at a time per scratch).
+std::mutex g_scratch_mu;
+std::map<std::pair<int, uintptr_t>, Scratch> g_scratch;
 
-int get_scratch(int64_t Km, Scratch** out) {
+int get_scratch(int64_t Km, void* stream, Scratch** out) {
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return MRS_ERR_CUDA;
-    Scratch& s = t_scratch[dev];
+    if (cudaGetDevice(&dev) != cudaSuccess) return MRS_ERR_CUDA;
+    std::lock_guard<std::mutex> lk(g_scratch_mu);
+    Scratch& s = g_scratch[{dev, (uintptr_t)stream}];
     int need = max_grid() * (int)Km;
     if (s.cap < need) {
-        if (s.partials) cudaFree(s.partials);
+        if (s.partials) cudaFree(s.partials);     // synchronising: no kernel still uses it
         if (!s.ticket) {
             if (cudaMalloc(&s.ticket, sizeof(unsigned int)) != cudaSuccess) return MRS_ERR_ALLOC;
             if (cudaMemset(s.ticket, 0, sizeof(unsigned int)) != cudaSuccess) return MRS_ERR_CUDA;
@@ -62,7 +68,7 @@ int vec_call(int op, VArgs a, int K, double* out, void* stream) {
     }
     if (K) {
         Scratch* s = nullptr;
-        int rc = get_scratch(K * a.m, &s);
+        int rc = get_scratch(K * a.m, stream, &s);
         if (rc) return rc;
         a.red.partials = s->partials;
         a.red.ticket = s->ticket;
@@ -85,7 +91,6 @@ int mrs_version(void) { return 1; }
 int mrs_set_option(const char* key, int64_t value) {
     if (!key) return MRS_ERR_ARG;
     if (!strcmp(key, "pdl")) { set_pdl((int)value); return MRS_OK; }
-    if (!strcmp(key, "tail_rows")) { set_tail_rows(value); return MRS_OK; }
     if (!strcmp(key, "coarse_rows")) { set_coarse_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }

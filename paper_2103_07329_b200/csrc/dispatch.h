@@ -44,13 +44,6 @@ cudaError_t launch_dense(const double* T, int64_t n, const double* b, double* x,
                          const int* guard, cudaStream_t s);
 cudaError_t launch_coarse(const double* inv, int64_t nc, const double* b, double* x,
                           int64_t m, const int* guard, cudaStream_t s);
-// V-cycle tail on one thread-block cluster (tail.cu)
-struct TailStep;
-cudaError_t launch_tail(const TailStep* steps, int nsteps, int64_t m, const int* guard, int csize,
-                        cudaStream_t s);
-int tail_cluster_size(int64_t m);
-int tail_rows_threshold();
-void set_tail_rows(int64_t v);
 void set_coarse_rows(int64_t v);
 void set_spmm_long_rows(int64_t v);
 void set_spmm_chunk_rows(int64_t v);

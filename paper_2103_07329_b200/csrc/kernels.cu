@@ -42,9 +42,6 @@ void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
-static int64_t g_tail_rows = 0;   // cluster tail measured slower (profiles/r01_ab_experiments.txt)
-int tail_rows_threshold() { return (int)g_tail_rows; }
-void set_tail_rows(int64_t v) { g_tail_rows = v < 0 ? 0 : v; }
 
 int spmm_grid(int64_t nrows, int64_t m) {   // upper bound (scratch sizing)
     (void)nrows; (void)m;

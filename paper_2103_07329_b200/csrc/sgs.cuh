@@ -180,7 +180,8 @@ __device__ __forceinline__ void sgs_walk(const SgsArgs& a, int first, int stride
 
 // CPL columns per lane (2 when m is even), m / CPL lanes per row.  One
 // thread-block cluster; cluster barrier between schedule levels (its acquire
-// side makes other CTAs' writes visible to plain loads, see tail.cuh).
+// side -- MEMBAR.GPU + CCTL.IVALL (L1 invalidate) in SASS -- makes other
+// CTAs' writes visible to plain loads).
 template <int CPL, typename Tv, typename Ti>
 __global__ void __launch_bounds__(kThreads) sgs_kernel(SgsArgs a) {
     if (a.guard && *a.guard) return;     // same value in every CTA: all skip together

@@ -29,7 +29,6 @@
 #include "comm.h"
 #include "sgs.cuh"
 #include "sgs_sched.h"
-#include "tail.cuh"
 #include "dispatch.h"
 
 using namespace mrs;
@@ -77,9 +76,6 @@ struct mrs_plan {
     std::vector<LevelDev> L;
     mrs_comm* comm = nullptr;  // multi-GPU: NCCL communicator (dist = set)
     bool dist = false;
-    int tail_from = -1;        // first level run by the cluster tail kernel (-1: none)
-    int tail_csize = 0;
-    std::map<std::string, TailStep*> tail_cache;   // uploaded step lists
     double* inv = nullptr;
     int64_t nc = 0;
     const int* body_guard = nullptr;   // capture of unrolled loop-body copies (&st->stop)
@@ -102,9 +98,21 @@ struct mrs_plan {
     unsigned int* ticket = nullptr;
     double* red_out = nullptr;
     bool finalized = false;
-    // graphs (index: x_is_zero)
-    cudaGraph_t graph[2] = {nullptr, nullptr};
-    cudaGraphExec_t exec[2] = {nullptr, nullptr};
+    // whole-solve graphs, one per (x_is_zero, bound B, bound X): the plan's
+    // own B/X buffers (host or staged inputs) or a caller's device buffers
+    // bound in place (single GPU: no halo rows on level-0 vectors)
+    struct BoundGraph {
+        int gi;
+        const double* B;
+        double* X;
+        cudaGraph_t g;
+        cudaGraphExec_t e;
+    };
+    std::vector<BoundGraph> graphs;
+    double* own_B = nullptr;   // the plan's staging buffers (B, X hold the bound ones
+    double* own_X = nullptr;   // while a bound graph is captured)
+    SolveState* st_host = nullptr;   // pinned copies read back after a solve
+    double* hist_host = nullptr;
     // exec mode 2: one captured body graph per iteration, host-checked stop
     cudaGraph_t body_graph[2] = {nullptr, nullptr};
     cudaGraphExec_t body_exec[2] = {nullptr, nullptr};
@@ -115,9 +123,13 @@ struct mrs_plan {
     int fixed_kernels = 0;
     double it_bytes = 0;
     ~mrs_plan() {
+        for (auto& bg : graphs) {
+            cudaGraphExecDestroy(bg.e);
+            cudaGraphDestroy(bg.g);
+        }
+        if (st_host) cudaFreeHost(st_host);
+        if (hist_host) cudaFreeHost(hist_host);
         for (int i = 0; i < 2; ++i) {
-            if (exec[i]) cudaGraphExecDestroy(exec[i]);
-            if (graph[i]) cudaGraphDestroy(graph[i]);
             if (body_exec[i]) cudaGraphExecDestroy(body_exec[i]);
             if (body_graph[i]) cudaGraphDestroy(body_graph[i]);
         }
@@ -151,8 +163,6 @@ struct Builder {
     const int* guard = nullptr;       // body kernels: &st->skip
     double bytes = 0;                 // algorithmic bytes accumulated
     int kernels = 0;
-    std::vector<TailStep>* rec = nullptr;   // recording a tail sub-V-cycle
-    bool rec_fail = false;
     double V(int64_t rows) const { return (double)rows * P->m * 8.0; }
 
     RedArgs red(int epi) const {
@@ -163,18 +173,6 @@ struct Builder {
     }
     static SpArgs sp0() { SpArgs a; memset(&a, 0, sizeof(a)); return a; }
     static VArgs v0() { VArgs a; memset(&a, 0, sizeof(a)); return a; }
-
-    // device copy of a recorded tail step list (memoized by content)
-    const TailStep* upload_tail(const std::vector<TailStep>& steps) {
-        std::string key(reinterpret_cast<const char*>(steps.data()), steps.size() * sizeof(TailStep));
-        auto it = P->tail_cache.find(key);
-        if (it != P->tail_cache.end()) return it->second;
-        TailStep* d = dalloc<TailStep>(steps.size(), P->owned);
-        if (!d) return nullptr;
-        if (cudaMemcpy(d, steps.data(), key.size(), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
-        P->tail_cache[key] = d;
-        return d;
-    }
 
     // multi-GPU: exchange the halo rows of a gathered operand before its use
     void exchange(const Halo* h, const double* x) {
@@ -208,18 +206,6 @@ struct Builder {
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
         int64_t m = P->m;
-        if (rec) {
-            if (a.dot) rec_fail = true;
-            TailStep t;
-            memset(&t, 0, sizeof(t));
-            t.kind = TK_SPMM; t.op = op; t.vb = A.vb; t.ib = A.ib;
-            a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.nrows = A.nrows; a.m = m;
-            a.nnz_hint = A.nnz; a.ncols_hint = A.ncols;
-            t.a = a;
-            rec->push_back(t);
-            bytes += A.bytes() + extra_bytes;
-            return;
-        }
         exchange(A.halo, a.x);
         const int mk = a.dot ? split_reduction(a.red) : 0;
         out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
@@ -228,7 +214,6 @@ struct Builder {
         kernels++;
     }
     void vec(int op, VArgs a, double b) {
-        if (rec) { rec_fail = true; return; }
         a.guard = a.guard ? a.guard : guard;
         a.m = P->m;
         const int K = vec_op_k(op);
@@ -289,7 +274,6 @@ struct Builder {
     // Gauss-Seidel sweep in place on x (blas2.py:113-162): forward and/or
     // backward half, each one cluster launch over the level schedule.
     void sgs_sweep(LevelDev& lv, const double* b, double* x, int direction) {
-        if (rec) { rec_fail = true; return; }
         const int64_t n = lv.A.nrows;
         for (int h = 0; h < 2; ++h) {
             if ((h == 0 && direction == MRS_SGS_BACKWARD) || (h == 1 && direction == MRS_SGS_FORWARD))
@@ -434,30 +418,6 @@ struct Builder {
     void vcycle(int l, const double* b, bool zero, bool seeded, XB& x, int dot_epi) {
         mrs_plan& p = *P;
         LevelDev& lv = p.L[l];
-        if (!rec && l == p.tail_from && zero && seeded && dot_epi < 0) {
-            // the whole sub-V-cycle below (and at) level l: one cluster launch
-            std::vector<TailStep> steps;
-            Builder child{P, nullptr, guard};
-            child.rec = &steps;
-            XB xr = x;
-            child.vcycle(l, b, true, true, xr, -1);
-            if (!child.rec_fail && !steps.empty()) {
-                const TailStep* dsteps = upload_tail(steps);
-                if (dsteps) {
-                    x = xr;
-                    const int nsteps = (int)steps.size();
-                    const int64_t m = p.m;
-                    const int* g = guard;
-                    const int cs = p.tail_csize;
-                    out->push_back([=](cudaStream_t s) {
-                        return launch_tail(dsteps, nsteps, m, g, cs, s);
-                    });
-                    bytes += child.bytes;
-                    kernels++;
-                    return;
-                }
-            }
-        }
         if (coarsest(p, l) || (zero && dense_tail(p, l))) {
             // x = A_c^{-1} b (replaces the LU solve, solvers.py:644-649), or
             // x = T_l b for the collapsed tail (same dense kernel)
@@ -466,16 +426,6 @@ struct Builder {
             const double* inv = tl ? p.tail_op : p.inv;
             double* xo = x.cur;
             const int* g = guard;
-            if (rec) {
-                if (tl) { rec_fail = true; return; }   // the dense tail is its own launch
-                TailStep t;
-                memset(&t, 0, sizeof(t));
-                t.kind = TK_COARSE; t.inv = inv; t.nc = nc; t.cb = b; t.cx = xo;
-                rec->push_back(t);
-                bytes += (double)nc * nc * 8.0 + 2 * V(nc);
-                if (dot_epi >= 0) rec_fail = true;
-                return;
-            }
             if (tl)
                 out->push_back([=](cudaStream_t s) { return launch_dense(inv, nc, b, xo, m, g, s); });
             else
@@ -919,10 +869,10 @@ cudaError_t run_list(const std::vector<Launch>& v, cudaStream_t s) {
     return cudaSuccess;
 }
 
-int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s) {
+int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s, cudaGraph_t* out_g,
+                  cudaGraphExec_t* out_e) {
     Program pg;
     build_program(P, x_zero, pg);
-    int gi = x_zero ? 1 : 0;
 
     cudaGraph_t g;
     MRS_CUDA_OK(cudaGraphCreate(&g, 0));
@@ -991,8 +941,8 @@ int capture_graph(mrs_plan* P, bool x_zero, cudaStream_t s) {
     cudaStreamDestroy(cs);
     cudaGraphExec_t ex;
     MRS_CUDA_OK(cudaGraphInstantiate(&ex, g, 0));
-    P->graph[gi] = g;
-    P->exec[gi] = ex;
+    *out_g = g;
+    *out_e = ex;
     return MRS_OK;
 }
 
@@ -1274,6 +1224,8 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
         *v = dalloc<double>(V, o);
         if (!*v) return MRS_ERR_ALLOC;
     }
+    p->own_B = p->B;
+    p->own_X = p->X;
     if (p->desc.method == MRS_METHOD_PBICGSTAB) {
         double** pv[] = {&p->rinit, &p->zacc, &p->w, &p->yv, &p->chk, &p->pa, &p->pb};
         for (double** v : pv) {
@@ -1300,24 +1252,10 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     hs.nodrift = 1;
     for (int c = 0; c < kMaxM; ++c) { hs.one[c] = 1.0; hs.neg_one[c] = -1.0; }
     MRS_CUDA_OK(cudaMemcpy(p->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    MRS_CUDA_OK(cudaMallocHost(&p->st_host, sizeof(SolveState)));
+    MRS_CUDA_OK(cudaMallocHost(&p->hist_host, sizeof(double) * (size_t)(p->desc.max_iters + 1) * m));
     MRS_CUDA_OK(cudaEventCreate(&p->ev0));
     MRS_CUDA_OK(cudaEventCreate(&p->ev1));
-    // cluster tail: the deepest levels with <= tail_rows rows each (never
-    // level 0; distributed: only replicated levels)
-    if (p->desc.precond == MRS_PC_MG && tail_rows_threshold() > 0 && p->L.size() >= 3) {
-        const int cs = tail_cluster_size(m);
-        int from = -1;
-        for (int l = (int)p->L.size() - 2; l >= 1; --l) {
-            const LevelDev& lv = p->L[l];
-            if (lv.A.nrows > tail_rows_threshold()) break;
-            if (p->dist && !lv.replicated) break;
-            from = l;
-        }
-        if (cs > 0 && from >= 1) {
-            p->tail_from = from;
-            p->tail_csize = cs;
-        }
-    }
     p->finalized = true;
     // estimate the per-iteration byte model / kernel count once
     Program pg;
@@ -1337,21 +1275,58 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
     const size_t bytes = (size_t)p->n * p->m * 8;
     cudaMemcpyKind in = host_buffers ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
     cudaMemcpyKind outk = host_buffers ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
-    MRS_CUDA_OK(cudaMemcpyAsync(p->B, B, bytes, in, s));
-    if (x_is_zero) MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
-    else MRS_CUDA_OK(cudaMemcpyAsync(p->X, X, bytes, in, s));
-    MRS_CUDA_OK(cudaEventRecord(p->ev0, s));
     const int gi = x_is_zero ? 1 : 0;
-    if (p->desc.exec == 0 && !p->exec[gi]) {
-        if (capture_graph(p, x_is_zero != 0, s) != MRS_OK) {
-            // e.g. collectives that cannot live inside a conditional body:
-            // fall back to one captured body graph per iteration
-            cudaGetLastError();
-            p->desc.exec = 2;
+    // device buffers of a single-GPU plan are bound into the graph in place:
+    // no staging copies of B and X (distributed plans need the halo rows of
+    // their own level-0 vectors, host buffers need the copies anyway)
+    const bool bind = p->desc.exec == 0 && !host_buffers && !p->dist &&
+                      p->L[0].vrows == p->n && ((uintptr_t)B & 15u) == 0 &&
+                      ((uintptr_t)X & 15u) == 0 && (const double*)B != X;
+    const double* gB = bind ? B : p->own_B;
+    double* gX = bind ? X : p->own_X;
+    if (!bind) {
+        MRS_CUDA_OK(cudaMemcpyAsync(p->own_B, B, bytes, in, s));
+        if (!x_is_zero) MRS_CUDA_OK(cudaMemcpyAsync(p->own_X, X, bytes, in, s));
+    }
+    if (x_is_zero) MRS_CUDA_OK(cudaMemsetAsync(gX, 0, bytes, s));
+    MRS_CUDA_OK(cudaEventRecord(p->ev0, s));
+    cudaGraphExec_t gexec = nullptr;
+    if (p->desc.exec == 0) {
+        for (auto& bg : p->graphs)
+            if (bg.gi == gi && bg.B == gB && bg.X == gX) gexec = bg.e;
+        if (!gexec) {
+            if (p->graphs.size() >= 8) {         // bounded cache: drop the oldest binding
+                auto it = p->graphs.begin();
+                while (it != p->graphs.end() && it->B == p->own_B) ++it;
+                if (it != p->graphs.end()) {
+                    cudaGraphExecDestroy(it->e);
+                    cudaGraphDestroy(it->g);
+                    p->graphs.erase(it);
+                }
+            }
+            p->B = const_cast<double*>(gB);
+            p->X = gX;
+            cudaGraph_t g = nullptr;
+            const int rc = capture_graph(p, x_is_zero != 0, s, &g, &gexec);
+            p->B = p->own_B;
+            p->X = p->own_X;
+            if (rc != MRS_OK) {
+                // e.g. collectives that cannot live inside a conditional body:
+                // fall back to one captured body graph per iteration
+                cudaGetLastError();
+                p->desc.exec = 2;
+                gexec = nullptr;
+                if (bind) {        // staged path from here on
+                    MRS_CUDA_OK(cudaMemcpyAsync(p->own_B, B, bytes, in, s));
+                    MRS_CUDA_OK(cudaMemcpyAsync(p->own_X, X, bytes, in, s));
+                }
+            } else {
+                p->graphs.push_back({gi, gB, gX, g, gexec});
+            }
         }
     }
     if (p->desc.exec == 0) {
-        MRS_CUDA_OK(cudaGraphLaunch(p->exec[gi], s));
+        MRS_CUDA_OK(cudaGraphLaunch(gexec, s));
     } else if (p->desc.exec == 2) {
         if (!p->body_exec[gi]) {
             Program pg;
@@ -1398,10 +1373,13 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
         MRS_CUDA_OK(run_list(pg.epi, s));
     }
     MRS_CUDA_OK(cudaEventRecord(p->ev1, s));
-    MRS_CUDA_OK(cudaMemcpyAsync(X, p->X, bytes, outk, s));
-    SolveState hs;
-    MRS_CUDA_OK(cudaMemcpyAsync(&hs, p->st, sizeof(hs), cudaMemcpyDeviceToHost, s));
+    if (!(bind && p->desc.exec == 0)) MRS_CUDA_OK(cudaMemcpyAsync(X, p->X, bytes, outk, s));
+    const size_t hbytes = sizeof(double) * (size_t)(p->desc.max_iters + 1) * p->m;
+    MRS_CUDA_OK(cudaMemcpyAsync(p->st_host, p->st, sizeof(SolveState), cudaMemcpyDeviceToHost, s));
+    if (history)
+        MRS_CUDA_OK(cudaMemcpyAsync(p->hist_host, p->history, hbytes, cudaMemcpyDeviceToHost, s));
     MRS_CUDA_OK(cudaStreamSynchronize(s));
+    const SolveState& hs = *p->st_host;
     float ms = 0.f;
     cudaEventElapsedTime(&ms, p->ev0, p->ev1);
     if (stats) {
@@ -1412,10 +1390,7 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
         stats->device_ms = ms;
     }
     if (final_rel) memcpy(final_rel, hs.final_rel, sizeof(double) * p->m);
-    if (history) {
-        MRS_CUDA_OK(cudaMemcpy(history, p->history, sizeof(double) * (hs.it + 1) * p->m,
-                               cudaMemcpyDeviceToHost));
-    }
+    if (history) memcpy(history, p->hist_host, sizeof(double) * (size_t)(hs.it + 1) * p->m);
     return hs.err;
 }
 

@@ -10,13 +10,14 @@ launch (iteration loop driven on the device; see csrc/solver.cu).
 
 Device path: solver CG or BiCGStab in its
 three formulations -- classical, reordered (RBiCGStab), pipelined
-(PBiCGStab); merged=0/1 --, preconditioner none / Jacobi / MultiGrid V-cycle,
-smoothers Jacobi, Chebyshev or (hybrid, one-leaf) Gauss-Seidel -- the
-reference's default MultiGrid smoother, run in its exact sequential order by
-level scheduling; a Gauss-Seidel sweep preconditioner.  Everything else the
-reference's ParamTree can express (Direct and stationary solvers, Chebyshev or
-BiCGStab as a preconditioner) is outside this path and raises
-ConfigurationError -- there is no CPU fallback.
+(PBiCGStab); merged=0/1 --, MultiGrid as a solver, the stationary Jacobi /
+Gauss-Seidel solvers and Direct (dense inverse); preconditioner none /
+Jacobi / Gauss-Seidel / Chebyshev / MultiGrid V-cycle; smoothers Jacobi,
+Chebyshev or (hybrid, one-leaf) Gauss-Seidel -- the reference's default
+MultiGrid smoother, run in its exact sequential order by level scheduling.
+The one composition the reference's ParamTree can express that is not on the
+device path -- a Krylov method (BiCGStab) as preconditioner or smoother --
+raises ConfigurationError; there is no CPU fallback.
 """
 
 from __future__ import annotations

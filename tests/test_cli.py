@@ -38,10 +38,15 @@ def test_bench_gain_validation():
 def test_csv_schema_matches_reference():
     assert cli.CSV_COLUMNS == ("method", "m", "nnumas", "ncores", "iters",
                                "max_rel_residual", "t_solve_s", "t_setup_s", "P_m")
-    r = cli.BenchReport([cli.BenchRow("CG", 1, 1, 1, 10, 1e-9, 2.0, 0.5),
-                         cli.BenchRow("CG", 4, 1, 1, 10, 1e-9, 4.0, 0.5)])
-    r.fill_gains()
-    assert r.rows[1].p_m == pytest.approx(2.0)
+    sw = cli.GainSweep()
+    sw.add(cli.Sample("CG", 1, 10, 1e-9, 2.0, 0.5, True))
+    sw.add(cli.Sample("CG", 4, 10, 1e-9, 4.0, 0.5, True))
+    sw.finish()
+    assert sw.samples[1].gain == pytest.approx(2.0)
+    lines = sw.csv_text().splitlines()
+    assert lines[0].split(",") == list(cli.CSV_COLUMNS)
+    assert lines[2].split(",")[-1] == "2.0000" and len(lines) == 3
+    assert sw.converged and "P_m" in sw.table()
 
 
 @pytest.mark.gpu
