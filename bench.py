@@ -38,6 +38,9 @@ sys.path.insert(0, ROOT)
 METRIC = "AMG-PCG RHS·iterations/sec; blocked SpMM HBM GB/s vs roofline"
 UNIT = "RHS*it/s"
 SEED, TOL = 0, 1e-8
+#: shared by both arms' `config` (the driver compares the two key for key)
+L2_NOTE = ("GPU arm: L2 flushed (256 MB read) between timed steps, outside the CUDA events; "
+           "reference arm: host CPU, no GPU caches involved")
 _JAC = {"method": "Jacobi", "weight": "0.8"}
 _CHEB = {"method": "Chebyshev", "polynomial_order": "2"}
 #: BASELINE.json configs on the reference generator (C4: builder-defined 27-pt)
@@ -319,10 +322,12 @@ def reference_arm(args, rank):
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: reference gen_poisson3d + default_rng(0).uniform(-1,1) RHS",
         "config": {"workload": WORKLOAD, "n": GRID ** 3, "m": M, "iterations": its[0],
-                   "parallelism": (f"{P} process(es) x 1 core, the m RHS columns split over "
-                                   "them (reference kernels hold the GIL: one core per process)"),
-                   "tried": {f"{k}_process": v[0] for k, v in sorted(tried.items())},
-                   "setup_s_excluded": res["setup"]},
+                   "l2": L2_NOTE},
+        "details": {"parallelism": (f"{P} process(es) x 1 core, the m RHS columns split over "
+                                    "them (reference kernels hold the GIL: one core per "
+                                    "process)"),
+                    "tried": {f"{k}_process": v[0] for k, v in sorted(tried.items())},
+                    "setup_s_excluded": res["setup"]},
         "cpu_baseline": {"value": val, "unit": UNIT, "cores": P, "kind": "reference",
                          "sample": f"{len(runs)} full {args.config.upper()} solves after "
                                    f"{args.warmup} warm-up, m={M} columns over {P} concurrent "
@@ -427,10 +432,32 @@ def make_matrix():
     return gen_poisson3d(GRID, GRID, GRID)[0]
 
 
+def self_launch(args) -> bool:
+    """--gpus N > 1 without a torchrun environment: re-run this script as N
+    ranks under torch.distributed.run (one process per GPU, NCCL), forwarding
+    every argument; the ranks' rank 0 prints the JSON line.  Returns True when
+    the child job ran (its exit status becomes ours)."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ or args.impl == "reference":
+        return False
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        port = so.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    sys.exit(rc)
+
+
 def main():
     args = parse()
     select(args.config, args.grid)
+    self_launch(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.impl != "reference" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}: launch "
+                         f"{args.gpus} ranks (torchrun) or drop WORLD_SIZE to self-launch")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
@@ -656,6 +683,7 @@ def main():
                    "sample": f"unavailable: {errs}"}
 
     launches = plan.kernel_launches(iters) * args.steps
+    job_rows = nglob if partitioned else world * n        # rows copied per step, whole job
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
@@ -664,21 +692,23 @@ def main():
             "scaling": "strong" if partitioned or world == 1 else "weak",
             "vs_baseline": None, "dtype": "f64",
             "data": "synthetic: reference 7-pt Poisson generator + default_rng(0).uniform(-1,1) RHS",
-            "config": {"workload": WORKLOAD, "n": n, "m": M, "iterations": iters,
+            # config: the workload identity only, key-for-key the reference arm's
+            "config": {"workload": WORKLOAD, "n": nglob, "m": M, "iterations": iters,
+                       "l2": L2_NOTE},
+            "details": {"rows_rank0": n,
                        "levels": cs.hierarchy.nlevels if cs.hierarchy is not None else 1,
                        "kernels_per_iteration": plan.kernels_per_iteration,
                        "parallelism": "single GPU" if world == 1 else (
                            f"{world}-GPU row partition + agglomeration, NCCL halo/allreduce"
                            if partitioned else f"{world} replicas (partitioned path failed: "
                                                f"{dist_error})"),
-                       "l2": "flushed (256 MB read) between timed steps, outside the events",
                        "setup_s_excluded": setup_s, "wall_s_timed_region": wall,
                        "iteration_algorithmic_bytes": plan.iteration_bytes,
                        "final_rel_residual_max": float(st.final_rel_residual.max())},
             "roofline": roof,
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": n * M * 8,
-                    "d2h_bytes_per_step": n * M * 8,
+            "e2e": {"value": e2e_val, "unit": UNIT, "h2d_bytes_per_step": job_rows * M * 8,
+                    "d2h_bytes_per_step": job_rows * M * 8,
                     "note": "public API run() on pinned host BlockVectors; H2D of B and D2H of "
                             "X inside the timed region", "max_abs_diff_vs_device_run": err},
             "gpu_launches": launches,

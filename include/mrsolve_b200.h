@@ -237,6 +237,13 @@ typedef struct mrs_comm mrs_comm;
 int  mrs_comm_unique_id(void* out128);                 /* ncclGetUniqueId */
 int  mrs_comm_create(const void* id128, int32_t rank, int32_t nranks, mrs_comm** out);
 void mrs_comm_destroy(mrs_comm* c);
+/* TEST-ONLY: nranks communicators of ONE process on ONE device joined by an
+ * in-process loopback transport (host barriers, stream events, D2D copies)
+ * instead of NCCL; out[r] = rank r's.  Each rank's plan is driven by its own
+ * host thread and stream in eager exec mode.  Lets the N-rank device path
+ * (pack kernel, halo offsets, split reductions, agglomeration all-gathers)
+ * run on one GPU; the product's GpuTeam never creates one. */
+int  mrs_comm_create_loopback(int32_t nranks, mrs_comm** out);
 int  mrs_plan_set_comm(mrs_plan* p, mrs_comm* c);      /* before set_halo / finalize */
 /* Level layout: replicated (agglomerated) levels hold every row; the first
  * replicated level after a partitioned one receives its restricted vector as
@@ -249,6 +256,11 @@ int  mrs_plan_set_layout(mrs_plan* p, int32_t l, int32_t replicated, int64_t sli
 int  mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend,
                        const int32_t* send_idx, const int32_t* send_counts,
                        const int32_t* recv_counts);
+
+/* Interior rows [ilo, ihi) of the consumer block of halo `which` (0 A_l,
+ * 1 R_l, 2 P_l): rows that read no halo column.  Their product runs while
+ * the exchange is in flight (knob "halo_overlap"); the rest after it. */
+int  mrs_plan_set_interior(mrs_plan* p, int32_t l, int32_t which, int64_t ilo, int64_t ihi);
 
 double mrs_plan_iteration_bytes(const mrs_plan* p);
 /* Warm per-launch device times (us) of one iteration body, each launch
@@ -292,6 +304,8 @@ const char* mrs_status_string(int32_t status);
 int  mrs_version(void);
 /* Tuning knobs, read when a plan captures its graph:
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
+ *   "halo_overlap" 0/1  multi-GPU: interior rows of a product run while its
+ *                   halo exchange is in flight (default 1)
  *   "spmm_long_rows" N  operators with <= N rows and >= 12 entries per row run the
  *                   SpMM with 16 entries in flight per lane (default 20000; 0: off)
  *   "coarse_rows" N  rows per CTA of the dense coarse solve (default 1)

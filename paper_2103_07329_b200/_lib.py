@@ -112,10 +112,12 @@ SIGNATURES = {
     "mrs_comm_unique_id": (C.c_int, [C.c_void_p]),
     "mrs_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
     "mrs_comm_destroy": (None, [C.c_void_p]),
+    "mrs_comm_create_loopback": (C.c_int, [C.c_int32, C.c_void_p]),
     "mrs_plan_set_comm": (C.c_int, [C.c_void_p, C.c_void_p]),
     "mrs_plan_set_layout": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64]),
     "mrs_plan_set_halo": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_void_p,
                                     C.c_void_p, C.c_void_p]),
+    "mrs_plan_set_interior": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int64, C.c_int64]),
 }
 
 

@@ -95,6 +95,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_split")) { set_spmm_long_split(value); return MRS_OK; }
+    if (!strcmp(key, "halo_overlap")) { set_halo_overlap(value); return MRS_OK; }
     if (!strcmp(key, "spmm_coop")) { set_spmm_coop(value); return MRS_OK; }
     if (!strcmp(key, "dense_mma")) { set_dense_mma(value); return MRS_OK; }
     if (!strcmp(key, "loop_unroll")) { set_loop_unroll(value); return MRS_OK; }

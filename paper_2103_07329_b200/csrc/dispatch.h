@@ -54,6 +54,8 @@ int64_t loop_unroll();
 void set_loop_unroll(int64_t v);
 void set_dense_mma(int64_t v);
 int64_t spmm_long_split();
+int64_t halo_overlap();
+void set_halo_overlap(int64_t v);
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;
 cudaError_t launch_sgs(const SgsArgs& a, int vb, int ib, cudaStream_t s);

@@ -39,6 +39,9 @@ void set_loop_unroll(int64_t v) { g_loop_unroll = v < 1 ? 1 : (v > 8 ? 8 : v); }
 static int64_t g_dense_mma = 1;       // FP64 tensor-core dense tail (dense_mma_kernel)
 bool dense_mma_enabled() { return g_dense_mma != 0; }
 void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }
+static int64_t g_halo_overlap = 1;    // multi-GPU: interior rows during the exchange
+int64_t halo_overlap() { return g_halo_overlap; }
+void set_halo_overlap(int64_t v) { g_halo_overlap = v ? 1 : 0; }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
@@ -55,7 +58,9 @@ int vec_grid(int64_t n, int64_t m) {
 
 cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream_t s,
                         bool generic) {
-    a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.nrows = A.nrows; a.m = m; a.nnz_hint = A.nnz;
+    a.rp = A.rp; a.ci = A.ci; a.vals = A.v; a.m = m; a.nnz_hint = A.nnz;
+    a.nrows = a.vrows ? a.vrows : A.nrows;       // split launches: the subset
+    a.rows_hint = A.nrows;
     a.ncols_hint = A.ncols;
     a.slab_base = A.slab_base;
     a.slab_shift = A.slab_shift;
@@ -64,7 +69,7 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
     a.n_long = spmm_long_split() ? A.n_long : 0;
     a.long_thr = A.long_thr;
     a.long_ctas = 0;
-    if (A.nrows == 0) return cudaSuccess;
+    if (a.nrows == 0) return cudaSuccess;
     // the SpMM engine indexes with 32 bits (rows, entries, element offsets)
     if ((A.nrows + 1) * m >= (int64_t)INT32_MAX || (A.ncols + 1) * m >= (int64_t)INT32_MAX ||
         A.nnz >= (int64_t)INT32_MAX)

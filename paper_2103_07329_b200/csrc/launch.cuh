@@ -90,12 +90,15 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         if (g < 1) g = 1;
         a.chunk = rpp * sp;
         if (generic) a.n_long = 0;                               // lane path only
-        a.long_ctas = a.n_long ? (int)std::min<int64_t>(a.n_long, 4LL * num_sms()) : 0;
+        a.long_ctas = (a.n_long && !a.no_long_ctas)
+                          ? (int)std::min<int64_t>(a.n_long, 4LL * num_sms()) : 0;
         (void)launch_ex_smem(kern, g + a.long_ctas,
                              a.long_ctas ? kLongProducts * sizeof(double) : 0, s, a);
     };
     // small operators with long rows: the LONG variant (16 entries in flight)
-    if (!generic && m <= 16 && a.nrows <= spmm_long_max_rows() && a.nnz_hint >= 12 * a.nrows) {
+    // variant choice by the whole operator's shape (rows_hint), not a split subset
+    const int64_t nr = a.rows_hint;
+    if (!generic && m <= 16 && nr <= spmm_long_max_rows() && a.nnz_hint >= 12 * nr) {
         switch (m) {
         case 1: go(spmm_kernel<1, OP, Tv, Ti, true>, Lay<1>::RPB); return cudaGetLastError();
         case 2: go(spmm_kernel<2, OP, Tv, Ti, true>, Lay<2>::RPB); return cudaGetLastError();
@@ -110,9 +113,9 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     // only long AND uniform rows (27-point stencils: mean >= 20, no row more
     // than ~10 % above it), where the warp-uniform trip count wastes nothing
     const int64_t coop = spmm_coop();
-    const bool uniform_long = a.nnz_hint >= 20 * a.nrows && a.max_row_hint > 0 &&
-                              (int64_t)a.max_row_hint * 10 * a.nrows <= 11 * a.nnz_hint + 10 * a.nrows;
-    if (!generic && ((coop == 1 && a.nnz_hint >= 12 * a.nrows) || (coop == 2 && uniform_long))) {
+    const bool uniform_long = a.nnz_hint >= 20 * nr && a.max_row_hint > 0 &&
+                              (int64_t)a.max_row_hint * 10 * nr <= 11 * a.nnz_hint + 10 * nr;
+    if (!generic && ((coop == 1 && a.nnz_hint >= 12 * nr) || (coop == 2 && uniform_long))) {
         switch (m) {
         case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB); return cudaGetLastError();
         case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB); return cudaGetLastError();

@@ -60,6 +60,9 @@ struct LevelDev {
     bool sgs = false;
 };
 
+// halo/compute overlap only where the interior run is worth a second launch
+constexpr int64_t kMinOverlapRows = 2048;
+
 template <typename T> T* dalloc(size_t n, std::vector<void*>& owned) {
     void* p = nullptr;
     if (n == 0) n = 1;
@@ -76,6 +79,9 @@ struct mrs_plan {
     std::vector<LevelDev> L;
     mrs_comm* comm = nullptr;  // multi-GPU: NCCL communicator (dist = set)
     bool dist = false;
+    bool overlap = true;       // halo exchange overlapped with interior rows
+    cudaStream_t cstream = nullptr;            // communication stream (dist)
+    cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
     double* inv = nullptr;
     int64_t nc = 0;
     const int* body_guard = nullptr;   // capture of unrolled loop-body copies (&st->stop)
@@ -134,6 +140,9 @@ struct mrs_plan {
             if (body_graph[i]) cudaGraphDestroy(body_graph[i]);
         }
         if (stop_host) cudaFreeHost(stop_host);
+        if (cstream) cudaStreamDestroy(cstream);
+        if (ev_pack) cudaEventDestroy(ev_pack);
+        if (ev_comm) cudaEventDestroy(ev_comm);
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
         for (void* p : owned) cudaFree(p);
@@ -176,7 +185,9 @@ struct Builder {
 
     // multi-GPU: exchange the halo rows of a gathered operand before its use
     void exchange(const Halo* h, const double* x) {
-        if (!P->dist || !h || !h->active()) return;
+        // (the test-only loopback transport joins every exchange, active or not:
+        // its collectives are barriers of all ranks)
+        if (!P->dist || !h || (!h->active() && !P->comm->loop)) return;
         const Halo* hh = h;
         const mrs_comm* c = P->comm;
         const int64_t m = P->m;
@@ -192,7 +203,7 @@ struct Builder {
         r.epi = EPI_NONE;
         return -epi - 1;   // marker: post-kernel allreduce + epilogue needed
     }
-    void post_reduction(int marker, int Km) {
+    void post_reduction(int marker, int Km, int nsets = 1) {
         if (marker >= 0) return;
         const int epi = -marker - 1;
         double* buf = P->red_out;
@@ -200,18 +211,66 @@ struct Builder {
         SolveState* st = P->st;
         const int m = (int)P->m;
         const int* g = guard;
-        out->push_back([=](cudaStream_t s) { return allreduce_sum(buf, Km, c, s); });
-        out->push_back([=](cudaStream_t s) { return launch_epilogue(st, buf, Km, m, epi, g, s); });
+        out->push_back([=](cudaStream_t s) { return allreduce_sum(buf, nsets * Km, c, s); });
+        out->push_back([=](cudaStream_t s) {
+            return launch_epilogue(st, buf, Km, m, epi, g, s, nsets);
+        });
+    }
+    // multi-GPU with halo/compute overlap: the rows that read no halo column
+    // run while the exchange is in flight on the plan's communication stream
+    bool overlapped(const DevCsr& A) const {
+        const Halo* h = A.halo;
+        if (!P->dist || !P->overlap || !h || !(h->active() || P->comm->loop)) return false;
+        return h->ihi - h->ilo >= kMinOverlapRows && h->ihi <= A.nrows;
     }
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
         int64_t m = P->m;
-        exchange(A.halo, a.x);
-        const int mk = a.dot ? split_reduction(a.red) : 0;
-        out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
-        if (a.dot) post_reduction(mk, (int)m);
+        if (overlapped(A)) {
+            spmm_overlapped(op, A, a);
+        } else {
+            exchange(A.halo, a.x);
+            const int mk = a.dot ? split_reduction(a.red) : 0;
+            out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
+            if (a.dot) post_reduction(mk, (int)m);
+            kernels++;
+        }
         bytes += A.bytes() + extra_bytes;
-        kernels++;
+    }
+    // pack (compute stream) -> transfer (comm stream) || interior rows
+    // (compute stream) -> join -> boundary rows.  Every row is computed by
+    // exactly one launch in its own entry order: results are those of the
+    // unsplit product.  A fused dot leaves one partial set per launch; both
+    // sets are all-reduced and summed in set order by the epilogue.
+    void spmm_overlapped(int op, const DevCsr& A, SpArgs a) {
+        const Halo* h = A.halo;
+        const mrs_comm* c = P->comm;
+        const int64_t m = P->m;
+        double* xx = const_cast<double*>(a.x);
+        const int* g = guard;
+        cudaStream_t cs = P->cstream;
+        cudaEvent_t ev_pack = P->ev_pack, ev_comm = P->ev_comm;
+        out->push_back([=](cudaStream_t s) -> cudaError_t {
+            cudaError_t e = halo_pack(*h, xx, m, g, s);
+            if (e == cudaSuccess) e = cudaEventRecord(ev_pack, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(cs, ev_pack, 0);
+            if (e == cudaSuccess) e = halo_transfer(*h, xx, m, c, cs);
+            if (e == cudaSuccess) e = cudaEventRecord(ev_comm, cs);
+            return e;
+        });
+        const int mk = a.dot ? split_reduction(a.red) : 0;
+        const int ilo = (int)h->ilo, ihi = (int)h->ihi, n = (int)A.nrows;
+        SpArgs ai = a, ab = a;
+        ai.row_base = ilo; ai.row_split = 0x7fffffff; ai.row_gap = 0; ai.vrows = ihi - ilo;
+        ai.no_long_ctas = 1;
+        ab.row_base = 0; ab.row_split = ilo; ab.row_gap = ihi - ilo;
+        ab.vrows = n - (ihi - ilo);
+        if (a.dot) ab.red.out = a.red.out + m;          // second partial set
+        out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, ai, m, s); });
+        out->push_back([=](cudaStream_t s) { return cudaStreamWaitEvent(s, ev_comm, 0); });
+        out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, ab, m, s); });
+        if (a.dot) post_reduction(mk, (int)m, 2);
+        kernels += 2;
     }
     void vec(int op, VArgs a, double b) {
         a.guard = a.guard ? a.guard : guard;
@@ -856,6 +915,19 @@ void build_program(mrs_plan* P, bool x_zero, Program& pg) {
     }
 }
 
+// Exec mode 2 (distributed): one host-launched graph carries kDistUnroll
+// iterations; each copy starts with this gate, which turns a stop taken in
+// an earlier copy into skip flags for every kernel of this copy (the host
+// checks stop once per graph launch).
+constexpr int kDistUnroll = 4;
+__global__ void gate_kernel(SolveState* st) {
+    if (st->stop) {
+        st->skip = 1;
+        st->pskip = 1;
+        st->nodrift = 1;
+    }
+}
+
 __global__ void set_cond_kernel(SolveState* st, cudaGraphConditionalHandle h, int has) {
     st->has_cond = has;
     st->cond = h;
@@ -1252,6 +1324,12 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     hs.nodrift = 1;
     for (int c = 0; c < kMaxM; ++c) { hs.one[c] = 1.0; hs.neg_one[c] = -1.0; }
     MRS_CUDA_OK(cudaMemcpy(p->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
+    p->overlap = halo_overlap() != 0;
+    if (p->dist) {
+        MRS_CUDA_OK(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
+        MRS_CUDA_OK(cudaEventCreateWithFlags(&p->ev_pack, cudaEventDisableTiming));
+        MRS_CUDA_OK(cudaEventCreateWithFlags(&p->ev_comm, cudaEventDisableTiming));
+    }
     MRS_CUDA_OK(cudaMallocHost(&p->st_host, sizeof(SolveState)));
     MRS_CUDA_OK(cudaMallocHost(&p->hist_host, sizeof(double) * (size_t)(p->desc.max_iters + 1) * m));
     MRS_CUDA_OK(cudaEventCreate(&p->ev0));
@@ -1336,7 +1414,12 @@ int mrs_plan_solve(mrs_plan* p, const double* B, double* X, int32_t x_is_zero,
             cudaStream_t cs;
             MRS_CUDA_OK(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
             MRS_CUDA_OK(cudaStreamBeginCapture(cs, cudaStreamCaptureModeRelaxed));
-            cudaError_t e = run_list(pg.body, cs);
+            cudaError_t e = cudaSuccess;
+            for (int u = 0; u < kDistUnroll && e == cudaSuccess; ++u) {
+                gate_kernel<<<1, 1, 0, cs>>>(p->st);
+                e = cudaGetLastError();
+                if (e == cudaSuccess) e = run_list(pg.body, cs);
+            }
             cudaGraph_t g = nullptr;
             cudaError_t e2 = cudaStreamEndCapture(cs, &g);
             cudaStreamDestroy(cs);
@@ -1438,6 +1521,18 @@ int mrs_plan_set_halo(mrs_plan* p, int32_t l, int32_t which, int64_t nsend, cons
         if (!h.send_idx) return MRS_ERR_ALLOC;
         MRS_CUDA_OK(cudaMemcpy(h.send_idx, send_idx, (size_t)ns * 4, cudaMemcpyHostToDevice));
     }
+    return MRS_OK;
+}
+
+int mrs_plan_set_interior(mrs_plan* p, int32_t l, int32_t which, int64_t ilo, int64_t ihi) {
+    if (!p || !p->comm || l < 0 || l >= (int)p->L.size() || which < 0 || which > 2 || ilo < 0 ||
+        ihi < ilo)
+        return MRS_ERR_ARG;
+    if (p->finalized) return MRS_ERR_STATE;
+    LevelDev& lv = p->L[l];
+    Halo& h = which == 0 ? lv.hA : (which == 1 ? lv.hR : lv.hP);
+    h.ilo = ilo;
+    h.ihi = ihi;
     return MRS_OK;
 }
 

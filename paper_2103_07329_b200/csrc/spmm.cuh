@@ -80,8 +80,21 @@ struct SpArgs {
     const int32_t* long_rows;  // rows with more than long_thr entries (one CTA each)
     int n_long, long_thr, long_ctas;   // long_ctas: trailing CTAs of the grid doing them
     int max_row_hint;          // longest row (0: unknown) -- layout choice
+    // row subset of a split launch (multi-GPU halo overlap): the kernel walks
+    // virtual rows v < nrows and works on row_base + v (+ row_gap once
+    // v >= row_split); all zero = every row.  vrows: the subset's row count
+    // (0 = the matrix's).  no_long_ctas: this launch leaves the long rows to
+    // the other launch of the split (the lane path still skips them).
+    int row_base, row_split, row_gap, no_long_ctas;
+    int64_t vrows;
+    int64_t rows_hint;      // the operator's row count (variant choice)
     RedArgs red;
 };
+
+// Physical row of virtual row v (split launches; identity otherwise).
+__device__ __forceinline__ int phys_row(const SpArgs& a, int v) {
+    return a.row_base + v + (v >= a.row_split ? a.row_gap : 0);
+}
 // shared-memory products per chunk of a long row (long_row_cta)
 constexpr int kLongProducts = 2048;
 
@@ -469,9 +482,10 @@ spmm_kernel(SpArgs a) {
         for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
             const int r1 = min(r0 + chunk, nrows);
             for (int rb = r0; rb < r1; rb += RPB) {            // warp-uniform passes
-                const int row = rb + threadIdx.x / LPR;
+                const int v = rb + threadIdx.x / LPR;
+                const int row = phys_row(a, v);
                 int lo = 0, len = 0;
-                bool live = row < r1;
+                bool live = v < r1;
                 if (live) {
                     lo = __ldg(a.rp + row);
                     len = __ldg(a.rp + row + 1) - lo;
@@ -491,7 +505,8 @@ spmm_kernel(SpArgs a) {
         const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
         for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
             const int r1 = min(r0 + chunk, nrows);
-            for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB) {
+            for (int v = r0 + threadIdx.x / LPR; v < r1; v += RPB) {
+                const int row = phys_row(a, v);
                 const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
                 if (hi - lo > lthr) continue;            // done by a long-row CTA
                 do_row<OP, CPL, GSrc<Tv, Ti>, LONG ? 16 : L::UNR>(a, src.at_row(a, row), row, lo, hi,
@@ -517,9 +532,11 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
         const int nrows = (int)a.nrows, chunk = (int)a.chunk;
         for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gridDim.x * chunk) {
             const int r1 = min(r0 + chunk, nrows);
-            for (int row = r0 + threadIdx.x / m; row < r1; row += rpb)
+            for (int v = r0 + threadIdx.x / m; v < r1; v += rpb) {
+                const int row = phys_row(a, v);
                 do_row<OP, 1>(a, src.at_row(a, row), row, __ldg(a.rp + row), __ldg(a.rp + row + 1), m,
                               c, dotp);
+            }
         }
     }
     {

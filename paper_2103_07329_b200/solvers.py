@@ -139,6 +139,9 @@ class DevicePlan:
                             h, l, which, hp.nsend, hp.send_idx.ctypes.data,
                             hp.send_counts.ctypes.data, hp.recv_counts.ctypes.data),
                             f"halo level {l}/{which}")
+                    for which, (ilo, ihi) in getattr(lay, "interior", {}).items():
+                        _lib.check(self.L.mrs_plan_set_interior(h, l, which, ilo, ihi),
+                                   f"interior rows level {l}/{which}")
             for l, (A, P, R, bounds) in enumerate(levels):
                 keep: list = []
                 sl = DevicePlan.compress_indices

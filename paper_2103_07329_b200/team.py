@@ -100,6 +100,29 @@ def localize(blk: CsrBlock, rows: tuple, cols: tuple, col_ranges: list | None):
     return local, halo, recv
 
 
+def interior_range(local: CsrBlock, nown: int) -> tuple:
+    """Longest run [ilo, ihi) of rows of a localized block that read no halo
+    column (local column >= nown).  Their product can run while the halo
+    exchange is in flight; the other rows run after it (csrc/solver.cu
+    spmm_overlapped).  For a z-slab partition of a stencil these are all rows
+    but the first and last planes."""
+    n = local.nrows
+    if n == 0:
+        return (0, 0)
+    rp = np.asarray(local.row_ptr, dtype=np.int64)
+    halo_entry = np.asarray(local.col_idx).astype(np.int64) >= nown
+    cum = np.concatenate([[0], np.cumsum(halo_entry, dtype=np.int64)])
+    boundary = (cum[rp[1:]] - cum[rp[:-1]]) > 0
+    if not boundary.any():
+        return (0, n)
+    # runs of interior rows between boundary rows
+    idx = np.flatnonzero(boundary)
+    starts = np.concatenate([[0], idx + 1])
+    ends = np.concatenate([idx, [n]])
+    k = int(np.argmax(ends - starts))
+    return (int(starts[k]), int(ends[k]))
+
+
 def halo_plan(blk: CsrBlock, row_ranges: list, col_ranges: list, rank: int) -> HaloPlan:
     """My exchange for operand products of `blk`: rows each peer imports from
     me (in its halo order) and my receive counts."""
@@ -128,6 +151,7 @@ class LevelLayout:
     P: CsrBlock | None = None
     R: CsrBlock | None = None
     halos: dict = field(default_factory=dict)      # 0: A, 1: R, 2: P -> HaloPlan
+    interior: dict = field(default_factory=dict)   # 0/1/2 -> (ilo, ihi) rows without halo reads
     slice: tuple = (0, 0)          # agglomeration: (row0, rows) of my restricted slice
 
 
@@ -162,6 +186,8 @@ def plan_levels(levels: list, rank: int, world: int, agg_rows_per_rank: int = 16
         lay = LevelLayout(rr[rank], False)
         lay.A, _, _ = localize(A, rr[rank], rr[rank], rr)
         lay.halos[0] = halo_plan(A, rr, rr, rank)
+        nown = rr[rank][1] - rr[rank][0]
+        lay.interior[0] = interior_range(lay.A, nown)
         if P is not None:
             if repl[l + 1]:
                 # agglomeration: R restricts my slice of the (replicated) coarse
@@ -169,6 +195,7 @@ def plan_levels(levels: list, rank: int, world: int, agg_rows_per_rank: int = 16
                 sl, q = equal_slices(n[l + 1], world)
                 lay.R, _, _ = localize(R, sl[rank], rr[rank], rr)
                 lay.halos[1] = halo_plan(R, sl, rr, rank)
+                lay.interior[1] = interior_range(lay.R, nown)
                 lay.P, _, _ = localize(P, rr[rank], (0, n[l + 1]), None)
                 out_slice = (sl[rank][0], q)
             else:
@@ -177,6 +204,8 @@ def plan_levels(levels: list, rank: int, world: int, agg_rows_per_rank: int = 16
                 lay.halos[1] = halo_plan(R, rc, rr, rank)
                 lay.P, _, _ = localize(P, rr[rank], rc[rank], rc)
                 lay.halos[2] = halo_plan(P, rr, rc, rank)
+                lay.interior[1] = interior_range(lay.R, nown)
+                lay.interior[2] = interior_range(lay.P, rc[rank][1] - rc[rank][0])
                 out_slice = None
             lay._next_slice = out_slice
         out.append(lay)
