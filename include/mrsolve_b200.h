@@ -304,8 +304,9 @@ const char* mrs_status_string(int32_t status);
 int  mrs_version(void);
 /* Tuning knobs, read when a plan captures its graph:
  *   "pdl"       0/1   programmatic dependent launch of the solve-path kernels
- *   "halo_overlap" 0/1  multi-GPU: interior rows of a product run while its
- *                   halo exchange is in flight (default 1)
+ *   "halo_overlap" 0/1/2  multi-GPU: interior rows of a product run while its
+ *                   halo exchange is in flight (default 1; 2 = test mode: every
+ *                   product with an interior range, halo or not, any size)
  *   "spmm_long_rows" N  operators with <= N rows and >= 12 entries per row run the
  *                   SpMM with 16 entries in flight per lane (default 20000; 0: off)
  *   "coarse_rows" N  rows per CTA of the dense coarse solve (default 1)

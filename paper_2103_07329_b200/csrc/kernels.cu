@@ -41,7 +41,7 @@ bool dense_mma_enabled() { return g_dense_mma != 0; }
 void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }
 static int64_t g_halo_overlap = 1;    // multi-GPU: interior rows during the exchange
 int64_t halo_overlap() { return g_halo_overlap; }
-void set_halo_overlap(int64_t v) { g_halo_overlap = v ? 1 : 0; }
+void set_halo_overlap(int64_t v) { g_halo_overlap = v < 0 ? 0 : (v > 2 ? 2 : v); }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }

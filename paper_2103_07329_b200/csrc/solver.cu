@@ -79,7 +79,7 @@ struct mrs_plan {
     std::vector<LevelDev> L;
     mrs_comm* comm = nullptr;  // multi-GPU: NCCL communicator (dist = set)
     bool dist = false;
-    bool overlap = true;       // halo exchange overlapped with interior rows
+    int overlap = 1;           // halo exchange overlapped with interior rows (knob)
     cudaStream_t cstream = nullptr;            // communication stream (dist)
     cudaEvent_t ev_pack = nullptr, ev_comm = nullptr;
     double* inv = nullptr;
@@ -218,10 +218,14 @@ struct Builder {
     }
     // multi-GPU with halo/compute overlap: the rows that read no halo column
     // run while the exchange is in flight on the plan's communication stream
+    // (knob halo_overlap: 0 off, 1 on, 2 = test mode: every product with an
+    // interior range, with or without a halo, whatever its size)
     bool overlapped(const DevCsr& A) const {
         const Halo* h = A.halo;
-        if (!P->dist || !P->overlap || !h || !(h->active() || P->comm->loop)) return false;
-        return h->ihi - h->ilo >= kMinOverlapRows && h->ihi <= A.nrows;
+        if (!P->dist || P->overlap == 0 || !h) return false;
+        if (P->overlap == 1 && !(h->active() || P->comm->loop)) return false;
+        const int64_t min_rows = P->overlap == 2 ? 1 : kMinOverlapRows;
+        return h->ihi - h->ilo >= min_rows && h->ihi <= A.nrows;
     }
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
@@ -232,7 +236,18 @@ struct Builder {
             exchange(A.halo, a.x);
             const int mk = a.dot ? split_reduction(a.red) : 0;
             out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
-            if (a.dot) post_reduction(mk, (int)m);
+            if (a.dot && mk < 0 && P->overlap) {
+                // the reduction has the shape of a split product on every rank
+                // (whether a rank splits depends on its own interior range):
+                // an empty second partial set
+                double* set1 = P->red_out + m;
+                out->push_back([=](cudaStream_t s) {
+                    return cudaMemsetAsync(set1, 0, sizeof(double) * m, s);
+                });
+                post_reduction(mk, (int)m, 2);
+            } else if (a.dot) {
+                post_reduction(mk, (int)m);
+            }
             kernels++;
         }
         bytes += A.bytes() + extra_bytes;
@@ -260,6 +275,19 @@ struct Builder {
         });
         const int mk = a.dot ? split_reduction(a.red) : 0;
         const int ilo = (int)h->ilo, ihi = (int)h->ihi, n = (int)A.nrows;
+        if (ihi - ilo == n) {            // no boundary rows: one launch after the join
+            out->push_back([=](cudaStream_t s) { return cudaStreamWaitEvent(s, ev_comm, 0); });
+            out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
+            if (a.dot && mk < 0) {
+                double* set1 = P->red_out + m;
+                out->push_back([=](cudaStream_t s) {
+                    return cudaMemsetAsync(set1, 0, sizeof(double) * m, s);
+                });
+                post_reduction(mk, (int)m, 2);
+            }
+            kernels++;
+            return;
+        }
         SpArgs ai = a, ab = a;
         ai.row_base = ilo; ai.row_split = 0x7fffffff; ai.row_gap = 0; ai.vrows = ihi - ilo;
         ai.no_long_ctas = 1;
@@ -855,7 +883,8 @@ void build_stationary(mrs_plan* P, bool x_zero, Program& pg) {
         b.dot(P->r, P->r, n, EPI_RNORM_INIT);
     }
     {
-        Builder b{P, &pg.body, nullptr};
+        // guarded by skip: a no-op once a gate (exec mode 2) saw the stop flag
+        Builder b{P, &pg.body, &P->st->skip};
         LevelDev& lv = P->L[0];
         // the step runs on a NONZERO x: on the zero first guess this is the
         // reference's zero-flag short-cut value (0 + w*(b/d) == w*(b/d), ...)
@@ -1324,7 +1353,7 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     hs.nodrift = 1;
     for (int c = 0; c < kMaxM; ++c) { hs.one[c] = 1.0; hs.neg_one[c] = -1.0; }
     MRS_CUDA_OK(cudaMemcpy(p->st, &hs, sizeof(hs), cudaMemcpyHostToDevice));
-    p->overlap = halo_overlap() != 0;
+    p->overlap = (int)halo_overlap();
     if (p->dist) {
         MRS_CUDA_OK(cudaStreamCreateWithFlags(&p->cstream, cudaStreamNonBlocking));
         MRS_CUDA_OK(cudaEventCreateWithFlags(&p->ev_pack, cudaEventDisableTiming));

@@ -112,3 +112,36 @@ def test_team_of_one_other_families(roles):
     assert sd.iterations == ss.iterations
     np.testing.assert_array_equal(Xd.data, Xs.data)
     team.close()
+
+
+@pytest.mark.parametrize("name", ["amg_pcg", "amg_bicgstab_mixed", "amg_pbicgstab"])
+def test_team_of_one_split_products_in_captured_graphs(name, monkeypatch):
+    """The halo/compute overlap as the product captures it (exec mode 2: the
+    body graph holds 4 gated iterations, the exchange on the communication
+    stream joined back by events): with one rank there is no halo, so the
+    test mode of the knob forces the split on a shrunken interior range --
+    interior rows, then boundary rows, two partial dot sets.  Same iterations,
+    X to roundoff (the split dot sums two partial sets)."""
+    from paper_2103_07329_b200 import _lib, amg, team as T
+    monkeypatch.setattr(amg, "DENSE_TAIL_ROWS", 0)
+    monkeypatch.setattr(T, "interior_range", lambda blk, nown: (blk.nrows // 4,
+                                                                 3 * blk.nrows // 4))
+    A, _ = gen_poisson3d(14, 13, 12)
+    B = np.random.default_rng(5).uniform(-1, 1, (A.nrows, 4))
+    roles = CASES[name]
+    Xs = BlockVector.zeros(A.nrows, 4)
+    ss = prepare(tree(roles), A).run(BlockVector.from_array(B), Xs)
+    _lib.set_option("halo_overlap", 2)
+    try:
+        team = GpuTeam(agg_rows_per_rank=1)
+        cs = prepare(tree(roles), A, team=team)
+        assert cs.layouts[0].interior[0] == (A.nrows // 4, 3 * A.nrows // 4)
+        Xd = BlockVector.zeros(A.nrows, 4)
+        sd = cs.run(BlockVector.from_array(B), Xd)
+        sd2 = cs.run(BlockVector.from_array(B), BlockVector.zeros(A.nrows, 4))   # graph replay
+    finally:
+        _lib.set_option("halo_overlap", 1)
+    assert sd.iterations == ss.iterations == sd2.iterations and sd.all_converged
+    err = np.abs(Xd.data - Xs.data).max() / np.abs(Xs.data).max()
+    assert err <= 1e-11, err
+    team.close()
