@@ -268,15 +268,12 @@ class GpuTeam:
             pass
 
 
-def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: str = "graph",
-                        eig_bounds=None):
-    """``prepare`` on a team: every rank builds the (identical, deterministic)
-    global hierarchy, keeps its local blocks and uploads them.  ``run(B, X)``
-    takes THIS rank's rows of B and X (``team.row_range(n)``)."""
-    from .solvers import ConfiguredSolver, DevicePlan, _configure, _vector_args
-    from .errors import ShapeMismatchError
-    cfg = _configure(config, A, hierarchy, exec_mode, eig_bounds)
-    desc, levels, inv, h, name, Ab = cfg
+def _torch_dist():
+    import torch.distributed as dist
+    return dist if (dist.is_available() and dist.is_initialized()) else None
+
+
+def _check_team_config(desc):
     if _lib.PC_SGS == desc.precond or _lib.SMOOTH_SGS in (
             (desc.pre.kind, desc.post.kind) if desc.precond == _lib.PC_MG else ()):
         # the reference's hybrid sweep couples leaves through the pre-sweep
@@ -284,15 +281,76 @@ def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: 
         raise ConfigurationError("Gauss-Seidel smoothing is single-GPU only on the device path")
     if desc.method == _lib.METHOD_DIRECT:
         raise ConfigurationError("the Direct solver (dense inverse) is single-GPU only")
+
+
+def _rank_payload(cfg, glob, rank, team):
+    """Everything rank `rank` uploads: plan descriptor, its layouts (local
+    blocks + halo plans + interior ranges), per-level Chebyshev bounds, the
+    coarse operators, the method name."""
+    desc, levels, inv, h, name, Ab = cfg
+    lays = plan_levels(glob, rank, team.world_size, team.agg_rows_per_rank,
+                       team.force_replicate_from)
+    return {"desc": bytes(desc), "lays": lays, "bounds": [lv[3] for lv in levels],
+            "inv": inv, "name": name, "nlevels": len(levels)}
+
+
+def _scatter_setup(config, A, team, hierarchy, exec_mode, eig_bounds, dist):
+    """One setup for the whole team: rank 0 builds the hierarchy, the coarse
+    operators and every rank's local blocks, and sends each rank ONLY its own
+    (torch.distributed point-to-point object messages, one rank at a time, so
+    rank 0 never holds more than one foreign payload).  Other ranks keep host
+    memory proportional to their rows.  A setup error on rank 0 is re-raised
+    on every rank."""
+    from .solvers import _configure
+    if team.rank == 0:
+        payload, err = None, None
+        try:
+            cfg = _configure(config, A, hierarchy, exec_mode, eig_bounds)
+            _check_team_config(cfg[0])
+            glob = [(lv[0], lv[1], lv[2]) for lv in cfg[1]]
+        except Exception as e:          # sent to the other ranks, raised everywhere
+            err = e
+        for r in range(1, team.world_size):
+            msg = [err if err is not None else _rank_payload(cfg, glob, r, team)]
+            dist.send_object_list(msg, dst=r)
+        if err is not None:
+            raise err
+        payload = _rank_payload(cfg, glob, 0, team)
+        return payload, cfg[3]
+    msg = [None]
+    dist.recv_object_list(msg, src=0)
+    if isinstance(msg[0], Exception):
+        raise msg[0]
+    return msg[0], None
+
+
+def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: str = "graph",
+                        eig_bounds=None):
+    """``prepare`` on a team.  With a torch.distributed world the setup runs
+    ONCE, on rank 0, which sends every rank its own local blocks
+    (:func:`_scatter_setup`); without one (a 1-rank team, the test-only
+    loopback ranks) each rank derives its blocks from the same deterministic
+    global setup.  ``run(B, X)`` takes THIS rank's rows of B and X
+    (``team.row_range(n)``)."""
+    from .solvers import ConfiguredSolver, DevicePlan, _configure, _vector_args
+    from .errors import ShapeMismatchError
+    dist = _torch_dist()
+    if dist is not None and team.world_size > 1:
+        payload, h = _scatter_setup(config, A, team, hierarchy, exec_mode, eig_bounds, dist)
+        desc = _lib.mrs_plan_desc.from_buffer_copy(payload["desc"])
+    else:
+        cfg = _configure(config, A, hierarchy, exec_mode, eig_bounds)
+        _check_team_config(cfg[0])
+        glob = [(lv[0], lv[1], lv[2]) for lv in cfg[1]]
+        payload = _rank_payload(cfg, glob, team.rank, team)
+        desc, h = cfg[0], cfg[3]
+    lays, inv, name = payload["lays"], payload["inv"], payload["name"]
     if exec_mode == "graph":
         # NCCL p2p/collectives are captured into one ordinary graph per
-        # iteration (host checks convergence between launches) rather than
+        # 4 iterations (host checks convergence between launches) rather than
         # into a conditional-node body
         desc.exec = 2
-    glob = [(lv[0], lv[1], lv[2]) for lv in levels]
-    lays = plan_levels(glob, team.rank, team.world_size, team.agg_rows_per_rank,
-                       team.force_replicate_from)
-    local_levels = [(lay.A, lay.P, lay.R, levels[l][3]) for l, lay in enumerate(lays)]
+    local_levels = [(lay.A, lay.P, lay.R, payload["bounds"][l]) for l, lay in enumerate(lays)]
     lo, hi = lays[0].rows
     desc.nrows = hi - lo
     plans: dict = {}
@@ -319,4 +377,5 @@ def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: 
     cs = ConfiguredSolver(name, run, h, plan_for)
     cs.layouts = lays
     cs.row_range = (lo, hi)
+    cs.nlevels = payload["nlevels"]
     return cs

@@ -169,3 +169,64 @@ def test_slab_compress_roundtrip_and_bandwidth_limit():
     from mrs_testutil import random_csr
     R = random_csr(70001, 70001, 8.0, rng)
     assert slab_compress(R.row_ptr, R.col_idx.astype(np.uint32)) is None
+
+
+def _setup_worker(rank, world, port, ret):
+    """prepare() on a gloo world: rank 0 sets up, every rank receives only its
+    own layouts; they equal what the rank would derive from the global setup."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_07329_b200 import amg as amg_mod
+        from paper_2103_07329_b200.params import tree
+        from paper_2103_07329_b200.solvers import prepare
+        from paper_2103_07329_b200.team import GpuTeam
+        calls = []
+        real = amg_mod.setup
+
+        def counting_setup(*a, **k):
+            calls.append(1)
+            return real(*a, **k)
+        import paper_2103_07329_b200.solvers as S
+        S.amg_setup = counting_setup
+        A = gen_poisson3d(20, 18, 16)[0]
+        roles = {"solver": {"method": "CG"}, "preconditioner": {"method": "MultiGrid"},
+                 "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+                 "post_smoother": {"method": "Jacobi", "weight": "0.8"}}
+        team = GpuTeam(agg_rows_per_rank=800)
+        cs = prepare(tree(roles), A, team=team)
+        h = real(A)
+        want = plan_levels([(lv.A, lv.P, lv.R) for lv in h.levels], rank, world, 800)
+        ok = len(want) == len(cs.layouts) == cs.nlevels
+        for a, b in zip(want, cs.layouts):
+            ok &= a.rows == b.rows and a.replicated == b.replicated and a.slice == b.slice
+            ok &= a.interior == b.interior
+            for tag in ("A", "P", "R"):
+                x, y = getattr(a, tag), getattr(b, tag)
+                ok &= (x is None) == (y is None)
+                if x is not None:
+                    ok &= np.array_equal(x.row_ptr, y.row_ptr) and np.array_equal(
+                        x.col_idx, y.col_idx) and np.array_equal(x.values, y.values)
+            for w, hp in a.halos.items():
+                ok &= np.array_equal(hp.send_idx, b.halos[w].send_idx)
+                ok &= np.array_equal(hp.recv_counts, b.halos[w].recv_counts)
+        # a configuration error on rank 0 is raised on every rank
+        from paper_2103_07329_b200.errors import ConfigurationError
+        bad = {"solver": {"method": "Direct"}}
+        raised = False
+        try:
+            prepare(tree(bad), A, team=team)
+        except ConfigurationError:
+            raised = True
+        ret[rank] = (bool(ok), len(calls), cs.hierarchy is not None, raised)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_one_setup_for_all_ranks_gloo_world2():
+    world = 2
+    ctx = mp.get_context("spawn")
+    ret = ctx.Manager().dict()
+    mp.spawn(_setup_worker, args=(world, _free_port(), ret), nprocs=world, join=True)
+    assert ret[0] == (True, 1, True, True), ret[0]       # rank 0: the one setup
+    assert ret[1] == (True, 0, False, True), ret[1]      # rank 1: no setup, own blocks only
