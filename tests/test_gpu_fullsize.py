@@ -45,8 +45,14 @@ ROLES = {
            "preconditioner": {"method": "MultiGrid", "mg_mixed_precision": "1"},
            "pre_smoother": CHEB, "post_smoother": CHEB},
     "c4_24": AMG_PCG, "c4_32": AMG_PCG, "c4_64": AMG_PCG, "c4_128": AMG_PCG,
+    "c4_256": AMG_PCG,          # BASELINE config 4 at full size (449 M nnz, 17 levels)
 }
 CASES = [c for c in ROLES if os.path.exists(os.path.join(GOLDEN, f"full_{c}.npz"))]
+
+
+def _sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()[:32]
 
 
 def _matrix(g):
@@ -63,7 +69,19 @@ def test_full_size_solve_vs_reference(name):
     m = int(g["m"])
     B = np.random.default_rng(int(g["seed"])).uniform(-1.0, 1.0, (A.nrows, m))
     X = BlockVector.zeros(A.nrows, m)
-    st = prepare(tree(ROLES[name]), A).run(BlockVector.from_array(B), X)
+    cs = prepare(tree(ROLES[name]), A)
+    # the uploaded hierarchy is the reference's, level by level (SHA-256 of
+    # row_ptr / col_idx / values of A, P, R)
+    if "nlevels" in g.files:
+        assert cs.hierarchy.nlevels == int(g["nlevels"])
+        for l, lv in enumerate(cs.hierarchy.levels):
+            for tag in ("A", "P", "R"):
+                blk = getattr(lv, tag)
+                if blk is not None:
+                    got = [_sha(blk.row_ptr.astype(np.int64)),
+                           _sha(blk.col_idx.astype(np.int64)), _sha(blk.values)]
+                    assert got == list(g[f"L{l}_{tag}_sha"]), (name, l, tag)
+    st = cs.run(BlockVector.from_array(B), X)
     it_ref = int(g["iters"])
     assert abs(st.iterations - it_ref) <= 1, (st.iterations, it_ref)
     assert st.all_converged and np.all(st.final_rel_residual <= 1e-8)
