@@ -1,14 +1,14 @@
 """Parity at BASELINE.json's full sizes, against the reference's own outputs.
 
 * C1 / C2 / C3 at full size and the C4 operator family (27-point anisotropic,
-  24^3 .. 128^3): the device solve vs the reference run on the same seeded
+  24^3 .. 256^3, the last = BASELINE config 4): the device solve vs the reference run on the same seeded
   inputs (tests/golden/full_<case>.npz, written by oracle/gen_golden.py
   ``fullsize`` with the reference itself): iterations within +-1 (north
   star), every column's final relative residual <= tol, the strided X sample
   within 1e-6 of the reference's relative to the column's max, the residual
-  history within 1e-5 relative over the common iterations.  The hierarchy
-  the device uploads is the reference's bitwise
-  (tests/test_fullsize_hierarchy.py).
+  history within 1e-5 relative over the common iterations; the hierarchy the
+  device uploads hashes equal to the reference's, level by level (also on
+  CPU: tests/test_fullsize_golden.py).
 * C5 (n = 2^22, ~67 M entries): the device SpMM (slab-compressed 16-bit and
   32-bit columns, f64 and f32 values, m = 8) bitwise equals the oracle's C
   restatement of the reference kernel on the full matrix.
