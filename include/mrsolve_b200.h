@@ -317,6 +317,9 @@ int  mrs_version(void);
  *                   1 = operators with >= 12 entries per row (outside the LONG range),
  *                   2 = (default) only long uniform rows (>= 20 per row, max <= 1.1 x mean;
  *                   27-point stencils), 0 = off
+ *   "spmm_variant" 0..3  force one SpMM variant for every operator (A/B runs):
+ *                   0 = per operator (default), 1 = lane, 2 = cooperative loads,
+ *                   3 = 16 entries in flight
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

@@ -61,6 +61,14 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cu, cpp, _ = _sources()
     jobs = []
     for src in cu:
+        if os.path.basename(src) == "spmm_inst.cu":
+            # the SpMM template family: one object per (value type, op)
+            for f32 in (0, 1):
+                for op in range(4):
+                    obj = os.path.join(BUILD, f"spmm_inst_{'f32' if f32 else 'f64'}_{op}.o")
+                    jobs.append([nvcc, *ARCH, *NVCC_FLAGS, f"-DMRS_INST_F32={f32}",
+                                 f"-DMRS_INST_OP={op}", "-c", src, "-o", obj])
+            continue
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")
         jobs.append([nvcc, *ARCH, *NVCC_FLAGS, "-c", src, "-o", obj])
     cxx = os.environ.get("CXX", "g++")
@@ -72,7 +80,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         r = subprocess.run(cmd, capture_output=True, text=True)
         return cmd, r
 
-    with cf.ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 2)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=min(12, os.cpu_count() or 2)) as ex:
         for cmd, r in ex.map(run, jobs):
             if verbose or r.returncode != 0:
                 sys.stderr.write(" ".join(cmd) + "\n" + r.stdout + r.stderr)

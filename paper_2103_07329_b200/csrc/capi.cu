@@ -9,6 +9,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -57,6 +58,46 @@ int get_scratch(int64_t Km, void* stream, Scratch** out) {
     return MRS_OK;
 }
 
+// Plugin SpMM calls carry no plan: the variant of an operator is measured on
+// its first call with a given m (outside stream capture; the product goes to
+// a scratch block, the caller's buffers are untouched) and remembered by the
+// operator's device arrays.  A later operator reusing those addresses only
+// inherits a speed choice -- every variant computes the same bits.
+struct TuneKey {
+    const void* rp; const void* ci; const void* v; const void* slab;
+    int64_t nrows, nnz, m;
+    bool operator<(const TuneKey& o) const {
+        return std::tie(rp, ci, v, slab, nrows, nnz, m) <
+               std::tie(o.rp, o.ci, o.v, o.slab, o.nrows, o.nnz, o.m);
+    }
+};
+std::mutex g_tune_mu;
+std::map<TuneKey, int> g_tuned;
+
+int plugin_variant(const DevCsr& D, const double* x, int64_t m, cudaStream_t s) {
+    if (!spmm_autotune_enabled()) return SV_AUTO;
+    TuneKey k{D.rp, D.ci, D.v, D.slab_base, D.nrows, D.nnz, m};
+    {
+        std::lock_guard<std::mutex> lk(g_tune_mu);
+        auto it = g_tuned.find(k);
+        if (it != g_tuned.end()) return it->second;
+    }
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone)
+        return SV_AUTO;
+    double* scratch = nullptr;
+    if (cudaMalloc(&scratch, sizeof(double) * (size_t)D.nrows * m) != cudaSuccess) {
+        cudaGetLastError();
+        return SV_AUTO;
+    }
+    const int v = spmm_tune(D, x, scratch, m, s);
+    cudaStreamSynchronize(s);
+    cudaFree(scratch);
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tuned[k] = v;
+    return v;
+}
+
 int vec_call(int op, VArgs a, int K, double* out, void* stream) {
     if (a.n < 0 || !m_ok(a.m)) return MRS_ERR_ARG;
     if (a.n == 0) {
@@ -95,6 +136,8 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_split")) { set_spmm_long_split(value); return MRS_OK; }
+    if (!strcmp(key, "spmm_autotune")) { set_spmm_autotune(value); return MRS_OK; }
+    if (!strcmp(key, "spmm_variant")) { set_spmm_variant(value); return MRS_OK; }
     if (!strcmp(key, "halo_overlap")) { set_halo_overlap(value); return MRS_OK; }
     if (!strcmp(key, "spmm_coop")) { set_spmm_coop(value); return MRS_OK; }
     if (!strcmp(key, "dense_mma")) { set_dense_mma(value); return MRS_OK; }
@@ -145,11 +188,12 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_
         D.n_long = A->n_long;
         D.long_thr = A->long_thr;
     }
+    // unaligned views fall back to the scalar-per-column kernel
+    bool vec_ok = aligned16(x) && aligned16(y) && (!b || aligned16(b));
+    if (vec_ok) D.variant = plugin_variant(D, x, m, (cudaStream_t)stream);
     SpArgs a;
     memset(&a, 0, sizeof(a));
     a.x = x; a.y = y; a.b = b; a.mode = mode;
-    // unaligned views fall back to the scalar-per-column kernel
-    bool vec_ok = aligned16(x) && aligned16(y) && (!b || aligned16(b));
     cudaError_t e = launch_spmm(OP_SPMV, D, a, m, (cudaStream_t)stream, !vec_ok && m > 1);
     return e == cudaSuccess ? MRS_OK : MRS_ERR_CUDA;
 }

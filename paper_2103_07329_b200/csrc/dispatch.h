@@ -26,6 +26,7 @@ struct DevCsr {
     int32_t* long_rows = nullptr; // rows with > long_thr entries (spmm.cuh long_row_cta)
     int n_long = 0, long_thr = 0;
     int max_row = 0;              // longest row (solver levels; 0 = unknown)
+    int variant = 0;              // SpmmVariant chosen for this operator (0 = heuristic)
     bool present() const { return rp != nullptr; }
     // algorithmic bytes of one pass over the CSR arrays
     double bytes() const {
@@ -55,6 +56,12 @@ void set_loop_unroll(int64_t v);
 void set_dense_mma(int64_t v);
 int64_t spmm_long_split();
 int64_t halo_overlap();
+// per-operator SpMM variant by measurement (kernels.cu); knob spmm_autotune
+int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
+              float* best_us = nullptr);
+int64_t spmm_autotune_enabled();
+void set_spmm_autotune(int64_t v);
+void set_spmm_variant(int64_t v);
 void set_halo_overlap(int64_t v);
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;

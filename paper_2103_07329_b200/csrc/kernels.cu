@@ -1,6 +1,7 @@
 // kernels.cu -- template instantiation and dispatch of the SpMM and vector
 // kernel families, and the dense coarse-level solve.
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 #include <unordered_map>
 
@@ -42,6 +43,9 @@ void set_dense_mma(int64_t v) { g_dense_mma = v ? 1 : 0; }
 static int64_t g_halo_overlap = 1;    // multi-GPU: interior rows during the exchange
 int64_t halo_overlap() { return g_halo_overlap; }
 void set_halo_overlap(int64_t v) { g_halo_overlap = v < 0 ? 0 : (v > 2 ? 2 : v); }
+static int64_t g_variant = 0;         // 0: per operator (autotuned / heuristic)
+int64_t spmm_variant() { return g_variant; }
+void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 3 ? 0 : v); }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
@@ -74,9 +78,71 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
     if ((A.nrows + 1) * m >= (int64_t)INT32_MAX || (A.ncols + 1) * m >= (int64_t)INT32_MAX ||
         A.nnz >= (int64_t)INT32_MAX)
         return cudaErrorInvalidValue;
-    if (A.vb == 8) return launch_spmm_f64(op, A, a, m, s, generic);
-    if (A.vb == 4) return launch_spmm_f32(op, A, a, m, s, generic);
+    a.variant = A.variant;
+    if (A.vb == 8) {
+        switch (op) {
+        case OP_SPMV: return launch_spmm_op_f64<OP_SPMV>(A, a, m, s, generic);
+        case OP_JAC_SWEEP: return launch_spmm_op_f64<OP_JAC_SWEEP>(A, a, m, s, generic);
+        case OP_CHEB_FIRST: return launch_spmm_op_f64<OP_CHEB_FIRST>(A, a, m, s, generic);
+        case OP_CHEB_STEP: return launch_spmm_op_f64<OP_CHEB_STEP>(A, a, m, s, generic);
+        }
+    } else if (A.vb == 4) {
+        switch (op) {
+        case OP_SPMV: return launch_spmm_op_f32<OP_SPMV>(A, a, m, s, generic);
+        case OP_JAC_SWEEP: return launch_spmm_op_f32<OP_JAC_SWEEP>(A, a, m, s, generic);
+        case OP_CHEB_FIRST: return launch_spmm_op_f32<OP_CHEB_FIRST>(A, a, m, s, generic);
+        case OP_CHEB_STEP: return launch_spmm_op_f32<OP_CHEB_STEP>(A, a, m, s, generic);
+        }
+    }
     return cudaErrorInvalidValue;
+}
+
+// Per-operator SpMM variant choice by measurement: every applicable variant
+// (lane / cooperative loads / 16 in flight) runs the operator's product
+// y = A x (ASSIGN) back to back on the given buffers and the fastest wins.
+// All variants compute the same bits, so the choice only affects speed.
+// Returns the SpmmVariant to store in A.variant (SV_AUTO: nothing to choose).
+static int64_t g_autotune = 1;
+int64_t spmm_autotune_enabled() { return g_autotune; }
+void set_spmm_autotune(int64_t v) { g_autotune = v ? 1 : 0; }
+
+int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
+              float* best_us) {
+    if (best_us) *best_us = 0.f;
+    if (!g_autotune || A.nrows == 0 || A.nnz == 0 || spmm_variant() != SV_AUTO) return SV_AUTO;
+    int cand[3], nc = 0;
+    cand[nc++] = SV_LANE;
+    if (m == 4 || m == 8 || m == 16) cand[nc++] = SV_COOP;
+    if (m <= 16 && (m & (m - 1)) == 0) cand[nc++] = SV_LONG;
+    if (nc == 1) return SV_AUTO;
+    cudaEvent_t e0, e1;
+    if (cudaEventCreate(&e0) != cudaSuccess) return SV_AUTO;
+    if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); return SV_AUTO; }
+    SpArgs a;
+    memset(&a, 0, sizeof(a));
+    a.x = x; a.y = y; a.mode = MRS_MODE_ASSIGN;
+    int best = SV_AUTO;
+    float best_t = 3.4e38f;
+    const int reps = 5;
+    for (int i = 0; i < nc; ++i) {
+        DevCsr B = A;
+        B.variant = cand[i];
+        cudaError_t e = launch_spmm(OP_SPMV, B, a, m, s);           // warm-up
+        cudaEventRecord(e0, s);
+        for (int r = 0; r < reps && e == cudaSuccess; ++r) e = launch_spmm(OP_SPMV, B, a, m, s);
+        cudaEventRecord(e1, s);
+        if (e != cudaSuccess || cudaEventSynchronize(e1) != cudaSuccess) {
+            cudaGetLastError();
+            continue;
+        }
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, e0, e1);
+        if (ms < best_t) { best_t = ms; best = cand[i]; }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (best_us && best != SV_AUTO) *best_us = 1e3f * best_t / reps;
+    return best;
 }
 
 template <int OP>

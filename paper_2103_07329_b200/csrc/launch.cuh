@@ -13,6 +13,7 @@ namespace mrs {
 int64_t spmm_long_max_rows();   // LONG-row SpMM variant up to this many rows (knob)
 int64_t spmm_chunk_rows();      // rows per CTA chunk of the SpMM grid (knob)
 int64_t spmm_coop();            // cooperative entry loads for long-row operators (knob)
+int64_t spmm_variant();         // force one SpmmVariant everywhere (knob; 0 = per operator)
 
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
@@ -95,10 +96,21 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         (void)launch_ex_smem(kern, g + a.long_ctas,
                              a.long_ctas ? kLongProducts * sizeof(double) : 0, s, a);
     };
-    // small operators with long rows: the LONG variant (16 entries in flight)
-    // variant choice by the whole operator's shape (rows_hint), not a split subset
-    const int64_t nr = a.rows_hint;
-    if (!generic && m <= 16 && nr <= spmm_long_max_rows() && a.nnz_hint >= 12 * nr) {
+    int v = a.variant ? a.variant : (int)spmm_variant();
+    if (v == SV_AUTO) {
+        // shape heuristic: small operators with long rows -> LONG (16 entries
+        // in flight); large operators with long AND uniform rows (27-point
+        // stencils: mean >= 20, no row more than ~10 % above it) -> COOP
+        // (knob spmm_coop: 1 = every operator with >= 12 entries per row)
+        const int64_t nr = a.rows_hint;      // the whole operator, not a split subset
+        const int64_t coop = spmm_coop();
+        const bool uniform_long = a.nnz_hint >= 20 * nr && a.max_row_hint > 0 &&
+                                  (int64_t)a.max_row_hint * 10 * nr <= 11 * a.nnz_hint + 10 * nr;
+        if (m <= 16 && nr <= spmm_long_max_rows() && a.nnz_hint >= 12 * nr) v = SV_LONG;
+        else if ((coop == 1 && a.nnz_hint >= 12 * nr) || (coop == 2 && uniform_long)) v = SV_COOP;
+        else v = SV_LANE;
+    }
+    if (!generic && v == SV_LONG) {
         switch (m) {
         case 1: go(spmm_kernel<1, OP, Tv, Ti, true>, Lay<1>::RPB); return cudaGetLastError();
         case 2: go(spmm_kernel<2, OP, Tv, Ti, true>, Lay<2>::RPB); return cudaGetLastError();
@@ -108,14 +120,7 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         default: break;
         }
     }
-    // large operators with long rows: cooperative entry loads (coop_accumulate)
-    // spmm_coop: 1 = every operator with >= 12 entries per row; 2 (default) =
-    // only long AND uniform rows (27-point stencils: mean >= 20, no row more
-    // than ~10 % above it), where the warp-uniform trip count wastes nothing
-    const int64_t coop = spmm_coop();
-    const bool uniform_long = a.nnz_hint >= 20 * nr && a.max_row_hint > 0 &&
-                              (int64_t)a.max_row_hint * 10 * nr <= 11 * a.nnz_hint + 10 * nr;
-    if (!generic && ((coop == 1 && a.nnz_hint >= 12 * nr) || (coop == 2 && uniform_long))) {
+    if (!generic && v == SV_COOP) {
         switch (m) {
         case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB); return cudaGetLastError();
         case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB); return cudaGetLastError();
@@ -145,9 +150,12 @@ inline cudaError_t spmm_op(const DevCsr& A, const SpArgs& a, int64_t m, cudaStre
     return cudaErrorInvalidValue;
 }
 
-cudaError_t launch_spmm_f64(int op, const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s,
-                            bool generic);
-cudaError_t launch_spmm_f32(int op, const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s,
-                            bool generic);
+// One translation unit per (value type, op) (spmm_<t>_<op>.cu): parallel builds.
+template <int OP>
+cudaError_t launch_spmm_op_f64(const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s,
+                               bool generic);
+template <int OP>
+cudaError_t launch_spmm_op_f32(const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s,
+                               bool generic);
 
 }  // namespace mrs

@@ -1141,6 +1141,42 @@ static int build_sgs_schedule(const mrs_host_csr* h, LevelDev& lv, std::vector<v
     return MRS_OK;
 }
 
+// Per-operator SpMM variant (kernels.cu spmm_tune), measured once at
+// finalize on the plan's own level buffers: every operator the solve
+// multiplies with (A_l, R_l, P_l) gets the variant that ran fastest for it
+// at the plan's m.  Scratch contents are overwritten later anyway.
+void tune_operators(mrs_plan* p) {
+    if (!spmm_autotune_enabled()) return;
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
+    const int64_t m = p->m;
+    auto zero = [&](double* buf, int64_t rows) {
+        if (buf) cudaMemsetAsync(buf, 0, sizeof(double) * rows * m, s);
+    };
+    for (size_t l = 0; l < p->L.size(); ++l) {
+        LevelDev& lv = p->L[l];
+        const bool mg = p->desc.precond == MRS_PC_MG;
+        double* x = (l == 0 || !mg) ? p->p : lv.xa;
+        double* y = (l == 0 || !mg) ? p->q : lv.r;
+        if (l > 0 && !mg) break;
+        zero(x, lv.vrows);
+        if (lv.A.present() && x && y) lv.A.variant = spmm_tune(lv.A, x, y, m, s);
+        if (!mg || l + 1 >= p->L.size()) continue;
+        LevelDev& lc = p->L[l + 1];
+        if (lv.R.present() && lv.r && lc.b) {
+            zero(lv.r, lv.vrows);
+            lv.R.variant = spmm_tune(lv.R, lv.r, lc.b, m, s);
+        }
+        if (lv.P.present() && lc.xa && lv.r) {
+            zero(lc.xa, lc.vrows);
+            lv.P.variant = spmm_tune(lv.P, lc.xa, lv.r, m, s);
+        }
+    }
+    cudaStreamSynchronize(s);
+    cudaStreamDestroy(s);
+    cudaGetLastError();
+}
+
 // diagonal of a host CSR in full precision (core.py:500-510); MRS_ERR_SINGULAR
 // when a row has no structural diagonal or a zero diagonal entry.
 int host_diag(const mrs_host_csr* h, std::vector<double>& d) {
@@ -1363,6 +1399,7 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
     MRS_CUDA_OK(cudaMallocHost(&p->hist_host, sizeof(double) * (size_t)(p->desc.max_iters + 1) * m));
     MRS_CUDA_OK(cudaEventCreate(&p->ev0));
     MRS_CUDA_OK(cudaEventCreate(&p->ev1));
+    tune_operators(p);
     p->finalized = true;
     // estimate the per-iteration byte model / kernel count once
     Program pg;

@@ -38,6 +38,15 @@ template <int M> struct Lay {
     static constexpr int UNR = 4;                  // entries in flight per lane
 };
 
+// Lane-path variants of one SpMM (all bitwise identical; per-operator choice,
+// csrc/solver.cu autotune / knob spmm_variant).
+enum SpmmVariant : int {
+    SV_AUTO = 0,     // shape heuristic (launch.cuh spmm_m)
+    SV_LANE = 1,     // LPR lanes per row, every lane loads every entry, 4 in flight
+    SV_COOP = 2,     // lanes load distinct entries and shuffle (m in {4, 8, 16})
+    SV_LONG = 3,     // 16 entries in flight per lane, 1 CTA/SM (m <= 16)
+};
+
 // Kernel operation selector.
 enum SpOp : int {
     OP_SPMV = 0,         // y op= A x by `mode` (+ optional next-level seed)   (csr_spmv)
@@ -88,6 +97,7 @@ struct SpArgs {
     int row_base, row_split, row_gap, no_long_ctas;
     int64_t vrows;
     int64_t rows_hint;      // the operator's row count (variant choice)
+    int variant;            // SpmmVariant forced for this operator (0 = heuristic)
     RedArgs red;
 };
 
@@ -458,8 +468,10 @@ __device__ __forceinline__ void coop_accumulate(const SpArgs& a, const Src& src,
 // 16 entries in flight per lane -- the row's dependent chain is 4x shorter;
 // register-heavy, so only used where few CTAs run anyway.  Same order.
 // COOP: large operators with long rows (coop_accumulate), M in {4, 8, 16}.
+// COOP runs at 4 CTAs/SM (64 registers): its shuffled (column, value) pairs
+// and LPR gathered slices in flight spill at 40.
 template <int M, int OP, typename Tv, typename Ti, bool LONG = false, bool COOP = false>
-__global__ void __launch_bounds__(kThreads, LONG ? 1 : spmm_min_blocks<M, OP>())
+__global__ void __launch_bounds__(kThreads, LONG ? 1 : (COOP ? 4 : spmm_min_blocks<M, OP>()))
 spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
