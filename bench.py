@@ -88,6 +88,16 @@ CONFIGS["c2g"] = dict(CONFIGS["c2"], workload=(
     "MultiGrid smoother: RS AMG V(1,1) symmetric Gauss-Seidel + PCG, fp64, tol 1e-8"),
     roles={"solver": {"method": "CG", "rel_tolerance": "1e-8"},
            "preconditioner": {"method": "MultiGrid"}})
+# C3 with the fp32-vector V-cycle (extension: "fp32 preconditioner"; levels
+# 1 .. tail-1 store their block vectors in float32, fp64 accumulation)
+CONFIGS["c3v32"] = dict(CONFIGS["c3"], workload=CONFIGS["c3"]["workload"].replace(
+    "fp64 vectors)", "fp64 Krylov vectors, fp32 V-cycle vectors below level 0)"),
+    roles=dict(CONFIGS["c3"]["roles"], preconditioner={
+        "method": "MultiGrid", "mg_mixed_precision": "1", "mg_vector_precision": "fp32"}))
+CONFIGS["c2v32"] = dict(CONFIGS["c2"], workload=CONFIGS["c2"]["workload"].replace(
+    "fp64, tol", "fp64 Krylov vectors, fp32 V-cycle vectors below level 0, tol"),
+    roles=dict(CONFIGS["c2"]["roles"], preconditioner={
+        "method": "MultiGrid", "mg_vector_precision": "fp32"}))
 CONFIGS["fig3"] = dict(grid=128, m=16, workload=(
     "Fig. 3 solver on 3D Poisson 7-pt 128^3, m=16 seeded RHS, zero guess: PBiCGStab + RS AMG "
     "(aggressive coarsening on 2 levels, 2 paths, coarse <= 500) V(1,1) Chebyshev-2, fp64, "
@@ -256,8 +266,12 @@ def run_reference_cpu(steps: int, warmup: int, timeout: float = 900.0, nproc: in
     cols = [(M * i // nproc, M * (i + 1) // nproc) for i in range(nproc)]
     procs = []
     for i, (c0, c1) in enumerate(cols):
+        # the reference knows no fp32-vector V-cycle (our extension): its arm
+        # runs the same configuration with fp64 vectors
+        ref_roles = {r: {k: v for k, v in e.items() if k != "mg_vector_precision"}
+                     for r, e in ROLES.items()}
         code = REF_SNIPPET.format(grid=GRID, m=M, seed=SEED, tol=TOL, steps=steps, warmup=warmup,
-                                  roles=repr(ROLES), s27=CFG.get("kind") == "s27", root=ROOT,
+                                  roles=repr(ref_roles), s27=CFG.get("kind") == "s27", root=ROOT,
                                   col0=c0, ncol=c1 - c0, nproc=nproc, bdir=bdir)
         cmd = ["taskset", "-c", str(cores[i % len(cores)]), sys.executable, "-c", code]
         procs.append(subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE,

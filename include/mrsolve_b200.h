@@ -187,6 +187,10 @@ typedef struct {
     double  drift_limit; /* PBiCGStab: ||true r|| / ||recurrence r|| above this raises
                             MRS_ERR_INSTABILITY (solvers.py:68, :415-423); 0 = 1e3 */
     int32_t pc_direction;/* MRS_PC_SGS: MRS_SGS_* (sweeps = pc_sweeps) */
+    int32_t vec32;       /* MultiGrid, single GPU: 1 = the V-cycle vectors of levels
+                            1 .. (collapsed tail or coarsest) - 1 are float32 (loads
+                            widened, fp64 accumulation, stores rounded); the Krylov
+                            vectors and level 0 stay float64 (an fp32 preconditioner) */
 } mrs_plan_desc;
 
 typedef struct mrs_plan mrs_plan;

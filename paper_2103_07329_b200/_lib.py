@@ -52,7 +52,7 @@ class mrs_plan_desc(C.Structure):
                 ("pc_weight", C.c_double), ("pc_sweeps", C.c_int32), ("mg_cycles", C.c_int32),
                 ("pre", mrs_smoother), ("post", mrs_smoother), ("nlevels", C.c_int32),
                 ("exec", C.c_int32), ("merged", C.c_int32), ("drift_limit", C.c_double),
-                ("pc_direction", C.c_int32)]
+                ("pc_direction", C.c_int32), ("vec32", C.c_int32)]
 
 
 class mrs_stats(C.Structure):

@@ -75,7 +75,9 @@ std::mutex g_tune_mu;
 std::map<TuneKey, int> g_tuned;
 
 int plugin_variant(const DevCsr& D, const double* x, int64_t m, cudaStream_t s) {
-    if (!spmm_autotune_enabled()) return SV_AUTO;
+    // (a forced variant -- knob spmm_variant -- is applied by the launcher;
+    // nothing is measured or remembered meanwhile)
+    if (!spmm_autotune_enabled() || spmm_variant() != SV_AUTO) return SV_AUTO;
     TuneKey k{D.rp, D.ci, D.v, D.slab_base, D.nrows, D.nnz, m};
     {
         std::lock_guard<std::mutex> lk(g_tune_mu);

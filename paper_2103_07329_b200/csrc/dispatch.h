@@ -58,10 +58,11 @@ int64_t spmm_long_split();
 int64_t halo_overlap();
 // per-operator SpMM variant by measurement (kernels.cu); knob spmm_autotune
 int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
-              float* best_us = nullptr);
+              float* best_us = nullptr, int vp = 0);
 int64_t spmm_autotune_enabled();
 void set_spmm_autotune(int64_t v);
 void set_spmm_variant(int64_t v);
+int64_t spmm_variant();
 void set_halo_overlap(int64_t v);
 // Gauss-Seidel half-sweep on one thread-block cluster (sgs.cu)
 struct SgsArgs;

@@ -45,7 +45,7 @@ int64_t halo_overlap() { return g_halo_overlap; }
 void set_halo_overlap(int64_t v) { g_halo_overlap = v < 0 ? 0 : (v > 2 ? 2 : v); }
 static int64_t g_variant = 0;         // 0: per operator (autotuned / heuristic)
 int64_t spmm_variant() { return g_variant; }
-void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 3 ? 0 : v); }
+void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 5 ? 0 : v); }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
@@ -107,20 +107,24 @@ int64_t spmm_autotune_enabled() { return g_autotune; }
 void set_spmm_autotune(int64_t v) { g_autotune = v ? 1 : 0; }
 
 int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
-              float* best_us) {
+              float* best_us, int vp) {
     if (best_us) *best_us = 0.f;
     if (!g_autotune || A.nrows == 0 || A.nnz == 0 || spmm_variant() != SV_AUTO) return SV_AUTO;
-    int cand[3], nc = 0;
+    int cand[5], nc = 0;
     cand[nc++] = SV_LANE;
-    if (m == 4 || m == 8 || m == 16) cand[nc++] = SV_COOP;
+    if (vp == VP_DD && (m == 4 || m == 8 || m == 16)) cand[nc++] = SV_COOP;
     if (m <= 16 && (m & (m - 1)) == 0) cand[nc++] = SV_LONG;
+    if (vp == VP_DD && m <= 16 && (m & (m - 1)) == 0) {
+        cand[nc++] = SV_LANE_L2;
+        cand[nc++] = SV_LANE_NA;
+    }
     if (nc == 1) return SV_AUTO;
     cudaEvent_t e0, e1;
     if (cudaEventCreate(&e0) != cudaSuccess) return SV_AUTO;
     if (cudaEventCreate(&e1) != cudaSuccess) { cudaEventDestroy(e0); return SV_AUTO; }
     SpArgs a;
     memset(&a, 0, sizeof(a));
-    a.x = x; a.y = y; a.mode = MRS_MODE_ASSIGN;
+    a.x = x; a.y = y; a.mode = MRS_MODE_ASSIGN; a.vp = vp;
     int best = SV_AUTO;
     float best_t = 3.4e38f;
     const int reps = 5;

@@ -69,9 +69,12 @@ inline void wave_grid(const void* fn, int64_t nrows, int64_t rows_per_pass, int&
 }
 
 
-// SpMM family: chunk-strided one-wave grid (see spmm.cuh).
-template <int OP, typename Tv, typename Ti>
+// SpMM family: chunk-strided one-wave grid (see spmm.cuh).  Tx / Ty: vector
+// types (double, or the float levels of the fp32-vector V-cycle: lane and
+// LONG variants, m in {1, 2, 4, 8, 16, 32}).
+template <int OP, typename Tv, typename Ti, typename Tx = double, typename Ty = double>
 inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
+    constexpr bool kF64 = sizeof(Tx) == 8 && sizeof(Ty) == 8;
     int g;
     auto go = [&](auto kern, int64_t rpp) {
         // Balanced one wave: every CTA gets the same number of passes (the
@@ -112,41 +115,89 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     }
     if (!generic && v == SV_LONG) {
         switch (m) {
-        case 1: go(spmm_kernel<1, OP, Tv, Ti, true>, Lay<1>::RPB); return cudaGetLastError();
-        case 2: go(spmm_kernel<2, OP, Tv, Ti, true>, Lay<2>::RPB); return cudaGetLastError();
-        case 4: go(spmm_kernel<4, OP, Tv, Ti, true>, Lay<4>::RPB); return cudaGetLastError();
-        case 8: go(spmm_kernel<8, OP, Tv, Ti, true>, Lay<8>::RPB); return cudaGetLastError();
-        case 16: go(spmm_kernel<16, OP, Tv, Ti, true>, Lay<16>::RPB); return cudaGetLastError();
+        case 1: go(spmm_kernel<1, OP, Tv, Ti, true, false, Tx, Ty>, Lay<1>::RPB); return cudaGetLastError();
+        case 2: go(spmm_kernel<2, OP, Tv, Ti, true, false, Tx, Ty>, Lay<2>::RPB); return cudaGetLastError();
+        case 4: go(spmm_kernel<4, OP, Tv, Ti, true, false, Tx, Ty>, Lay<4>::RPB); return cudaGetLastError();
+        case 8: go(spmm_kernel<8, OP, Tv, Ti, true, false, Tx, Ty>, Lay<8>::RPB); return cudaGetLastError();
+        case 16: go(spmm_kernel<16, OP, Tv, Ti, true, false, Tx, Ty>, Lay<16>::RPB); return cudaGetLastError();
         default: break;
         }
     }
-    if (!generic && v == SV_COOP) {
-        switch (m) {
-        case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB); return cudaGetLastError();
-        case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB); return cudaGetLastError();
-        case 16: go(spmm_kernel<16, OP, Tv, Ti, false, true>, Lay<16>::RPB); return cudaGetLastError();
-        default: break;
+    if constexpr (kF64) {
+        if (!generic && (v == SV_LANE_L2 || v == SV_LANE_NA)) {
+            const bool l2 = v == SV_LANE_L2;
+            switch (m) {
+            case 1: l2 ? go(spmm_kernel<1, OP, Tv, Ti, false, false, double, double, 1>, Lay<1>::RPB)
+                       : go(spmm_kernel<1, OP, Tv, Ti, false, false, double, double, 2>, Lay<1>::RPB);
+                return cudaGetLastError();
+            case 2: l2 ? go(spmm_kernel<2, OP, Tv, Ti, false, false, double, double, 1>, Lay<2>::RPB)
+                       : go(spmm_kernel<2, OP, Tv, Ti, false, false, double, double, 2>, Lay<2>::RPB);
+                return cudaGetLastError();
+            case 4: l2 ? go(spmm_kernel<4, OP, Tv, Ti, false, false, double, double, 1>, Lay<4>::RPB)
+                       : go(spmm_kernel<4, OP, Tv, Ti, false, false, double, double, 2>, Lay<4>::RPB);
+                return cudaGetLastError();
+            case 8: l2 ? go(spmm_kernel<8, OP, Tv, Ti, false, false, double, double, 1>, Lay<8>::RPB)
+                       : go(spmm_kernel<8, OP, Tv, Ti, false, false, double, double, 2>, Lay<8>::RPB);
+                return cudaGetLastError();
+            case 16: l2 ? go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 1>, Lay<16>::RPB)
+                        : go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 2>, Lay<16>::RPB);
+                return cudaGetLastError();
+            default: break;
+            }
+        }
+        if (!generic && v == SV_COOP) {
+            switch (m) {
+            case 4: go(spmm_kernel<4, OP, Tv, Ti, false, true>, Lay<4>::RPB); return cudaGetLastError();
+            case 8: go(spmm_kernel<8, OP, Tv, Ti, false, true>, Lay<8>::RPB); return cudaGetLastError();
+            case 16: go(spmm_kernel<16, OP, Tv, Ti, false, true>, Lay<16>::RPB); return cudaGetLastError();
+            default: break;
+            }
         }
     }
     switch (generic ? 0 : m) {
-    case 1: go(spmm_kernel<1, OP, Tv, Ti>, Lay<1>::RPB); break;
-    case 2: go(spmm_kernel<2, OP, Tv, Ti>, Lay<2>::RPB); break;
-    case 4: go(spmm_kernel<4, OP, Tv, Ti>, Lay<4>::RPB); break;
-    case 8: go(spmm_kernel<8, OP, Tv, Ti>, Lay<8>::RPB); break;
-    case 16: go(spmm_kernel<16, OP, Tv, Ti>, Lay<16>::RPB); break;
-    case 32: go(spmm_kernel<32, OP, Tv, Ti>, Lay<32>::RPB); break;
-    case 64: go(spmm_kernel<64, OP, Tv, Ti>, Lay<64>::RPB); break;
-    default: go(spmm_kernel_generic<OP, Tv, Ti>, kThreads / m); break;
+    case 1: go(spmm_kernel<1, OP, Tv, Ti, false, false, Tx, Ty>, Lay<1>::RPB); break;
+    case 2: go(spmm_kernel<2, OP, Tv, Ti, false, false, Tx, Ty>, Lay<2>::RPB); break;
+    case 4: go(spmm_kernel<4, OP, Tv, Ti, false, false, Tx, Ty>, Lay<4>::RPB); break;
+    case 8: go(spmm_kernel<8, OP, Tv, Ti, false, false, Tx, Ty>, Lay<8>::RPB); break;
+    case 16: go(spmm_kernel<16, OP, Tv, Ti, false, false, Tx, Ty>, Lay<16>::RPB); break;
+    case 32: go(spmm_kernel<32, OP, Tv, Ti, false, false, Tx, Ty>, Lay<32>::RPB); break;
+    default:
+        if constexpr (kF64) {
+            if (!generic && m == 64) go(spmm_kernel<64, OP, Tv, Ti>, Lay<64>::RPB);
+            else go(spmm_kernel_generic<OP, Tv, Ti>, kThreads / m);
+        } else {
+            return cudaErrorInvalidValue;     // float vectors: m in {1, ..., 32} powers of 2
+        }
+        break;
     }
     return cudaGetLastError();
 }
 
+// Vector precision of one launch (SpArgs::vp): VP_DD all double; VP_FF all
+// float (a float level); VP_DF double gathered operand -> float row operands
+// (restriction into a float level); VP_FD float gathered -> double row
+// operands (prolongation from a float level).
+template <int OP, typename Tv, typename Ti>
+inline cudaError_t spmm_vp(const SpArgs& a, int64_t m, cudaStream_t s, bool g) {
+    switch (a.vp) {
+    case VP_DD: return spmm_m<OP, Tv, Ti>(a, m, s, g);
+    case VP_FF: return spmm_m<OP, Tv, Ti, float, float>(a, m, s, g);
+    case VP_DF:
+        if constexpr (OP == OP_SPMV) return spmm_m<OP, Tv, Ti, double, float>(a, m, s, g);
+        break;
+    case VP_FD:
+        if constexpr (OP == OP_SPMV) return spmm_m<OP, Tv, Ti, float, double>(a, m, s, g);
+        break;
+    }
+    return cudaErrorInvalidValue;
+}
+
 template <int OP, typename Tv>
 inline cudaError_t spmm_op(const DevCsr& A, const SpArgs& a, int64_t m, cudaStream_t s, bool g) {
-    if (A.ib == 4) return spmm_m<OP, Tv, uint32_t>(a, m, s, g);
-    if (A.ib == 2) return spmm_m<OP, Tv, uint16_t>(a, m, s, g);
+    if (A.ib == 4) return spmm_vp<OP, Tv, uint32_t>(a, m, s, g);
+    if (A.ib == 2) return spmm_vp<OP, Tv, uint16_t>(a, m, s, g);
     if constexpr (OP == OP_SPMV)
-        if (A.ib == 1) return spmm_m<OP, Tv, uint8_t>(a, m, s, g);
+        if (A.ib == 1) return spmm_m<OP, Tv, uint8_t>(a, m, s, g);     // plugin: double only
     return cudaErrorInvalidValue;
 }
 

@@ -44,6 +44,7 @@ struct LevelDev {
     int64_t nloc = 0;        // rows this rank owns (replicated level: all rows)
     int64_t vrows = 0;       // allocated rows of level vectors (own + largest halo; gather pad)
     bool replicated = false; // agglomerated: every rank holds the whole level
+    bool f32 = false;        // this level's V-cycle vectors are float (plan vec32)
     int64_t slice_row0 = 0, slice_rows = 0;   // agglomeration: my restricted slice, allgather count
     Halo hA, hR, hP;         // operand exchanges of A_l x, R_l r, P_l x_{l+1}
     double lmin = 0, lmax = 0;
@@ -172,7 +173,11 @@ struct Builder {
     const int* guard = nullptr;       // body kernels: &st->skip
     double bytes = 0;                 // algorithmic bytes accumulated
     int kernels = 0;
-    double V(int64_t rows) const { return (double)rows * P->m * 8.0; }
+    double V(int64_t rows, bool f32 = false) const { return (double)rows * P->m * (f32 ? 4.0 : 8.0); }
+    // vector precision of a launch gathering level-precision gx and writing gy
+    static int vp(bool gx32, bool gy32) {
+        return gx32 ? (gy32 ? VP_FF : VP_FD) : (gy32 ? VP_DF : VP_DD);
+    }
 
     RedArgs red(int epi) const {
         RedArgs r;
@@ -320,17 +325,20 @@ struct Builder {
     // y = A x (mode); optional fused dot (dvec or x own row) . y -> epilogue;
     // optional seed of y for the level whose diagonal is sd.d.
     void spmv(const DevCsr& A, const double* x, double* y, int mode, const double* b = nullptr,
-              int dot_epi = -1, const double* dvec = nullptr, const Seed& sd = Seed()) {
+              int dot_epi = -1, const double* dvec = nullptr, const Seed& sd = Seed(),
+              int vprec = VP_DD) {
         SpArgs a = sp0();
-        a.x = x; a.y = y; a.b = b; a.mode = mode;
-        double vb = V(A.ncols) + V(A.nrows) + (mode == MRS_MODE_ASSIGN ? 0 : V(A.nrows));
+        a.x = x; a.y = y; a.b = b; a.mode = mode; a.vp = vprec;
+        const bool x32 = vprec == VP_FF || vprec == VP_FD, y32 = vprec == VP_FF || vprec == VP_DF;
+        double vb = V(A.ncols, x32) + V(A.nrows, y32) +
+                    (mode == MRS_MODE_ASSIGN ? 0 : V(A.nrows, y32));
         if (dot_epi >= 0) {
             a.dot = 1; a.red = red(dot_epi); a.x_in = dvec; vb += V(A.nrows);
         }
         if (sd.mode) {
             a.seed = sd.mode; a.seed_out = sd.out; a.d = sd.d;
             if (sd.mode == 1) a.w = sd.w; else a.theta = sd.w;
-            vb += seed_bytes(sd, A.nrows);
+            vb += sd.mode ? V(A.nrows, y32) + 8.0 * A.nrows : 0.0;
         }
         spmm(OP_SPMV, A, a, vb);
     }
@@ -400,7 +408,9 @@ struct Builder {
 
     void jacobi_sweep(LevelDev& lv, const double* b, double w, XB& x, int dot_epi) {
         SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.w = w; a.x_out = x.alt;
-        double eb = 3 * V(lv.A.nrows) + 8.0 * lv.A.nrows;
+        a.vp = lv.f32 ? VP_FF : VP_DD;
+        // x gathered (ncols) + b + x_out (rows) + d
+        double eb = V(lv.A.ncols, lv.f32) + 2 * V(lv.A.nrows, lv.f32) + 8.0 * lv.A.nrows;
         if (dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); }
         spmm(OP_JAC_SWEEP, lv.A, a, eb);
         x.swap();
@@ -419,11 +429,13 @@ struct Builder {
             SpArgs a = sp0(); a.x = dv_cur; a.x_in = x_in; a.r_in = r_in; a.d = lv.d; a.b = b;
             a.c1 = rho_new * rho; a.c2 = 2.0 * rho_new / delta;
             a.x_out = x.cur;
+            a.vp = lv.f32 ? VP_FF : VP_DD;
             const bool more = k + 1 < order;
             a.r_out = more ? lv.r : nullptr;
             a.dv_out = more ? dv_alt : nullptr;
-            double eb = 4 * V(n) + 8.0 * n + (more ? 2 * V(n) : 0);
-            if (!more && dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); eb += V(n); }
+            const bool f = lv.f32;
+            double eb = 4 * V(n, f) + 8.0 * n + (more ? 2 * V(n, f) : 0);
+            if (!more && dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); eb += V(n, f); }
             spmm(OP_CHEB_STEP, lv.A, a, eb);
             rho = rho_new;
             std::swap(dv_cur, dv_alt);
@@ -462,10 +474,12 @@ struct Builder {
         const double theta = 0.5 * (lv.lmax + lv.lmin), delta = 0.5 * (lv.lmax - lv.lmin);
         SpArgs a = sp0(); a.x = x.cur; a.b = b; a.d = lv.d; a.theta = theta;
         a.x_out = x.alt;
+        a.vp = lv.f32 ? VP_FF : VP_DD;
         const bool more = order > 1;
         a.r_out = more ? lv.r : nullptr;
         a.dv_out = more ? lv.dva : nullptr;
-        double eb = 3 * V(n) + 8.0 * n + (more ? 2 * V(n) : 0);
+        const bool f = lv.f32;
+        double eb = 3 * V(n, f) + 8.0 * n + (more ? 2 * V(n, f) : 0);
         if (!more && dot_epi >= 0) { a.dot = 1; a.red = red(dot_epi); }
         spmm(OP_CHEB_FIRST, lv.A, a, eb);
         x.swap();
@@ -530,7 +544,8 @@ struct Builder {
             smooth_nonzero(lv, b, pre, x, -1);
         }
         LevelDev& lc = p.L[l + 1];
-        spmv(lv.A, x.cur, lv.r, MRS_MODE_RSUB, b);                    // r = b - A x
+        spmv(lv.A, x.cur, lv.r, MRS_MODE_RSUB, b, -1, nullptr, Seed(),
+             vp(lv.f32, lv.f32));                                      // r = b - A x
         XB xc{lc.xa, lc.xb};
         if (p.dist && lc.replicated && !lv.replicated) {
             // agglomeration: my slice of rc = R r, allgather, replicated below
@@ -542,10 +557,11 @@ struct Builder {
             vcycle(l + 1, lc.b, true, false, xc, -1);
         } else {
             spmv(lv.R, lv.r, lc.b, MRS_MODE_ASSIGN, nullptr, -1, nullptr,
-                 level_seed(l + 1, xc));                              // rc = R r (+ seed)
+                 level_seed(l + 1, xc), vp(lv.f32, lc.f32));          // rc = R r (+ seed)
             vcycle(l + 1, lc.b, true, true, xc, -1);
         }
-        spmv(lv.P, xc.cur, x.cur, MRS_MODE_ADD);                      // x += P xc
+        spmv(lv.P, xc.cur, x.cur, MRS_MODE_ADD, nullptr, -1, nullptr, Seed(),
+             vp(lc.f32, lv.f32));                                      // x += P xc
         smooth_nonzero(lv, b, p.desc.post, x, dot_epi);
     }
 };
@@ -1150,26 +1166,28 @@ void tune_operators(mrs_plan* p) {
     cudaStream_t s;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
     const int64_t m = p->m;
-    auto zero = [&](double* buf, int64_t rows) {
-        if (buf) cudaMemsetAsync(buf, 0, sizeof(double) * rows * m, s);
+    auto zero = [&](double* buf, int64_t rows, bool f32) {
+        if (buf) cudaMemsetAsync(buf, 0, (f32 ? 4 : 8) * (size_t)rows * m, s);
     };
+    const bool mg = p->desc.precond == MRS_PC_MG;
     for (size_t l = 0; l < p->L.size(); ++l) {
         LevelDev& lv = p->L[l];
-        const bool mg = p->desc.precond == MRS_PC_MG;
+        if (l > 0 && !mg) break;
         double* x = (l == 0 || !mg) ? p->p : lv.xa;
         double* y = (l == 0 || !mg) ? p->q : lv.r;
-        if (l > 0 && !mg) break;
-        zero(x, lv.vrows);
-        if (lv.A.present() && x && y) lv.A.variant = spmm_tune(lv.A, x, y, m, s);
+        const bool f = lv.f32;
+        zero(x, lv.vrows, f);
+        if (lv.A.present() && x && y)
+            lv.A.variant = spmm_tune(lv.A, x, y, m, s, nullptr, Builder::vp(f, f));
         if (!mg || l + 1 >= p->L.size()) continue;
         LevelDev& lc = p->L[l + 1];
         if (lv.R.present() && lv.r && lc.b) {
-            zero(lv.r, lv.vrows);
-            lv.R.variant = spmm_tune(lv.R, lv.r, lc.b, m, s);
+            zero(lv.r, lv.vrows, f);
+            lv.R.variant = spmm_tune(lv.R, lv.r, lc.b, m, s, nullptr, Builder::vp(f, lc.f32));
         }
         if (lv.P.present() && lc.xa && lv.r) {
-            zero(lc.xa, lc.vrows);
-            lv.P.variant = spmm_tune(lv.P, lc.xa, lv.r, m, s);
+            zero(lc.xa, lc.vrows, lc.f32);
+            lv.P.variant = spmm_tune(lv.P, lc.xa, lv.r, m, s, nullptr, Builder::vp(lc.f32, f));
         }
     }
     cudaStreamSynchronize(s);
@@ -1323,9 +1341,21 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
             if (!lv.A.present() || !lv.P.present() || !lv.R.present()) return MRS_ERR_STATE;
         }
         if (!p->inv || p->nc != p->L.back().A.nrows) return MRS_ERR_STATE;
+        if (p->desc.vec32) {
+            // fp32 V-cycle vectors: levels 1 .. (collapsed tail or coarsest) - 1,
+            // single GPU, Jacobi / Chebyshev smoothing (the Gauss-Seidel sweep
+            // and the dense kernels stay double)
+            const mrs_plan_desc& d = p->desc;
+            if (p->dist || d.pre.kind == MRS_SMOOTH_SGS || d.post.kind == MRS_SMOOTH_SGS)
+                return MRS_ERR_UNSUPPORTED;
+            if (p->m > 32 || (p->m & (p->m - 1)) != 0) return MRS_ERR_UNSUPPORTED;
+            const int end = p->dense_from >= 1 ? p->dense_from : (int)p->L.size() - 1;
+            for (int l = 1; l < end; ++l) p->L[l].f32 = true;
+        }
         for (size_t l = 0; l < p->L.size(); ++l) {
             LevelDev& lv = p->L[l];
-            int64_t nl = lv.vrows;
+            // float levels: the same element count in half the bytes
+            const int64_t nl = lv.f32 ? (lv.vrows + 1) / 2 : lv.vrows;
             if (l > 0) lv.b = dalloc<double>(nl * m, o);
             lv.xa = dalloc<double>(nl * m, o);
             lv.xb = dalloc<double>(nl * m, o);

@@ -45,7 +45,12 @@ enum SpmmVariant : int {
     SV_LANE = 1,     // LPR lanes per row, every lane loads every entry, 4 in flight
     SV_COOP = 2,     // lanes load distinct entries and shuffle (m in {4, 8, 16})
     SV_LONG = 3,     // 16 entries in flight per lane, 1 CTA/SM (m <= 16)
+    SV_LANE_L2 = 4,  // lane, gathered x through L2 only (ld.global.cg: no L1 fills)
+    SV_LANE_NA = 5,  // lane, gathered x with L1::no_allocate (hits kept, misses not filled)
 };
+
+// Vector precisions of one SpMM launch (gathered operand -> row operands).
+enum VecPrec : int { VP_DD = 0, VP_FF = 1, VP_DF = 2, VP_FD = 3 };
 
 // Kernel operation selector.
 enum SpOp : int {
@@ -98,6 +103,7 @@ struct SpArgs {
     int64_t vrows;
     int64_t rows_hint;      // the operator's row count (variant choice)
     int variant;            // SpmmVariant forced for this operator (0 = heuristic)
+    int vp;                 // vector precision (VP_*: fp32-vector V-cycle levels)
     RedArgs red;
 };
 
@@ -117,44 +123,121 @@ __device__ __forceinline__ double seed_value(int mode, double v, double d, doubl
     return mode == 1 ? mul(w_or_theta, divd(v, d)) : divd(v, mul(d, w_or_theta));
 }
 
-// Vector-operand loads: NC = through the read-only path (normal kernels: a
-// buffer is never written by the kernel that reads it); !NC = coherent loads
-// for the tail kernel, whose steps read what earlier steps wrote.
-template <int CPL>
-__device__ __forceinline__ Vec<CPL> load_vec_cg(const double* p) {
+// Typed vector operands.  Each level's block vectors are double, or float in
+// the fp32-vector V-cycle (plan option vec32): loads widen to double, stores
+// round to the vector's type; accumulation is always double.  Tx = type of the
+// gathered operand (x / dv), Ty = type of the row operands (b, y, seed, x_out,
+// r, dv ...).  Transfers between a double and a float level mix the two.
+template <int CPL, typename T>
+__device__ __forceinline__ Vec<CPL> ldt(const T* p) {        // read-only path
+    if constexpr (sizeof(T) == 8) {
+        return load_vec<CPL>(reinterpret_cast<const double*>(p));
+    } else {
+        Vec<CPL> r;
+        if constexpr (CPL == 1) {
+            r.v[0] = (double)__ldg(p);
+        } else if constexpr (CPL == 2) {
+            const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+            r.v[0] = t.x; r.v[1] = t.y;
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPL; i += 4) {
+                const float4 t = __ldg(reinterpret_cast<const float4*>(p + i));
+                r.v[i] = t.x; r.v[i + 1] = t.y; r.v[i + 2] = t.z; r.v[i + 3] = t.w;
+            }
+        }
+        return r;
+    }
+}
+template <int CPL, typename T>
+__device__ __forceinline__ Vec<CPL> ldt_rw(const T* p) {     // coherent (read-modify-write)
+    if constexpr (sizeof(T) == 8) {
+        return load_vec_rw<CPL>(reinterpret_cast<const double*>(p));
+    } else {
+        Vec<CPL> r;
+        if constexpr (CPL == 1) {
+            r.v[0] = (double)*p;
+        } else if constexpr (CPL == 2) {
+            const float2 t = *reinterpret_cast<const float2*>(p);
+            r.v[0] = t.x; r.v[1] = t.y;
+        } else {
+#pragma unroll
+            for (int i = 0; i < CPL; i += 4) {
+                const float4 t = *reinterpret_cast<const float4*>(p + i);
+                r.v[i] = t.x; r.v[i + 1] = t.y; r.v[i + 2] = t.z; r.v[i + 3] = t.w;
+            }
+        }
+        return r;
+    }
+}
+template <int CPL, typename T>
+__device__ __forceinline__ void stt(T* p, const Vec<CPL>& a) {
+    if constexpr (sizeof(T) == 8) {
+        store_vec<CPL>(reinterpret_cast<double*>(p), a);
+    } else if constexpr (CPL == 1) {
+        *p = __double2float_rn(a.v[0]);
+    } else if constexpr (CPL == 2) {
+        *reinterpret_cast<float2*>(p) = make_float2(__double2float_rn(a.v[0]),
+                                                    __double2float_rn(a.v[1]));
+    } else {
+#pragma unroll
+        for (int i = 0; i < CPL; i += 4)
+            *reinterpret_cast<float4*>(p + i) =
+                make_float4(__double2float_rn(a.v[i]), __double2float_rn(a.v[i + 1]),
+                            __double2float_rn(a.v[i + 2]), __double2float_rn(a.v[i + 3]));
+    }
+}
+// typed views of the SpArgs operand pointers (declared double*; a float
+// level's buffers are passed through them)
+template <typename T> __device__ __forceinline__ const T* tp(const double* p) {
+    return reinterpret_cast<const T*>(p);
+}
+template <typename T> __device__ __forceinline__ T* tpw(double* p) {
+    return reinterpret_cast<T*>(p);
+}
+
+// Value of the gathered operand at column `col` (CPL columns at cofs).
+// LM: cache mode of the gathered operand (double only): 0 read-only path,
+// 1 L2 only (cg), 2 L1 no-allocate.  Operators whose gathers rarely hit L1
+// (random columns over a window larger than L1, e.g. the C5 band) spend the
+// L1 data pipe on fills that are never reused; the choice is measured per
+// operator (SpmmVariant SV_LANE_L2 / SV_LANE_NA).
+__device__ __forceinline__ double2 ld_na2(const double* p) {
+    double2 r;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.f64 {%0, %1}, [%2];"
+                 : "=d"(r.x), "=d"(r.y) : "l"(p));
+    return r;
+}
+__device__ __forceinline__ double ld_na1(const double* p) {
+    double r;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(r) : "l"(p));
+    return r;
+}
+template <int CPL, int LM>
+__device__ __forceinline__ Vec<CPL> ld_mode(const double* p) {
+    if constexpr (LM == 0) return load_vec<CPL>(p);
     Vec<CPL> r;
     if constexpr (CPL == 1) {
-        r.v[0] = __ldcg(p);
+        r.v[0] = LM == 1 ? __ldcg(p) : ld_na1(p);
     } else {
 #pragma unroll
         for (int i = 0; i < CPL; i += 2) {
-            double2 t = __ldcg(reinterpret_cast<const double2*>(p + i));
+            const double2 t = LM == 1 ? __ldcg(reinterpret_cast<const double2*>(p + i))
+                                      : ld_na2(p + i);
             r.v[i] = t.x; r.v[i + 1] = t.y;
         }
     }
     return r;
 }
-// !NC: plain (L1-cached) loads -- coherent in the tail kernel because its
-// cluster barrier carries MEMBAR.GPU + CCTL.IVALL (L1 invalidate) in SASS.
-template <int CPL, bool NC>
-__device__ __forceinline__ Vec<CPL> ldv(const double* p) {
-    if constexpr (NC) return load_vec<CPL>(p);
-    else return load_vec_rw<CPL>(p);
-}
-// read-modify-write operands of a row (the thread that reads also writes)
-template <int CPL, bool NC>
-__device__ __forceinline__ Vec<CPL> ldv_rw(const double* p) {
-    return load_vec_rw<CPL>(p);
-}
 
-// Value of the gathered operand at column `col` (CPL columns at cofs).
-template <int OP, int CPL, bool NC = true>
+template <int CPL, typename Tx, int LM = 0>
 __device__ __forceinline__ Vec<CPL> gather(const SpArgs& a, int col, int ld, int cofs) {
-    return ldv<CPL, NC>(a.x + col * ld + cofs);
+    if constexpr (sizeof(Tx) == 8 && LM != 0) return ld_mode<CPL, LM>(a.x + col * ld + cofs);
+    else return ldt<CPL>(tp<Tx>(a.x) + col * ld + cofs);
 }
 
-// Where a row's (column, value) entries come from: global memory (read-only
-// path) or a shared-memory copy (tail kernel).
+// Where a row's (column, value) entries come from (global memory, read-only
+// path); slab-compressed indices add the row's slab base.
 template <typename Tv, typename Ti> struct GSrc {
     const Ti* __restrict__ ci;
     const Tv* __restrict__ v;
@@ -168,17 +251,10 @@ template <typename Tv, typename Ti> struct GSrc {
         return r;
     }
 };
-template <typename Tv, typename Ti> struct SSrc {
-    const Ti* ci;          // shared memory; entry k lives at ci[k - ci_off]
-    const Tv* v;
-    int ci_off, v_off;
-    __device__ __forceinline__ int col(int k) const { return (int)ci[k - ci_off]; }
-    __device__ __forceinline__ double val(int k) const { return widen(v[k - v_off]); }
-};
 
 // Accumulate one row: acc op= sum_k v_k * g(col_k), entry order; the loads
 // of a group of UNR entries are issued before their (ordered) accumulation.
-template <int OP, int CPL, bool SUBTRACT, class Src, int UNR = 4, bool NC = true>
+template <int CPL, bool SUBTRACT, typename Tx, class Src, int UNR = 4, int LM = 0>
 __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, int lo,
                                                int hi, int ld, int cofs,
                                                double (&acc)[CPL]) {
@@ -201,7 +277,7 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
         compiler_fence();   // keep the group's loads issued together (the
                             // scheduler otherwise interleaves them with uses)
 #pragma unroll
-        for (int u = 0; u < UNR; ++u) g[u] = gather<OP, CPL, NC>(a, c[u], ld, cofs);
+        for (int u = 0; u < UNR; ++u) g[u] = gather<CPL, Tx, LM>(a, c[u], ld, cofs);
         compiler_fence();
 #pragma unroll
         for (int u = 0; u < UNR; ++u) {
@@ -219,21 +295,21 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
 // One (row, column-slice) of work for every op, in three parts so that the
 // long-row path (long_row_cta) can run the same prologue / epilogue around a
 // CTA-cooperative accumulation.  row_begin loads the accumulator's start
-// value (and operands the epilogue reuses); `sub` = entries are subtracted.
-template <int OP, int CPL, bool NC = true>
+// value; `subtract` = entries are subtracted.
+template <int OP, int CPL, typename Ty>
 __device__ __forceinline__ void row_begin(const SpArgs& a, int o, double (&acc)[CPL],
-                                          Vec<CPL>& keep, bool& subtract) {
+                                          bool& subtract) {
     if constexpr (OP == OP_SPMV) {
         const int mode = a.mode;
         if (mode == MRS_MODE_ASSIGN) {
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = 0.0;
         } else if (mode == MRS_MODE_RSUB) {
-            Vec<CPL> t = ldv<CPL, NC>(a.b + o);
+            Vec<CPL> t = ldt<CPL>(tp<Ty>(a.b) + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         } else {
-            Vec<CPL> t = ldv_rw<CPL, NC>(a.y + o);
+            Vec<CPL> t = ldt_rw<CPL>(tp<Ty>(a.y) + o);
 #pragma unroll
             for (int i = 0; i < CPL; ++i) acc[i] = t.v[i];
         }
@@ -242,7 +318,7 @@ __device__ __forceinline__ void row_begin(const SpArgs& a, int o, double (&acc)[
         // r = b - A x  (RSUB order: start at b, subtract in entry order); b
         // is re-read by row_end for the fused dot rather than held across
         // the accumulation (4 fewer live registers in the gather loop)
-        Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
+        Vec<CPL> bb = ldt<CPL>(tp<Ty>(a.b) + o);
 #pragma unroll
         for (int i = 0; i < CPL; ++i) acc[i] = bb.v[i];
         subtract = true;
@@ -253,29 +329,33 @@ __device__ __forceinline__ void row_begin(const SpArgs& a, int o, double (&acc)[
     }
 }
 
-template <int OP, int CPL, bool NC = true>
+// Fused dots exist only on double vectors (the Krylov level).
+template <int OP, int CPL, typename Tx, typename Ty>
 __device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double (&acc)[CPL],
-                                        const Vec<CPL>& keep, double (&dotp)[CPL]) {
+                                        double (&dotp)[CPL]) {
+    constexpr bool kDot = sizeof(Tx) == 8 && sizeof(Ty) == 8;
     if constexpr (OP == OP_SPMV) {
         Vec<CPL> out;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) out.v[i] = acc[i];
-        store_vec<CPL>(a.y + o, out);
+        stt<CPL>(tpw<Ty>(a.y) + o, out);
         if (a.seed) {
             const double dd = __ldg(a.d + row);
             const double wt = a.seed == 1 ? a.w : a.theta;
 #pragma unroll
             for (int i = 0; i < CPL; ++i) out.v[i] = seed_value(a.seed, acc[i], dd, wt);
-            store_vec<CPL>(a.seed_out + o, out);
+            stt<CPL>(tpw<Ty>(a.seed_out) + o, out);
         }
-        if (a.dot) {   // (x_in ? x_in : x)_own . y  (x_in: e.g. BiCGStab's r0)
-            Vec<CPL> xo = ldv<CPL, NC>((a.x_in ? a.x_in : a.x) + o);
+        if constexpr (kDot) {
+            if (a.dot) {   // (x_in ? x_in : x)_own . y  (x_in: e.g. BiCGStab's r0)
+                Vec<CPL> xo = ldt<CPL>((a.x_in ? a.x_in : a.x) + o);
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
+                for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
+            }
         }
     } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
         const double dd = __ldg(a.d + row);
-        Vec<CPL> xo = ldv<CPL, NC>(a.x + o);
+        Vec<CPL> xo = ldt<CPL>(tp<Ty>(a.x) + o);
         if constexpr (OP == OP_CHEB_FIRST) {
             const double dt = mul(dd, a.theta);
             Vec<CPL> r, dv;
@@ -285,23 +365,25 @@ __device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double 
                 dv.v[i] = divd(acc[i], dt);                 // dv = r / (d*theta)
                 xo.v[i] = add(xo.v[i], dv.v[i]);            // x + dv
             }
-            if (a.r_out) store_vec<CPL>(a.r_out + o, r);
-            if (a.dv_out) store_vec<CPL>(a.dv_out + o, dv);
+            if (a.r_out) stt<CPL>(tpw<Ty>(a.r_out) + o, r);
+            if (a.dv_out) stt<CPL>(tpw<Ty>(a.dv_out) + o, dv);
         } else {
 #pragma unroll
             for (int i = 0; i < CPL; ++i) xo.v[i] = add(xo.v[i], mul(a.w, divd(acc[i], dd)));  // blas2.py:181
         }
-        store_vec<CPL>(a.x_out + o, xo);
-        if (a.dot) {
-            const Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
+        stt<CPL>(tpw<Ty>(a.x_out) + o, xo);
+        if constexpr (kDot) {
+            if (a.dot) {
+                const Vec<CPL> bb = ldt<CPL>(a.b + o);
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+                for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+            }
         }
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
         const double dd = __ldg(a.d + row);
-        Vec<CPL> r = ldv<CPL, NC>(a.r_in + o);
-        Vec<CPL> dv = ldv<CPL, NC>(a.x + o);
-        Vec<CPL> xo = ldv_rw<CPL, NC>(a.x_in + o);
+        Vec<CPL> r = ldt<CPL>(tp<Ty>(a.r_in) + o);
+        Vec<CPL> dv = ldt<CPL>(tp<Ty>(a.x) + o);
+        Vec<CPL> xo = ldt_rw<CPL>(tp<Ty>(a.x_in) + o);
         Vec<CPL> dvn;
 #pragma unroll
         for (int i = 0; i < CPL; ++i) {
@@ -309,31 +391,32 @@ __device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double 
             dvn.v[i] = add(mul(dv.v[i], a.c1), mul(a.c2, divd(r.v[i], dd)));  // dv*c1 + c2*(r/d)
             xo.v[i] = add(xo.v[i], dvn.v[i]);                                 // x += dv
         }
-        store_vec<CPL>(a.x_out + o, xo);
-        if (a.r_out) store_vec<CPL>(a.r_out + o, r);
-        if (a.dv_out) store_vec<CPL>(a.dv_out + o, dvn);
-        if (a.dot) {
-            Vec<CPL> bb = ldv<CPL, NC>(a.b + o);
+        stt<CPL>(tpw<Ty>(a.x_out) + o, xo);
+        if (a.r_out) stt<CPL>(tpw<Ty>(a.r_out) + o, r);
+        if (a.dv_out) stt<CPL>(tpw<Ty>(a.dv_out) + o, dvn);
+        if constexpr (kDot) {
+            if (a.dot) {
+                Vec<CPL> bb = ldt<CPL>(a.b + o);
 #pragma unroll
-            for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+                for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(bb.v[i], xo.v[i]));
+            }
         }
     }
 }
 
-template <int OP, int CPL, class Src, int UNR = 4, bool NC = true>
+template <int OP, int CPL, typename Tx, typename Ty, class Src, int UNR = 4, int LM = 0>
 __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row, int lo,
                                        int hi, int ld, int cofs, double (&dotp)[CPL]) {
     // 32-bit indices: rows, entries and element offsets < 2^31 (launch checks)
     const int o = row * ld + cofs;
     double acc[CPL];
-    Vec<CPL> keep;
     bool subtract;
-    row_begin<OP, CPL, NC>(a, o, acc, keep, subtract);
+    row_begin<OP, CPL, Ty>(a, o, acc, subtract);
     if (subtract)
-        row_accumulate<OP, CPL, true, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
+        row_accumulate<CPL, true, Tx, Src, UNR, LM>(a, src, lo, hi, ld, cofs, acc);
     else
-        row_accumulate<OP, CPL, false, Src, UNR, NC>(a, src, lo, hi, ld, cofs, acc);
-    row_end<OP, CPL, NC>(a, row, o, acc, keep, dotp);
+        row_accumulate<CPL, false, Tx, Src, UNR, LM>(a, src, lo, hi, ld, cofs, acc);
+    row_end<OP, CPL, Tx, Ty>(a, row, o, acc, dotp);
 }
 
 // A long row (more than a.long_thr entries: AMG coarse operators carry rows
@@ -343,7 +426,7 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row,
 // the same separately rounded mul then add/sub sequence as row_accumulate,
 // so the result is bitwise that of the lane path, but the row's gathers run
 // in parallel instead of as ceil(len/UNR) dependent rounds.
-template <int M, int OP, typename Tv, typename Ti>
+template <int M, int OP, typename Tv, typename Ti, typename Tx, typename Ty>
 __device__ __forceinline__ void long_row_cta(const SpArgs& a, const GSrc<Tv, Ti>& src0, int row,
                                              double (&dotp)[Lay<M>::CPL]) {
     constexpr int CPL = Lay<M>::CPL, LPR = Lay<M>::LPR;
@@ -356,15 +439,14 @@ __device__ __forceinline__ void long_row_cta(const SpArgs& a, const GSrc<Tv, Ti>
     const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
     const int o = row * M + q * CPL;
     double acc[CPL];
-    Vec<CPL> keep;
     bool subtract = false;
-    if (q < LPR) row_begin<OP, CPL>(a, o, acc, keep, subtract);
+    if (q < LPR) row_begin<OP, CPL, Ty>(a, o, acc, subtract);
     for (int k0 = lo; k0 < hi; k0 += EPC) {
         const int ne = min(EPC, hi - k0);
 #pragma unroll 4
         for (int t = threadIdx.x; t < ne * M; t += kThreads) {
             const int e = t / M, c = t % M;
-            s_p[t] = mul(src.val(k0 + e), __ldg(a.x + src.col(k0 + e) * M + c));
+            s_p[t] = mul(src.val(k0 + e), (double)__ldg(tp<Tx>(a.x) + src.col(k0 + e) * M + c));
         }
         __syncthreads();
         if (q < LPR) {
@@ -380,7 +462,7 @@ __device__ __forceinline__ void long_row_cta(const SpArgs& a, const GSrc<Tv, Ti>
         }
         __syncthreads();
     }
-    if (q < LPR) row_end<OP, CPL>(a, row, o, acc, keep, dotp);
+    if (q < LPR) row_end<OP, CPL, Tx, Ty>(a, row, o, acc, dotp);
 }
 
 // CTA-level fixed-shape reduction of the fused-dot partials (warp xor tree
@@ -445,7 +527,7 @@ __device__ __forceinline__ void coop_accumulate(const SpArgs& a, const Src& src,
         if (live && k < len) {
             Vec<CPL> g[LPR];
 #pragma unroll
-            for (int u = 0; u < LPR; ++u) g[u] = load_vec<CPL>(a.x + c[u] * ld + cofs);
+            for (int u = 0; u < LPR; ++u) g[u] = load_vec<CPL>(a.x + c[u] * ld + cofs);   // double only
             compiler_fence();
             if (subtract) {
 #pragma unroll
@@ -469,8 +551,11 @@ __device__ __forceinline__ void coop_accumulate(const SpArgs& a, const Src& src,
 // register-heavy, so only used where few CTAs run anyway.  Same order.
 // COOP: large operators with long rows (coop_accumulate), M in {4, 8, 16}.
 // COOP runs at 4 CTAs/SM (64 registers): its shuffled (column, value) pairs
-// and LPR gathered slices in flight spill at 40.
-template <int M, int OP, typename Tv, typename Ti, bool LONG = false, bool COOP = false>
+// and LPR gathered slices in flight spill at 40.  Tx / Ty: vector types of
+// the gathered operand / the row operands (double, or float levels of the
+// fp32-vector V-cycle; COOP is double only).
+template <int M, int OP, typename Tv, typename Ti, bool LONG = false, bool COOP = false,
+          typename Tx = double, typename Ty = double, int LM = 0>
 __global__ void __launch_bounds__(kThreads, LONG ? 1 : (COOP ? 4 : spmm_min_blocks<M, OP>()))
 spmm_kernel(SpArgs a) {
     pdl_enter();
@@ -488,7 +573,7 @@ spmm_kernel(SpArgs a) {
     if ((int)blockIdx.x >= gl) {
         // long rows: one CTA each (long_row_cta), strided over the long CTAs
         for (int j = (int)blockIdx.x - gl; j < a.n_long; j += a.long_ctas)
-            long_row_cta<M, OP, Tv, Ti>(a, src, __ldg(a.long_rows + j), dotp);
+            long_row_cta<M, OP, Tv, Ti, Tx, Ty>(a, src, __ldg(a.long_rows + j), dotp);
     } else if constexpr (COOP) {
         const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
         for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
@@ -506,11 +591,10 @@ spmm_kernel(SpArgs a) {
                 const GSrc<Tv, Ti> rs = live ? src.at_row(a, row) : src;
                 const int o = row * M + cofs;
                 double acc[CPL];
-                Vec<CPL> keep;
                 bool subtract = false;
-                if (live) row_begin<OP, CPL>(a, o, acc, keep, subtract);
+                if (live) row_begin<OP, CPL, double>(a, o, acc, subtract);
                 coop_accumulate<CPL, LPR>(a, rs, lo, len, M, cofs, live, subtract, acc);
-                if (live) row_end<OP, CPL>(a, row, o, acc, keep, dotp);
+                if (live) row_end<OP, CPL, double, double>(a, row, o, acc, dotp);
             }
         }
     } else {
@@ -521,7 +605,7 @@ spmm_kernel(SpArgs a) {
                 const int row = phys_row(a, v);
                 const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
                 if (hi - lo > lthr) continue;            // done by a long-row CTA
-                do_row<OP, CPL, GSrc<Tv, Ti>, LONG ? 16 : L::UNR>(a, src.at_row(a, row), row, lo, hi,
+                do_row<OP, CPL, Tx, Ty, GSrc<Tv, Ti>, LONG ? 16 : L::UNR, LM>(a, src.at_row(a, row), row, lo, hi,
                                                                   M, cofs, dotp);
             }
         }
@@ -546,7 +630,8 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
             const int r1 = min(r0 + chunk, nrows);
             for (int v = r0 + threadIdx.x / m; v < r1; v += rpb) {
                 const int row = phys_row(a, v);
-                do_row<OP, 1>(a, src.at_row(a, row), row, __ldg(a.rp + row), __ldg(a.rp + row + 1), m,
+                do_row<OP, 1, double, double>(a, src.at_row(a, row), row, __ldg(a.rp + row),
+                                              __ldg(a.rp + row + 1), m,
                               c, dotp);
             }
         }

@@ -386,6 +386,15 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
         desc.mg_cycles = 1 if family == "MultiGrid" else max(pl.get_int("max_iters"), 1)
         desc.pre = _smoother(config.role("pre_smoother"))
         desc.post = _smoother(config.role("post_smoother"))
+        # extension (not in the reference schema): fp32 V-cycle vectors below
+        # level 0 -- the north star's "fp32 preconditioner" (csrc/solver.cu vec32)
+        try:
+            vprec = pl.get_str("mg_vector_precision")
+        except Exception:            # a reference ParamTree has no such key
+            vprec = "fp64"
+        if vprec not in ("fp64", "fp32"):
+            raise InvalidArgumentError(f"mg_vector_precision must be fp64 or fp32, got {vprec!r}")
+        desc.vec32 = int(vprec == "fp32")
         if hierarchy is None:
             params = AmgParams(strength_threshold=pl.get_float("mg_strength_threshold"),
                                agg_num_levels=pl.get_int("mg_agg_num_levels"),

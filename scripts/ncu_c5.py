@@ -1,0 +1,19 @@
+"""One C5 SpMM (n = 2^22, ASSIGN) per variant for an ncu capture:
+    ncu --set full -k regex:spmm_kernel python scripts/ncu_c5.py M VARIANT [VALUES]"""
+import sys, os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_2103_07329_b200 import _lib, kernels as K
+from paper_2103_07329_b200.io import gen_random_sdd
+m, variant = int(sys.argv[1]), int(sys.argv[2])
+vdt = sys.argv[3] if len(sys.argv) > 3 else "f64"
+A = gen_random_sdd()
+vals = A.values if vdt == "f64" else A.values.astype(np.float32)
+D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols, slab=False)
+x = torch.rand(A.ncols, m, dtype=torch.float64, device="cuda")
+y = torch.empty(A.nrows, m, dtype=torch.float64, device="cuda")
+_lib.set_option("spmm_variant", variant)
+for _ in range(2):
+    K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
+torch.cuda.synchronize()
+print("ok")

@@ -60,10 +60,10 @@ def main():
                             + 2 * A.nrows * m * 8)
                     row = {"op": name, "values": vdt, "idx": "u16slab" if nslab else f"u{8*ib}",
                            "m": m, "bytes": byts}
-                    for v, vn in ((1, "lane"), (2, "coop"), (3, "long")):
+                    for v, vn in ((1, "lane"), (2, "coop"), (3, "long"), (4, "l2"), (5, "na")):
                         if v == 2 and m not in (4, 8, 16):
                             continue
-                        if v == 3 and m > 16:
+                        if v in (3, 4, 5) and m > 16:
                             continue
                         _lib.set_option("spmm_variant", v)
                         t = timed(D, x, y)
