@@ -629,14 +629,20 @@ def main():
              torch.empty_like(Rd)) for _ in range(nset)]
     for (Dk, Xk, Bk, Rk) in sets:
         K.csr_spmv(Dk, None, None, Xk, Rk, K.MODE_RSUB, Bk)
+    # the 4 x NSET launches are captured into one CUDA graph and replayed: the
+    # host's per-call overhead (ctypes, ~10-20 us) never gaps the device
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        for _r in range(4):
+            for (Dk, Xk, Bk, Rk) in sets:
+                K.csr_spmv(Dk, None, None, Xk, Rk, K.MODE_RSUB, Bk)
     srounds, skts = 5, []
     for _ in range(srounds):
         flush_l2()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
-        for _r in range(4):
-            for (Dk, Xk, Bk, Rk) in sets:
-                K.csr_spmv(Dk, None, None, Xk, Rk, K.MODE_RSUB, Bk)
+        graph.replay()
         e1.record()
         torch.cuda.synchronize()
         skts.append(e0.elapsed_time(e1) * 1e-3 / (4 * nset))
@@ -658,9 +664,9 @@ def main():
                       f"{'(slab)' if nslab else ''}> "
                       f"on the fine-level operator A0 ({args.config})",
             "algorithmic_bytes": kbytes, "us_per_launch": kt * 1e6, "peak_source": peak_src,
-            "timing": f"average over back-to-back launches rotating {nset} independent cold copies "
-                      f"of matrix + operands (CUDA events on the launch stream, median of "
-                      f"{srounds} rounds of {4 * nset})",
+            "timing": f"average over back-to-back launches (one captured CUDA graph) rotating "
+                      f"{nset} independent cold copies of matrix + operands (CUDA events on the "
+                      f"launch stream, median of {srounds} rounds of {4 * nset})",
             "us_per_launch_isolated": kt_cold * 1e6,
             "frac_isolated": kbytes / kt_cold / 1e9 / peak}
 

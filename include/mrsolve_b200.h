@@ -269,7 +269,10 @@ int  mrs_plan_set_interior(mrs_plan* p, int32_t l, int32_t which, int64_t ilo, i
 double mrs_plan_iteration_bytes(const mrs_plan* p);
 /* Warm per-launch device times (us) of one iteration body, each launch
  * bracketed by CUDA events (diagnostics; call after one mrs_plan_solve). */
-int  mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32_t cap,
+/* B: right-hand sides (device, nrows x m) to profile with, or NULL = the plan's
+ * staging buffer (the last host / staged solve's B). */
+int  mrs_plan_profile(mrs_plan* p, const double* B, int32_t iters, void* stream, double* us,
+                      int32_t cap,
                       int32_t* count);
 /* Diagnostics: kernel name (mangled) of iteration-body launch `idx` (the
  * order of mrs_plan_profile). */
@@ -321,9 +324,14 @@ int  mrs_version(void);
  *                   1 = operators with >= 12 entries per row (outside the LONG range),
  *                   2 = (default) only long uniform rows (>= 20 per row, max <= 1.1 x mean;
  *                   27-point stencils), 0 = off
- *   "spmm_variant" 0..3  force one SpMM variant for every operator (A/B runs):
+ *   "spmm_variant" 0..5  force one SpMM variant for every operator (A/B runs):
  *                   0 = per operator (default), 1 = lane, 2 = cooperative loads,
- *                   3 = 16 entries in flight
+ *                   3 = 16 entries in flight, 4 = gathers through L2 only,
+ *                   5 = gathers with L1::no_allocate
+ *   "spmm_autotune" 0/1  plugin calls: measure the variants of an operator on its
+ *                   first call per m (default 1; env MRS_SPMM_AUTOTUNE)
+ *   "plan_autotune" 0/1  solver plans: the same measurement for every level
+ *                   operator at finalize (default 0: the shape heuristic)
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
 int  mrs_set_option(const char* key, int64_t value);
 

@@ -93,7 +93,8 @@ SIGNATURES = {
     "mrs_plan_solve": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
                                  C.c_void_p, C.POINTER(mrs_stats), C.c_void_p, C.c_void_p]),
     "mrs_plan_iteration_bytes": (C.c_double, [C.c_void_p]),
-    "mrs_plan_profile": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_int32,
+    "mrs_plan_profile": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                   C.c_int32,
                                    C.POINTER(C.c_int32)]),
     "mrs_plan_kernel_count": (C.c_int, [C.c_void_p]),
     "mrs_plan_launch_name": (C.c_int, [C.c_void_p, C.c_int32, C.c_char_p, C.c_int32]),

@@ -92,9 +92,14 @@ int plugin_variant(const DevCsr& D, const double* x, int64_t m, cudaStream_t s) 
         cudaGetLastError();
         return SV_AUTO;
     }
-    const int v = spmm_tune(D, x, scratch, m, s);
+    const int64_t fn = (160ll << 20) / 8;           // cold-cache tuning (see spmm_tune)
+    double* flush = nullptr;
+    if (cudaMalloc(&flush, fn * 8) != cudaSuccess) { cudaGetLastError(); flush = nullptr; }
+    else cudaMemsetAsync(flush, 0, fn * 8, s);
+    const int v = spmm_tune(D, x, scratch, m, s, nullptr, VP_DD, flush, flush ? fn : 0);
     cudaStreamSynchronize(s);
     cudaFree(scratch);
+    if (flush) cudaFree(flush);
     std::lock_guard<std::mutex> lk(g_tune_mu);
     g_tuned[k] = v;
     return v;
@@ -138,6 +143,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_long_rows")) { set_spmm_long_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_chunk_rows")) { set_spmm_chunk_rows(value); return MRS_OK; }
     if (!strcmp(key, "spmm_long_split")) { set_spmm_long_split(value); return MRS_OK; }
+    if (!strcmp(key, "plan_autotune")) { set_plan_autotune(value); return MRS_OK; }
     if (!strcmp(key, "spmm_autotune")) { set_spmm_autotune(value); return MRS_OK; }
     if (!strcmp(key, "spmm_variant")) { set_spmm_variant(value); return MRS_OK; }
     if (!strcmp(key, "halo_overlap")) { set_halo_overlap(value); return MRS_OK; }

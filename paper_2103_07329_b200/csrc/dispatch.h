@@ -57,9 +57,14 @@ void set_dense_mma(int64_t v);
 int64_t spmm_long_split();
 int64_t halo_overlap();
 // per-operator SpMM variant by measurement (kernels.cu); knob spmm_autotune
+// flush: an L2-sized device buffer read before every timed launch (cold
+// conditions), or null
 int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
-              float* best_us = nullptr, int vp = 0);
+              float* best_us = nullptr, int vp = 0, const double* flush = nullptr,
+              int64_t flush_n = 0);
 int64_t spmm_autotune_enabled();
+int64_t plan_autotune();
+void set_plan_autotune(int64_t v);
 void set_spmm_autotune(int64_t v);
 void set_spmm_variant(int64_t v);
 int64_t spmm_variant();

@@ -69,6 +69,23 @@ inline void wave_grid(const void* fn, int64_t nrows, int64_t rows_per_pass, int&
 }
 
 
+// Shape heuristic (the default when an operator carries no measured choice):
+// small operators with long rows -> LONG (16 entries in flight); large
+// operators with long AND uniform rows (27-point stencils: mean >= 20, no row
+// more than ~10 % above it) -> COOP (knob spmm_coop: 1 = every operator with
+// >= 12 entries per row); otherwise LANE.  Set by hand on whole solves in
+// round 1 (profiles/r01_ab_experiments.txt).
+inline int spmm_shape_variant(int64_t nr, int64_t nnz, int max_row, int64_t m) {
+    const int64_t coop = spmm_coop();
+    const bool uniform_long = nnz >= 20 * nr && max_row > 0 &&
+                              (int64_t)max_row * 10 * nr <= 11 * nnz + 10 * nr;
+    if (m <= 16 && nr <= spmm_long_max_rows() && nnz >= 12 * nr) return SV_LONG;
+    if ((m == 4 || m == 8 || m == 16) &&
+        ((coop == 1 && nnz >= 12 * nr) || (coop == 2 && uniform_long)))
+        return SV_COOP;
+    return SV_LANE;
+}
+
 // SpMM family: chunk-strided one-wave grid (see spmm.cuh).  Tx / Ty: vector
 // types (double, or the float levels of the fp32-vector V-cycle: lane and
 // LONG variants, m in {1, 2, 4, 8, 16, 32}).
@@ -100,19 +117,8 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
                              a.long_ctas ? kLongProducts * sizeof(double) : 0, s, a);
     };
     int v = a.variant ? a.variant : (int)spmm_variant();
-    if (v == SV_AUTO) {
-        // shape heuristic: small operators with long rows -> LONG (16 entries
-        // in flight); large operators with long AND uniform rows (27-point
-        // stencils: mean >= 20, no row more than ~10 % above it) -> COOP
-        // (knob spmm_coop: 1 = every operator with >= 12 entries per row)
-        const int64_t nr = a.rows_hint;      // the whole operator, not a split subset
-        const int64_t coop = spmm_coop();
-        const bool uniform_long = a.nnz_hint >= 20 * nr && a.max_row_hint > 0 &&
-                                  (int64_t)a.max_row_hint * 10 * nr <= 11 * a.nnz_hint + 10 * nr;
-        if (m <= 16 && nr <= spmm_long_max_rows() && a.nnz_hint >= 12 * nr) v = SV_LONG;
-        else if ((coop == 1 && a.nnz_hint >= 12 * nr) || (coop == 2 && uniform_long)) v = SV_COOP;
-        else v = SV_LANE;
-    }
+    if (v == SV_AUTO)
+        v = spmm_shape_variant(a.rows_hint, a.nnz_hint, a.max_row_hint, m);
     if (!generic && v == SV_LONG) {
         switch (m) {
         case 1: go(spmm_kernel<1, OP, Tv, Ti, true, false, Tx, Ty>, Lay<1>::RPB); return cudaGetLastError();

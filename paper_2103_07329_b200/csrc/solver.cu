@@ -230,7 +230,31 @@ struct Builder {
         if (!P->dist || P->overlap == 0 || !h) return false;
         if (P->overlap == 1 && !(h->active() || P->comm->loop)) return false;
         const int64_t min_rows = P->overlap == 2 ? 1 : kMinOverlapRows;
-        return h->ihi - h->ilo >= min_rows && h->ihi <= A.nrows;
+        if (A.n_long) return false;          // long-row CTAs index absolute rows
+        const auto [ilo, ihi] = interior(A);
+        return ihi - ilo >= min_rows && ihi <= A.nrows;
+    }
+    // the interior range rounded inward to slab boundaries (split launches
+    // start on a slab: their slab-base table is offset, not re-indexed)
+    static std::pair<int64_t, int64_t> interior(const DevCsr& A) {
+        int64_t ilo = A.halo->ilo, ihi = A.halo->ihi;
+        if (A.slab_base) {
+            const int64_t q = 1ll << A.slab_shift;
+            ilo = (ilo + q - 1) / q * q;
+            ihi = ihi / q * q;
+            if (ihi < ilo) ihi = ilo;
+        }
+        return {ilo, ihi};
+    }
+    // A fused dot of a distributed SpMM leaves kDotSets partial sets (one per
+    // launch of a split product, empty sets zeroed), on every rank whether or
+    // not its own product splits; the epilogue sums them in set order.
+    static constexpr int kDotSets = 3;
+    void zero_sets(int first, int last) {           // partial sets [first, last)
+        if (first >= last) return;
+        double* p0 = P->red_out + (int64_t)first * P->m;
+        const size_t nb = sizeof(double) * (size_t)(last - first) * P->m;
+        out->push_back([=](cudaStream_t s) { return cudaMemsetAsync(p0, 0, nb, s); });
     }
     void spmm(int op, const DevCsr& A, SpArgs a, double extra_bytes) {
         a.guard = guard;
@@ -242,14 +266,8 @@ struct Builder {
             const int mk = a.dot ? split_reduction(a.red) : 0;
             out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
             if (a.dot && mk < 0 && P->overlap) {
-                // the reduction has the shape of a split product on every rank
-                // (whether a rank splits depends on its own interior range):
-                // an empty second partial set
-                double* set1 = P->red_out + m;
-                out->push_back([=](cudaStream_t s) {
-                    return cudaMemsetAsync(set1, 0, sizeof(double) * m, s);
-                });
-                post_reduction(mk, (int)m, 2);
+                zero_sets(1, kDotSets);                 // the shape of a split product
+                post_reduction(mk, (int)m, kDotSets);
             } else if (a.dot) {
                 post_reduction(mk, (int)m);
             }
@@ -258,10 +276,9 @@ struct Builder {
         bytes += A.bytes() + extra_bytes;
     }
     // pack (compute stream) -> transfer (comm stream) || interior rows
-    // (compute stream) -> join -> boundary rows.  Every row is computed by
-    // exactly one launch in its own entry order: results are those of the
-    // unsplit product.  A fused dot leaves one partial set per launch; both
-    // sets are all-reduced and summed in set order by the epilogue.
+    // [ilo, ihi) (compute stream) -> join -> boundary rows [0, ilo) and
+    // [ihi, n).  Every row is computed by exactly one launch in its own entry
+    // order: results are those of the unsplit product.
     void spmm_overlapped(int op, const DevCsr& A, SpArgs a) {
         const Halo* h = A.halo;
         const mrs_comm* c = P->comm;
@@ -279,31 +296,29 @@ struct Builder {
             return e;
         });
         const int mk = a.dot ? split_reduction(a.red) : 0;
-        const int ilo = (int)h->ilo, ihi = (int)h->ihi, n = (int)A.nrows;
-        if (ihi - ilo == n) {            // no boundary rows: one launch after the join
-            out->push_back([=](cudaStream_t s) { return cudaStreamWaitEvent(s, ev_comm, 0); });
-            out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, a, m, s); });
-            if (a.dot && mk < 0) {
-                double* set1 = P->red_out + m;
-                out->push_back([=](cudaStream_t s) {
-                    return cudaMemsetAsync(set1, 0, sizeof(double) * m, s);
-                });
-                post_reduction(mk, (int)m, 2);
+        const auto [ilo, ihi] = interior(A);
+        const int64_t n = A.nrows;
+        const int64_t range[3][2] = {{ilo, ihi}, {0, ilo}, {ihi, n}};
+        int last = 0;                                     // the last launch takes the long rows
+        for (int k = 0; k < 3; ++k)
+            if (range[k][1] > range[k][0]) last = k;
+        for (int k = 0; k < 3; ++k) {
+            if (k == 1)                                   // boundary rows need the halo
+                out->push_back([=](cudaStream_t s) { return cudaStreamWaitEvent(s, ev_comm, 0); });
+            const int64_t r0 = range[k][0], r1 = range[k][1];
+            if (r1 <= r0) {
+                if (a.dot && mk < 0) zero_sets(k, k + 1);
+                continue;
             }
+            SpArgs ak = a;
+            ak.row0 = r0;
+            ak.vrows = r1 - r0;
+            ak.no_long_ctas = k != last;
+            if (a.dot) ak.red.out = a.red.out + k * m;    // partial set k
+            out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, ak, m, s); });
             kernels++;
-            return;
         }
-        SpArgs ai = a, ab = a;
-        ai.row_base = ilo; ai.row_split = 0x7fffffff; ai.row_gap = 0; ai.vrows = ihi - ilo;
-        ai.no_long_ctas = 1;
-        ab.row_base = 0; ab.row_split = ilo; ab.row_gap = ihi - ilo;
-        ab.vrows = n - (ihi - ilo);
-        if (a.dot) ab.red.out = a.red.out + m;          // second partial set
-        out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, ai, m, s); });
-        out->push_back([=](cudaStream_t s) { return cudaStreamWaitEvent(s, ev_comm, 0); });
-        out->push_back([=](cudaStream_t s) { return launch_spmm(op, A, ab, m, s); });
-        if (a.dot) post_reduction(mk, (int)m, 2);
-        kernels += 2;
+        if (a.dot) post_reduction(mk, (int)m, kDotSets);
     }
     void vec(int op, VArgs a, double b) {
         a.guard = a.guard ? a.guard : guard;
@@ -1162,7 +1177,11 @@ static int build_sgs_schedule(const mrs_host_csr* h, LevelDev& lv, std::vector<v
 // multiplies with (A_l, R_l, P_l) gets the variant that ran fastest for it
 // at the plan's m.  Scratch contents are overwritten later anyway.
 void tune_operators(mrs_plan* p) {
-    if (!spmm_autotune_enabled()) return;
+    // measured per-operator choice only on request (knob plan_autotune): an
+    // isolated cold launch mispredicts the operator inside a solve (A/B: C2
+    // 2.43 -> 2.50 ms with it, profiles/r02_spmm_variants.txt); plans keep the
+    // shape heuristic, plugin calls (a product on its own) are measured
+    if (!spmm_autotune_enabled() || !plan_autotune()) return;
     cudaStream_t s;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return;
     const int64_t m = p->m;
@@ -1170,6 +1189,13 @@ void tune_operators(mrs_plan* p) {
         if (buf) cudaMemsetAsync(buf, 0, (f32 ? 4 : 8) * (size_t)rows * m, s);
     };
     const bool mg = p->desc.precond == MRS_PC_MG;
+    // cold-cache conditions: an L2-sized read between tuning launches (the
+    // solve streams far more than L2 between two uses of one operator)
+    const int64_t fn = (160ll << 20) / 8;
+    double* flush = nullptr;
+    if (cudaMalloc(&flush, fn * 8) != cudaSuccess) { cudaGetLastError(); flush = nullptr; }
+    else cudaMemsetAsync(flush, 0, fn * 8, s);
+    const int64_t fl = flush ? fn : 0;
     for (size_t l = 0; l < p->L.size(); ++l) {
         LevelDev& lv = p->L[l];
         if (l > 0 && !mg) break;
@@ -1178,19 +1204,22 @@ void tune_operators(mrs_plan* p) {
         const bool f = lv.f32;
         zero(x, lv.vrows, f);
         if (lv.A.present() && x && y)
-            lv.A.variant = spmm_tune(lv.A, x, y, m, s, nullptr, Builder::vp(f, f));
+            lv.A.variant = spmm_tune(lv.A, x, y, m, s, nullptr, Builder::vp(f, f), flush, fl);
         if (!mg || l + 1 >= p->L.size()) continue;
         LevelDev& lc = p->L[l + 1];
         if (lv.R.present() && lv.r && lc.b) {
             zero(lv.r, lv.vrows, f);
-            lv.R.variant = spmm_tune(lv.R, lv.r, lc.b, m, s, nullptr, Builder::vp(f, lc.f32));
+            lv.R.variant = spmm_tune(lv.R, lv.r, lc.b, m, s, nullptr, Builder::vp(f, lc.f32),
+                                     flush, fl);
         }
         if (lv.P.present() && lc.xa && lv.r) {
             zero(lc.xa, lc.vrows, lc.f32);
-            lv.P.variant = spmm_tune(lv.P, lc.xa, lv.r, m, s, nullptr, Builder::vp(lc.f32, f));
+            lv.P.variant = spmm_tune(lv.P, lc.xa, lv.r, m, s, nullptr, Builder::vp(lc.f32, f),
+                                     flush, fl);
         }
     }
     cudaStreamSynchronize(s);
+    if (flush) cudaFree(flush);
     cudaStreamDestroy(s);
     cudaGetLastError();
 }
@@ -1346,7 +1375,10 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
             // single GPU, Jacobi / Chebyshev smoothing (the Gauss-Seidel sweep
             // and the dense kernels stay double)
             const mrs_plan_desc& d = p->desc;
-            if (p->dist || d.pre.kind == MRS_SMOOTH_SGS || d.post.kind == MRS_SMOOTH_SGS)
+            // (PBiCGStab's pipelined recurrences need a linear preconditioner:
+            // float rounding inside M makes them drift past its instability check)
+            if (p->dist || d.pre.kind == MRS_SMOOTH_SGS || d.post.kind == MRS_SMOOTH_SGS ||
+                d.method == MRS_METHOD_PBICGSTAB)
                 return MRS_ERR_UNSUPPORTED;
             if (p->m > 32 || (p->m & (p->m - 1)) != 0) return MRS_ERR_UNSUPPORTED;
             const int end = p->dense_from >= 1 ? p->dense_from : (int)p->L.size() - 1;
@@ -1638,13 +1670,15 @@ double mrs_plan_iteration_bytes(const mrs_plan* p) { return p ? p->it_bytes : 0.
 // iterations (warm caches, realistic data), each launch of the body is
 // captured R times back-to-back into its own graph and timed with CUDA
 // events; us[i] = device time per launch (no host launch gaps).
-int mrs_plan_profile(mrs_plan* p, int32_t iters, void* stream, double* us, int32_t cap,
+int mrs_plan_profile(mrs_plan* p, const double* B, int32_t iters, void* stream, double* us,
+                     int32_t cap,
                      int32_t* count) {
     if (!p || !p->finalized || !us || !count || iters < 1) return MRS_ERR_ARG;
     cudaStream_t s = (cudaStream_t)stream;
     Program pg;
     build_program(p, true, pg);
     const size_t bytes = (size_t)p->n * p->m * 8;
+    if (B) MRS_CUDA_OK(cudaMemcpyAsync(p->B, B, bytes, cudaMemcpyDeviceToDevice, s));
     MRS_CUDA_OK(cudaMemsetAsync(p->X, 0, bytes, s));
     set_cond_kernel<<<1, 1, 0, s>>>(p->st, 0, 0);
     MRS_CUDA_OK(run_list(pg.pro, s));

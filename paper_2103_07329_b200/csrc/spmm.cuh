@@ -94,23 +94,23 @@ struct SpArgs {
     const int32_t* long_rows;  // rows with more than long_thr entries (one CTA each)
     int n_long, long_thr, long_ctas;   // long_ctas: trailing CTAs of the grid doing them
     int max_row_hint;          // longest row (0: unknown) -- layout choice
-    // row subset of a split launch (multi-GPU halo overlap): the kernel walks
-    // virtual rows v < nrows and works on row_base + v (+ row_gap once
-    // v >= row_split); all zero = every row.  vrows: the subset's row count
-    // (0 = the matrix's).  no_long_ctas: this launch leaves the long rows to
-    // the other launch of the split (the lane path still skips them).
-    int row_base, row_split, row_gap, no_long_ctas;
+    // row range of a split launch (multi-GPU halo overlap): rows
+    // [row0, row0 + vrows) (vrows 0 = every row).  HOST-side only: the
+    // launcher offsets every row-indexed pointer by row0 and the kernel walks
+    // rows 0 .. vrows-1 -- a row offset inside the kernel's loop (even only in
+    // its bounds) measured 9-10 % slower on the 7-point SpMM.  xo: the
+    // gathered operand's own-row view (x + row0 * m; = x when unsplit).
+    // no_long_ctas: this launch leaves the long rows to another launch.
+    int64_t row0;
+    int no_long_ctas;
     int64_t vrows;
+    const double* xo;
     int64_t rows_hint;      // the operator's row count (variant choice)
     int variant;            // SpmmVariant forced for this operator (0 = heuristic)
     int vp;                 // vector precision (VP_*: fp32-vector V-cycle levels)
     RedArgs red;
 };
 
-// Physical row of virtual row v (split launches; identity otherwise).
-__device__ __forceinline__ int phys_row(const SpArgs& a, int v) {
-    return a.row_base + v + (v >= a.row_split ? a.row_gap : 0);
-}
 // shared-memory products per chunk of a long row (long_row_cta)
 constexpr int kLongProducts = 2048;
 
@@ -348,14 +348,14 @@ __device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double 
         }
         if constexpr (kDot) {
             if (a.dot) {   // (x_in ? x_in : x)_own . y  (x_in: e.g. BiCGStab's r0)
-                Vec<CPL> xo = ldt<CPL>((a.x_in ? a.x_in : a.x) + o);
+                Vec<CPL> xo = ldt<CPL>((a.x_in ? a.x_in : a.xo) + o);
 #pragma unroll
                 for (int i = 0; i < CPL; ++i) dotp[i] = add(dotp[i], mul(xo.v[i], acc[i]));
             }
         }
     } else if constexpr (OP == OP_JAC_SWEEP || OP == OP_CHEB_FIRST) {
         const double dd = __ldg(a.d + row);
-        Vec<CPL> xo = ldt<CPL>(tp<Ty>(a.x) + o);
+        Vec<CPL> xo = ldt<CPL>(tp<Ty>(a.xo) + o);
         if constexpr (OP == OP_CHEB_FIRST) {
             const double dt = mul(dd, a.theta);
             Vec<CPL> r, dv;
@@ -382,7 +382,7 @@ __device__ __forceinline__ void row_end(const SpArgs& a, int row, int o, double 
     } else {  // OP_CHEB_STEP  (solvers.py:559-571)
         const double dd = __ldg(a.d + row);
         Vec<CPL> r = ldt<CPL>(tp<Ty>(a.r_in) + o);
-        Vec<CPL> dv = ldt<CPL>(tp<Ty>(a.x) + o);
+        Vec<CPL> dv = ldt<CPL>(tp<Ty>(a.xo) + o);
         Vec<CPL> xo = ldt_rw<CPL>(tp<Ty>(a.x_in) + o);
         Vec<CPL> dvn;
 #pragma unroll
@@ -550,13 +550,14 @@ __device__ __forceinline__ void coop_accumulate(const SpArgs& a, const Src& src,
 // 16 entries in flight per lane -- the row's dependent chain is 4x shorter;
 // register-heavy, so only used where few CTAs run anyway.  Same order.
 // COOP: large operators with long rows (coop_accumulate), M in {4, 8, 16}.
-// COOP runs at 4 CTAs/SM (64 registers): its shuffled (column, value) pairs
-// and LPR gathered slices in flight spill at 40.  Tx / Ty: vector types of
+// COOP keeps the lane path's occupancy floor: at 4 CTAs/SM (no spills) the
+// isolated product is faster, but whole C4 solves ran 2.8 % slower (A/B,
+// profiles/r02_spmm_variants.txt).  Tx / Ty: vector types of
 // the gathered operand / the row operands (double, or float levels of the
 // fp32-vector V-cycle; COOP is double only).
 template <int M, int OP, typename Tv, typename Ti, bool LONG = false, bool COOP = false,
           typename Tx = double, typename Ty = double, int LM = 0>
-__global__ void __launch_bounds__(kThreads, LONG ? 1 : (COOP ? 4 : spmm_min_blocks<M, OP>()))
+__global__ void __launch_bounds__(kThreads, LONG ? 1 : spmm_min_blocks<M, OP>())
 spmm_kernel(SpArgs a) {
     pdl_enter();
     if (a.guard && *a.guard) return;
@@ -568,7 +569,8 @@ spmm_kernel(SpArgs a) {
     double dotp[CPL];
 #pragma unroll
     for (int i = 0; i < CPL; ++i) dotp[i] = 0.0;
-    const int nrows = (int)a.nrows, chunk = (int)a.chunk;
+    const int chunk = (int)a.chunk;
+    const int rbeg = 0, rend = (int)a.nrows;
     const int gl = (int)gridDim.x - a.long_ctas;   // CTAs of the lane path
     if ((int)blockIdx.x >= gl) {
         // long rows: one CTA each (long_row_cta), strided over the long CTAs
@@ -576,13 +578,12 @@ spmm_kernel(SpArgs a) {
             long_row_cta<M, OP, Tv, Ti, Tx, Ty>(a, src, __ldg(a.long_rows + j), dotp);
     } else if constexpr (COOP) {
         const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
-        for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
-            const int r1 = min(r0 + chunk, nrows);
+        for (int r0 = rbeg + blockIdx.x * chunk; r0 < rend; r0 += gl * chunk) {
+            const int r1 = min(r0 + chunk, rend);
             for (int rb = r0; rb < r1; rb += RPB) {            // warp-uniform passes
-                const int v = rb + threadIdx.x / LPR;
-                const int row = phys_row(a, v);
+                const int row = rb + threadIdx.x / LPR;
                 int lo = 0, len = 0;
-                bool live = v < r1;
+                bool live = row < r1;
                 if (live) {
                     lo = __ldg(a.rp + row);
                     len = __ldg(a.rp + row + 1) - lo;
@@ -599,10 +600,9 @@ spmm_kernel(SpArgs a) {
         }
     } else {
         const int lthr = a.n_long ? a.long_thr : 0x7fffffff;
-        for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gl * chunk) {
-            const int r1 = min(r0 + chunk, nrows);
-            for (int v = r0 + threadIdx.x / LPR; v < r1; v += RPB) {
-                const int row = phys_row(a, v);
+        for (int r0 = rbeg + blockIdx.x * chunk; r0 < rend; r0 += gl * chunk) {
+            const int r1 = min(r0 + chunk, rend);
+            for (int row = r0 + threadIdx.x / LPR; row < r1; row += RPB) {
                 const int lo = __ldg(a.rp + row), hi = __ldg(a.rp + row + 1);
                 if (hi - lo > lthr) continue;            // done by a long-row CTA
                 do_row<OP, CPL, Tx, Ty, GSrc<Tv, Ti>, LONG ? 16 : L::UNR, LM>(a, src.at_row(a, row), row, lo, hi,
@@ -625,11 +625,11 @@ __global__ void __launch_bounds__(kThreads) spmm_kernel_generic(SpArgs a) {
     const GSrc<Tv, Ti> src{reinterpret_cast<const Ti*>(a.ci), reinterpret_cast<const Tv*>(a.vals)};
     double dotp[1] = {0.0};
     if (threadIdx.x < rpb * m) {
-        const int nrows = (int)a.nrows, chunk = (int)a.chunk;
-        for (int r0 = blockIdx.x * chunk; r0 < nrows; r0 += gridDim.x * chunk) {
-            const int r1 = min(r0 + chunk, nrows);
-            for (int v = r0 + threadIdx.x / m; v < r1; v += rpb) {
-                const int row = phys_row(a, v);
+        const int chunk = (int)a.chunk;
+        const int rbeg = 0, rend = (int)a.nrows;
+        for (int r0 = rbeg + blockIdx.x * chunk; r0 < rend; r0 += gridDim.x * chunk) {
+            const int r1 = min(r0 + chunk, rend);
+            for (int row = r0 + threadIdx.x / m; row < r1; row += rpb) {
                 do_row<OP, 1, double, double>(a, src.at_row(a, row), row, __ldg(a.rp + row),
                                               __ldg(a.rp + row + 1), m,
                               c, dotp);

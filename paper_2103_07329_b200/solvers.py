@@ -187,12 +187,16 @@ class DevicePlan:
     def kernels_per_iteration(self) -> int:
         return self.L.mrs_plan_kernel_count(self.h)
 
-    def profile(self, iters: int = 3) -> np.ndarray:
-        """Warm per-launch times (us) of one iteration body (diagnostics)."""
+    def profile(self, iters: int = 3, B=None) -> np.ndarray:
+        """Warm per-launch times (us) of one iteration body (diagnostics).
+        ``B``: CUDA tensor of right-hand sides (None: the plan's staging copy,
+        i.e. the last solve run from host buffers)."""
         import torch
         out = np.zeros(512)
         n = C.c_int32()
-        _lib.check(self.L.mrs_plan_profile(self.h, iters, C.c_void_p(torch.cuda.current_stream().cuda_stream),
+        bp = C.c_void_p(B.data_ptr()) if B is not None else None
+        _lib.check(self.L.mrs_plan_profile(self.h, bp, iters,
+                                           C.c_void_p(torch.cuda.current_stream().cuda_stream),
                                            out.ctypes.data, 512, C.byref(n)), "profile")
         return out[:n.value].copy()
 

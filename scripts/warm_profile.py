@@ -29,8 +29,8 @@ def main():
     cs = prepare(tree(bench.ROLES), A)
     cs.run(B, X, x_is_zero=True)
     plan = cs.plan_factory(bench.M)
-    t = plan.profile(3)
-    t = plan.profile(3)
+    t = plan.profile(3, B)
+    t = plan.profile(3, B)
     import re
     vec_ops = ["axpby", "add2", "paired", "dot", "update_dot", "update_dot2", "copy",
                "cg_update", "cg_update_jac", "p_update", "seed", "bicg_p", "bicg_s", "dot3",

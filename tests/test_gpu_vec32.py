@@ -43,7 +43,7 @@ CASES = {
     "c3_shrunk": (lambda: gen_poisson3d(40, 40, 40)[0], 16, "BiCGStab", CHEB, "1"),
     "c2_shrunk": (lambda: gen_poisson3d(32, 32, 32)[0], 8, "CG", JAC, "0"),
     "s27": (lambda: gen_stencil27_aniso(24, seed=4), 8, "CG", JAC, "0"),
-    "pbicgstab_m4": (lambda: gen_poisson3d(24, 24, 24)[0], 4, "PBiCGStab", CHEB, "0"),
+    "rbicgstab_m4": (lambda: gen_poisson3d(24, 24, 24)[0], 4, "RBiCGStab", CHEB, "0"),
     "cg_m1": (lambda: gen_poisson3d(24, 24, 24)[0], 1, "CG", JAC, "0"),
 }
 
@@ -98,6 +98,8 @@ def test_vec32_unsupported_combinations_raise():
     B = np.random.default_rng(1).uniform(-1, 1, (A.nrows, 3))
     with pytest.raises(ConfigurationError):          # m not a power of two
         solve(A, B, roles("CG", JAC, "fp32"))
+    with pytest.raises(ConfigurationError):          # pipelined: needs a linear M
+        solve(A, B[:, :2].copy(), roles("PBiCGStab", JAC, "fp32"))
     r = roles("CG", JAC, "fp32")
     del r["pre_smoother"], r["post_smoother"]         # default Gauss-Seidel smoothing
     with pytest.raises(ConfigurationError):
