@@ -13,7 +13,9 @@ from .errors import (BreakdownError, ConfigurationError, DeviceError, Instabilit
                      InvalidArgumentError, SetupDegeneracyError, SingularDiagonalError)
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIBPATH = os.path.join(HERE, "libmrsolve_b200.so")
+# MRS_LIB: an alternative build of the same library (the checked variant,
+# MRS_CHECKS=1 python -m paper_2103_07329_b200.build); default the in-tree one
+LIBPATH = os.environ.get("MRS_LIB") or os.path.join(HERE, "libmrsolve_b200.so")
 
 MRS_OK, MRS_ERR_ARG, MRS_ERR_CUDA, MRS_ERR_UNSUPPORTED, MRS_ERR_ALLOC = 0, 1, 2, 3, 4
 MRS_ERR_BREAKDOWN, MRS_ERR_SINGULAR, MRS_ERR_DEGENERATE, MRS_ERR_STATE = 5, 6, 7, 8

@@ -21,11 +21,14 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
-LIB = os.path.join(HERE, "libmrsolve_b200.so")
-BUILD = os.path.join(ROOT, "build", "mrsolve_b200")
+# MRS_CHECKS=1: the checked variant (device asserts, see csrc/common.cuh)
+CHECKED = os.environ.get("MRS_CHECKS", "0") == "1"
+LIB = os.path.join(HERE, "libmrsolve_b200_checked.so" if CHECKED else "libmrsolve_b200.so")
+BUILD = os.path.join(ROOT, "build", "mrsolve_b200_checked" if CHECKED else "mrsolve_b200")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
+NVCC_FLAGS = (["-DMRS_CHECKS"] if os.environ.get("MRS_CHECKS", "0") == "1" else []) + [
+              "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
               "-Xptxas", "-warn-spills"]
 CXX_FLAGS = ["-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-std=c++17"]
 

@@ -19,6 +19,7 @@ __global__ void __launch_bounds__(kThreads) pack_kernel(const double* __restrict
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = e / m, c = e % m;
+        MRS_DCHECK(__ldg(idx + i) >= 0);
         out[e] = x[(int64_t)__ldg(idx + i) * m + c];
     }
 }

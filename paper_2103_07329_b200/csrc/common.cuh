@@ -8,6 +8,18 @@
 #pragma once
 
 #include <cuda_runtime.h>
+
+// Checked build (MRS_CHECKS=1 python -m paper_2103_07329_b200.build ->
+// libmrsolve_b200_checked.so, loaded with MRS_LIB=...): device-side asserts on
+// the index arithmetic and the synchronisation protocols (ticket folds,
+// cluster barriers) -- the in-house substitute for compute-sanitizer, which
+// this GPU pool does not allow.
+#ifdef MRS_CHECKS
+#include <cassert>
+#define MRS_DCHECK(cond) assert(cond)
+#else
+#define MRS_DCHECK(cond) ((void)0)
+#endif
 #include <stdint.h>
 
 #include "../../include/mrsolve_b200.h"

@@ -392,6 +392,7 @@ static __device__ void finish_reduction(const RedArgs& ra, const double* blk, in
     __syncthreads();
     if (threadIdx.x == 0) {
         unsigned t = atomicAdd(ra.ticket, 1u);
+        MRS_DCHECK(t < (unsigned)G);           // a stale or shared ticket overshoots
         s_last = (t == (unsigned)G - 1);
     }
     __syncthreads();

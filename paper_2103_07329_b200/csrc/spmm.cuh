@@ -242,7 +242,11 @@ template <typename Tv, typename Ti> struct GSrc {
     const Ti* __restrict__ ci;
     const Tv* __restrict__ v;
     int base = 0;          // slab-compressed indices: column = base(row) + ci
-    __device__ __forceinline__ int col(int k) const { return base + (int)__ldg(ci + k); }
+    __device__ __forceinline__ int col(int k) const {
+        const int c = base + (int)__ldg(ci + k);
+        MRS_DCHECK(c >= 0);
+        return c;
+    }
     __device__ __forceinline__ double val(int k) const { return widen(__ldg(v + k)); }
     // the row's view: slab base of `row` (16-bit slab-relative columns)
     __device__ __forceinline__ GSrc at_row(const SpArgs& a, int row) const {

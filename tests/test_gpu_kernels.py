@@ -271,3 +271,29 @@ def test_spmv_coop_entry_loads_bitwise(m, vdt, coop, rng):
             np.testing.assert_array_equal(y, ref, err_msg=f"mode {mode}")
     finally:
         _lib.set_option("spmm_coop", 2)
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8, 16])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+def test_every_spmm_variant_bitwise(m, variant, rng):
+    """Every SpMM variant the per-operator choice can pick (lane, cooperative
+    loads, 16 in flight, gathers through L2 only, L1::no_allocate) gives the
+    reference kernel's bits, every mode, both value types, slab indices."""
+    from mrs_testutil import random_csr
+    from paper_2103_07329_b200 import _lib
+    n = 20000
+    blk = random_csr(n, n, 14.0, rng)
+    x = rng.standard_normal((n, m))
+    b = rng.standard_normal((n, m))
+    y0 = rng.standard_normal((n, m))
+    try:
+        _lib.set_option("spmm_variant", variant)
+        for vdt in (np.float64, np.float32):
+            vals = blk.values.astype(vdt)
+            for mode in range(4):
+                y = spmv_dev(blk.row_ptr, blk.col_idx, vals, x, y0, mode, b if mode == 3 else None)
+                ref = y0.copy()
+                O.csr_spmv(blk.row_ptr, blk.col_idx, vals, x, ref, mode, b if mode == 3 else None)
+                np.testing.assert_array_equal(y, ref, err_msg=f"variant {variant} mode {mode}")
+    finally:
+        _lib.set_option("spmm_variant", 0)
