@@ -703,6 +703,11 @@ def main():
                    "sample": f"unavailable: {errs}"}
 
     launches = plan.kernel_launches(iters) * args.steps
+    try:
+        min_bytes = cs.minimal_iteration_bytes(M)
+    except Exception as e:           # informational
+        print(f"[bench] minimal byte model failed: {e}", file=sys.stderr)
+        min_bytes = None
     job_rows = nglob if partitioned else world * n        # rows copied per step, whole job
     if rank == 0:
         line = {
@@ -723,7 +728,14 @@ def main():
                            if partitioned else f"{world} replicas (partitioned path failed: "
                                                f"{dist_error})"),
                        "setup_s_excluded": setup_s, "wall_s_timed_region": wall,
-                       "iteration_algorithmic_bytes": plan.iteration_bytes,
+                       # two byte models per outer iteration: SURVEY 8(d)'s minimal one
+                       # (the algorithm's compulsory traffic) and the plan's own (incl.
+                       # its collapsed dense V-cycle tail); whole-solve fraction of the
+                       # measured HBM peak from the minimal one
+                       "iteration_bytes_minimal": min_bytes,
+                       "iteration_bytes_plan": plan.iteration_bytes,
+                       "solve_frac_of_hbm_minimal": (min_bytes * iters * args.steps / t_dev / 1e9
+                                                     / peak) if min_bytes else None,
                        "final_rel_residual_max": float(st.final_rel_residual.max())},
             "roofline": roof,
             "cpu_baseline": cpu,

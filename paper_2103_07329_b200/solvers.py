@@ -75,6 +75,15 @@ class ConfiguredSolver:
     run: object
     hierarchy: Hierarchy | None = None
     plan_factory: object = None
+    desc: object = None          # plan descriptor (without m)
+    levels: list | None = None   # [(A, P, R)] as uploaded
+
+    def minimal_iteration_bytes(self, m: int) -> float:
+        """SURVEY.md 8(d) minimal bytes of one outer iteration (byte_model);
+        the plan's own model (incl. the collapsed dense tail) is
+        ``plan_factory(m).iteration_bytes``."""
+        from .byte_model import iteration_bytes_minimal
+        return iteration_bytes_minimal(self.desc, self.levels, m)
 
 
 def _sgs_direction(plist) -> int:
@@ -462,7 +471,8 @@ def _prepare_single(desc, levels, inv, h, name, Ab, method):
             X.flags.initialized = True
         return stats
 
-    return ConfiguredSolver(method, run, h, plan_for)
+    return ConfiguredSolver(method, run, h, plan_for, desc,
+                            [(lv[0], lv[1], lv[2]) for lv in levels])
 
 
 def solve(config: ParamTree, A, B, X, team=None) -> SolveStats:

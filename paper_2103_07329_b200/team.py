@@ -374,7 +374,8 @@ def prepare_distributed(config, A, team: GpuTeam, *, hierarchy=None, exec_mode: 
             X.flags.initialized = True
         return st
 
-    cs = ConfiguredSolver(name, run, h, plan_for)
+    cs = ConfiguredSolver(name, run, h, plan_for, desc,
+                          [(lay.A, lay.P, lay.R) for lay in lays])
     cs.layouts = lays
     cs.row_range = (lo, hi)
     cs.nlevels = payload["nlevels"]
