@@ -390,6 +390,7 @@ def roofline_at_scale(torch, K, peak, grid=128):
 
 def spmm_sweep(torch, K, quick: bool):
     """Config 5: blocked SpMM GB/s against the HBM roofline (ASSIGN mode)."""
+    from paper_2103_07329_b200 import _lib
     from paper_2103_07329_b200.io import gen_random_sdd
     t0 = time.time()
     A = gen_random_sdd()
@@ -411,6 +412,7 @@ def spmm_sweep(torch, K, quick: bool):
                 for _ in range(3):
                     K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
                 times = []
+                sl0 = _lib.lib().mrs_stream_launches()
                 for _ in range(10):
                     torch.sum(flush_buf, dim=0, out=flush_sink)
                     e0 = torch.cuda.Event(enable_timing=True)
@@ -424,7 +426,9 @@ def spmm_sweep(torch, K, quick: bool):
                 vb = 8 if vdt == "f64" else 4
                 byts = A.nnz * (vb + ib) + (A.nrows + 1) * 4 + 4 * nslab + 2 * A.nrows * m * 8
                 out.append({"m": m, "values": vdt, "idx": idx, "us": t * 1e6,
-                            "GBps": byts / t / 1e9, "frac": byts / t / 1e9 / peak})
+                            "GBps": byts / t / 1e9, "frac": byts / t / 1e9 / peak,
+                            "kernel": "stream (TMA-fed, csrc/stream.cu)"
+                            if _lib.lib().mrs_stream_launches() > sl0 else "lane family (csrc/spmm.cuh)"})
                 del x, y
             del D
     return {"n": A.nrows, "nnz": A.nnz, "gen_s": gen_s, "points": out}

@@ -75,6 +75,17 @@ typedef struct {
     const int32_t* long_rows;
     int32_t n_long;
     int32_t long_thr;
+    /* Optional structure facts the caller knows from the host arrays (0 / -1:
+     * unknown).  With them a single right-hand side product of a banded operator
+     * runs on the TMA-fed "stream" kernel (csrc/stream.cu; same bits).
+     *   band     max |column - row| over the entries, -1 unknown
+     *   blk_max  most entries in any aligned block of 256 consecutive rows
+     *   flags    bit 0: col_idx and values have >= 64 bytes of readable slack
+     *            behind their nnz entries (stages are fetched in 16-byte units) */
+    int32_t band;
+    int32_t blk_max;
+    int32_t flags;
+    int32_t pad2_;
 } mrs_csr;
 
 /* Host CSR (the reference CsrBlock layout, core.py:146-254). */
@@ -97,6 +108,9 @@ typedef struct {
  * separately rounded mul/add: bitwise equal to the reference kernel. */
 int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m,
                  int32_t mode, const double* b, void* stream);
+/* Diagnostics: launches of the single-RHS stream kernel (csrc/stream.cu) made by
+ * this process so far -- lets tests and the bench see which path a product took. */
+int64_t mrs_stream_launches(void);
 
 /* Vector kernels over (n, m) blocks; per-column scalars a, b, c are DEVICE
  * arrays of length m.  Same per-element expressions as _ckernels.pyx:82-162. */

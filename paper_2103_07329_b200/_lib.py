@@ -33,7 +33,9 @@ class mrs_csr(C.Structure):
                 ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p),
                 ("idx_bytes", C.c_int32), ("val_bytes", C.c_int32),
                 ("slab_base", C.c_void_p), ("slab_shift", C.c_int32), ("pad_", C.c_int32),
-                ("long_rows", C.c_void_p), ("n_long", C.c_int32), ("long_thr", C.c_int32)]
+                ("long_rows", C.c_void_p), ("n_long", C.c_int32), ("long_thr", C.c_int32),
+                ("band", C.c_int32), ("blk_max", C.c_int32), ("flags", C.c_int32),
+                ("pad2_", C.c_int32)]
 
 
 class mrs_host_csr(C.Structure):
@@ -111,6 +113,7 @@ SIGNATURES = {
                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]),
     "mrs_status_string": (C.c_char_p, [C.c_int32]),
     "mrs_version": (C.c_int, []),
+    "mrs_stream_launches": (C.c_int64, []),
     "mrs_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
     "mrs_comm_unique_id": (C.c_int, [C.c_void_p]),
     "mrs_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),

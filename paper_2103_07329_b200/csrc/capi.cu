@@ -133,6 +133,8 @@ extern "C" {
 
 int mrs_version(void) { return 1; }
 
+int64_t mrs_stream_launches(void) { return spmm_stream_launches(); }
+
 // Tuning knobs.  "pdl": launch the solve-path kernels with programmatic
 // dependent launch (default 0; env MRS_PDL=1).  Plans capture their graph at
 // the first solve, so set options before preparing.
@@ -196,6 +198,9 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_
         D.n_long = A->n_long;
         D.long_thr = A->long_thr;
     }
+    D.band = A->band;
+    D.blk_max = A->blk_max;
+    D.padded = (A->flags & 1) != 0;
     // unaligned views fall back to the scalar-per-column kernel
     bool vec_ok = aligned16(x) && aligned16(y) && (!b || aligned16(b));
     if (vec_ok) D.variant = plugin_variant(D, x, m, (cudaStream_t)stream);

@@ -27,6 +27,10 @@ struct DevCsr {
     int n_long = 0, long_thr = 0;
     int max_row = 0;              // longest row (solver levels; 0 = unknown)
     int variant = 0;              // SpmmVariant chosen for this operator (0 = heuristic)
+    // structure facts for the m = 1 stream kernel (stream.cu); unknown = not eligible
+    int band = -1;                // max |column - row|
+    int blk_max = 0;              // most entries in an aligned block of 256 rows
+    bool padded = false;          // >= 64 readable bytes behind ci / v
     bool present() const { return rp != nullptr; }
     // algorithmic bytes of one pass over the CSR arrays
     double bytes() const {
@@ -38,6 +42,10 @@ struct DevCsr {
 // SpMM-family launch (OP = SpOp).  a.rp/ci/vals/nrows are filled from A.
 cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream_t s,
                         bool generic = false);
+// m = 1 stream variant (stream.cu): eligibility of one launch, and the launch.
+bool spmm_stream_eligible(const DevCsr& A, int64_t m, const SpArgs& a);
+cudaError_t launch_spmm_stream(const DevCsr& A, const SpArgs& a, cudaStream_t s);
+int64_t spmm_stream_launches();
 // Vector-family launch (OP = VecOp).
 cudaError_t launch_vec(int op, VArgs a, cudaStream_t s);
 // Dense coarse solve x = Ainv b for (nc, m) blocks.

@@ -47,7 +47,7 @@ int64_t halo_overlap() { return g_halo_overlap; }
 void set_halo_overlap(int64_t v) { g_halo_overlap = v < 0 ? 0 : (v > 2 ? 2 : v); }
 static int64_t g_variant = 0;         // 0: per operator (autotuned / heuristic)
 int64_t spmm_variant() { return g_variant; }
-void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 5 ? 0 : v); }
+void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 6 ? 0 : v); }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
@@ -107,6 +107,9 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
         A.nnz >= (int64_t)INT32_MAX)
         return cudaErrorInvalidValue;
     a.variant = A.variant;
+    if (op == OP_SPMV && (a.variant ? a.variant : (int)spmm_variant()) == SV_STREAM && !generic &&
+        spmm_stream_eligible(A, m, a))
+        return launch_spmm_stream(A, a, s);
     if (A.vb == 8) {
         switch (op) {
         case OP_SPMV: return launch_spmm_op_f64<OP_SPMV>(A, a, m, s, generic);
@@ -159,8 +162,14 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     if (best_us) *best_us = 0.f;
     if (!spmm_autotune_enabled() || A.nrows == 0 || A.nnz == 0 || spmm_variant() != SV_AUTO)
         return SV_AUTO;
-    int cand[5], nc = 0;
+    int cand[6], nc = 0;
     cand[nc++] = SV_LANE;
+    {
+        SpArgs probe;
+        memset(&probe, 0, sizeof(probe));
+        probe.x = x; probe.y = y; probe.vp = vp;
+        if (spmm_stream_eligible(A, m, probe)) cand[nc++] = SV_STREAM;
+    }
     if (vp == VP_DD && (m == 4 || m == 8 || m == 16)) cand[nc++] = SV_COOP;
     if (m <= 16 && (m & (m - 1)) == 0) cand[nc++] = SV_LONG;
     if (vp == VP_DD && m <= 16 && (m & (m - 1)) == 0) {
@@ -178,7 +187,7 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     a.x = x; a.y = y; a.mode = MRS_MODE_ASSIGN; a.vp = vp;
     int best = SV_AUTO;
     float best_t = 3.4e38f;
-    float tm[5] = {0.f, 0.f, 0.f, 0.f, 0.f};
+    float tm[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int i = 0; i < nc && made == 2 * kReps; ++i) {
         DevCsr B = A;
         B.variant = cand[i];

@@ -47,6 +47,7 @@ enum SpmmVariant : int {
     SV_LONG = 3,     // 16 entries in flight per lane, 1 CTA/SM (m <= 16)
     SV_LANE_L2 = 4,  // lane, gathered x through L2 only (ld.global.cg: no L1 fills)
     SV_LANE_NA = 5,  // lane, gathered x with L1::no_allocate (hits kept, misses not filled)
+    SV_STREAM = 6,   // m = 1, banded operators: TMA-fed entry-parallel products (stream.cu)
 };
 
 // Vector precisions of one SpMM launch (gathered operand -> row operands).

@@ -75,6 +75,8 @@ class DeviceCsr:
         ci = np.asarray(col_idx)
         if ci.dtype not in (np.uint8, np.uint16, np.uint32):
             ci = ci.astype(np.uint32)
+        # structure facts for the single-RHS stream kernel (csrc/stream.cu)
+        self.band, self.blk_max = band_facts(row_ptr, ci)
         self.slab_base, self.slab_shift = None, 0
         if slab and ci.dtype == np.uint32:
             from .core import slab_compress
@@ -82,8 +84,10 @@ class DeviceCsr:
             if sc is not None:
                 ci, base, self.slab_shift = sc
                 self.slab_base = torch.from_numpy(base).to(dev)
-        self.col_idx = torch.from_numpy(ci.copy()).to(dev)
-        self.values = torch.as_tensor(np.asarray(values)).to(dev)
+        # 64 bytes of slack behind the entry arrays: the stream kernel fetches
+        # stages in 16-byte units and may read past the last entry
+        self.col_idx = _padded_to(ci, dev)
+        self.values = _padded_to(np.asarray(values), dev)
         self.nrows, self.ncols = int(nrows), int(ncols)
         self.nnz = int(self.col_idx.numel())
         # rows far longer than the mean run on whole CTAs (same bits)
@@ -102,7 +106,43 @@ class DeviceCsr:
             v.long_rows = self.long_rows.data_ptr()
             v.n_long = int(self.long_rows.numel())
             v.long_thr = self.long_thr
+        v.band, v.blk_max, v.flags = self.band, self.blk_max, 1
         return v
+
+
+def _padded_to(arr, device):
+    """Device copy of a 1-d host array as a view of an allocation with 64
+    spare bytes behind it."""
+    arr = np.ascontiguousarray(arr)
+    t = torch.from_numpy(arr)
+    extra = -(-64 // max(1, arr.itemsize))
+    buf = torch.zeros(arr.size + extra, dtype=t.dtype, device=device)
+    buf[:arr.size].copy_(t)
+    return buf[:arr.size]
+
+
+def band_facts(row_ptr, col_idx, block_rows=256):
+    """(max |column - row|, most entries in an aligned block of ``block_rows``
+    rows) of a CSR pattern, computed on the host in row blocks."""
+    rp = np.asarray(row_ptr, dtype=np.int64)
+    n = rp.size - 1
+    if n <= 0 or rp[-1] <= 0:
+        return -1, 0
+    ci = np.asarray(col_idx)
+    band = 0
+    step = 1 << 18
+    for r0 in range(0, n, step):
+        r1 = min(n, r0 + step)
+        e0, e1 = int(rp[r0]), int(rp[r1])
+        if e1 == e0:
+            continue
+        rows = np.repeat(np.arange(r0, r1, dtype=np.int64), np.diff(rp[r0:r1 + 1]))
+        band = max(band, int(np.abs(ci[e0:e1].astype(np.int64) - rows).max()))
+    edges = rp[np.minimum(np.arange(0, n + block_rows, block_rows), n)]
+    blk_max = int(np.diff(edges).max())
+    if band > 2 ** 30 or blk_max > 2 ** 30:
+        return -1, 0
+    return band, blk_max
 
 
 def long_row_split(row_ptr, device):
