@@ -96,7 +96,7 @@ int plugin_variant(const DevCsr& D, const double* x, int64_t m, cudaStream_t s) 
     double* flush = nullptr;
     if (cudaMalloc(&flush, fn * 8) != cudaSuccess) { cudaGetLastError(); flush = nullptr; }
     else cudaMemsetAsync(flush, 0, fn * 8, s);
-    const int v = spmm_tune(D, x, scratch, m, s, nullptr, VP_DD, flush, flush ? fn : 0);
+    const int v = spmm_tune(D, x, scratch, m, s, nullptr, VP_DD, flush, flush ? fn : 0, 0.97f);
     cudaStreamSynchronize(s);
     cudaFree(scratch);
     if (flush) cudaFree(flush);

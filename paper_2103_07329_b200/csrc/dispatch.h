@@ -67,9 +67,12 @@ int64_t halo_overlap();
 // per-operator SpMM variant by measurement (kernels.cu); knob spmm_autotune
 // flush: an L2-sized device buffer read before every timed launch (cold
 // conditions), or null
+// keep: the shape heuristic's variant stays unless the fastest one takes less than
+// `keep` of its time (plans: 0.85 -- an isolated launch is only a proxy for the
+// operator's cost inside a solve; standalone plugin products: 0.97)
 int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
               float* best_us = nullptr, int vp = 0, const double* flush = nullptr,
-              int64_t flush_n = 0);
+              int64_t flush_n = 0, float keep = 0.85f);
 int64_t spmm_autotune_enabled();
 int64_t plan_autotune();
 void set_plan_autotune(int64_t v);

@@ -158,7 +158,7 @@ __global__ void l2_flush_kernel(const double* __restrict__ p, int64_t n, double*
 }
 
 int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream_t s,
-              float* best_us, int vp, const double* flush, int64_t flush_n) {
+              float* best_us, int vp, const double* flush, int64_t flush_n, float keep) {
     if (best_us) *best_us = 0.f;
     if (!spmm_autotune_enabled() || A.nrows == 0 || A.nnz == 0 || spmm_variant() != SV_AUTO)
         return SV_AUTO;
@@ -214,7 +214,7 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     // the shape heuristic's choice unless another variant is clearly faster.
     const int dflt = vp == VP_DD ? spmm_shape_variant(A.nrows, A.nnz, A.max_row, m) : SV_LANE;
     for (int i = 0; i < nc; ++i)
-        if (cand[i] == dflt && tm[i] > 0.f && best != dflt && best_t > 0.85f * tm[i]) {
+        if (cand[i] == dflt && tm[i] > 0.f && best != dflt && best_t > keep * tm[i]) {
             best = dflt;
             best_t = tm[i];
         }
