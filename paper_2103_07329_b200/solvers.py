@@ -23,6 +23,7 @@ raises ConfigurationError; there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -437,12 +438,80 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
         desc.nlevels = h.nlevels
         tl = dense_tail_level(levels, pre=desc.pre, post=desc.post)
         if tl >= 0:
-            T = vcycle_tail_operator(levels, tl, desc.pre, desc.post, inv)
+            T = tail_operator(levels, tl, desc.pre, desc.post, inv)
             if T is not None:
                 inv = CoarseOps(inv, tl, T)
     else:
         raise ConfigurationError(f"preconditioner {pl.method!r} is not on the device path")
     return desc, levels, inv, h, name, Ab
+
+
+#: where the collapsed tail's dense operator is built: "device" (default when a
+#: GPU is present) or "host" (amg.vcycle_tail_operator: scipy products; the CPU
+#: tests and MRS_TAIL_BUILD=host)
+TAIL_BUILD = os.environ.get("MRS_TAIL_BUILD", "device")
+
+
+def tail_operator(levels, start, pre, post, inv):
+    """Dense operator of the sub-V-cycle below level ``start`` (setup phase)."""
+    if TAIL_BUILD == "device":
+        try:
+            import torch
+            on_gpu = torch.cuda.is_available()
+        except Exception:
+            on_gpu = False
+        if on_gpu:
+            return tail_operator_device(levels, start, pre, post, inv)
+    return vcycle_tail_operator(levels, start, pre, post, inv)
+
+
+def tail_operator_device(levels, start: int, pre, post, inv, cols: int = 64):
+    """amg.vcycle_tail_operator on the GPU: the sub-hierarchy from level
+    ``start`` is uploaded as a MultiGrid-as-solver plan and ONE V-cycle from a
+    zero guess is applied to the n_l unit vectors, ``cols`` right-hand sides
+    at a time, with the plan's own per-level kernels (SpMM, fused smoothers,
+    level-scheduled Gauss-Seidel, dense coarse solve) -- the exact kernels the
+    collapsed tail replaces in the solve.  Replaces minutes of scipy products
+    on the host for the tail levels of large hierarchies (the dominant part of
+    ``prepare`` at C4 sizes).  Returns the (n_l, n_l) float64 array."""
+    import torch
+    for sm in (pre, post):
+        if sm.kind not in (_lib.SMOOTH_JACOBI, _lib.SMOOTH_CHEBYSHEV, _lib.SMOOTH_SGS):
+            return None
+    sub = list(levels[start:])
+    n = as_csr(sub[0][0]).nrows
+    d = _lib.mrs_plan_desc()
+    d.method = _lib.METHOD_STATIONARY
+    d.precond = _lib.PC_MG
+    d.nrows = n
+    d.m = cols
+    d.rel_tol = 0.0                      # never "converged": exactly max_iters = 1 cycle
+    d.max_iters = 1
+    d.exec = 1
+    d.mg_cycles = 1
+    d.pre, d.post = pre, post
+    d.nlevels = len(sub)
+    d.drift_limit = DRIFT_LIMIT
+    plan = DevicePlan(d, sub, inv, "tail-builder")
+    try:
+        dev = torch.device("cuda", torch.cuda.current_device())
+        stream = C.c_void_p(torch.cuda.current_stream().cuda_stream)
+        T = torch.empty((n, n), dtype=torch.float64, device=dev)
+        B = torch.empty((n, cols), dtype=torch.float64, device=dev)
+        X = torch.empty((n, cols), dtype=torch.float64, device=dev)
+        lanes = torch.arange(cols, device=dev)
+        for j0 in range(0, n, cols):
+            w = min(cols, n - j0)
+            # unit vectors e_j0 .. e_j0+w-1 (the last block repeats its last column)
+            B.zero_()
+            B[torch.clamp(lanes + j0, max=n - 1), lanes] = 1.0
+            X.zero_()
+            plan.solve(B.data_ptr(), X.data_ptr(), True, False, stream)
+            T[:, j0:j0 + w] = X[:, :w]
+        out = T.cpu().numpy()
+    finally:
+        del plan
+    return out
 
 
 def _prepare_single(desc, levels, inv, h, name, Ab, method):
