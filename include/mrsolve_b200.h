@@ -111,6 +111,9 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m,
 /* Diagnostics: launches of the single-RHS stream kernel (csrc/stream.cu) made by
  * this process so far -- lets tests and the bench see which path a product took. */
 int64_t mrs_stream_launches(void);
+/* Diagnostics: Galerkin products A_c = (R A) P that mrs_amg_setup ran on the GPU
+ * (csrc/spgemm.cu; option "setup_gpu" / env MRS_SETUP_GPU=0 forces the host path). */
+int64_t mrs_galerkin_gpu_count(void);
 
 /* Vector kernels over (n, m) blocks; per-column scalars a, b, c are DEVICE
  * arrays of length m.  Same per-element expressions as _ckernels.pyx:82-162. */

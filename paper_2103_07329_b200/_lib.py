@@ -114,6 +114,7 @@ SIGNATURES = {
     "mrs_status_string": (C.c_char_p, [C.c_int32]),
     "mrs_version": (C.c_int, []),
     "mrs_stream_launches": (C.c_int64, []),
+    "mrs_galerkin_gpu_count": (C.c_int64, []),
     "mrs_set_option": (C.c_int, [C.c_char_p, C.c_int64]),
     "mrs_comm_unique_id": (C.c_int, [C.c_void_p]),
     "mrs_comm_create": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),

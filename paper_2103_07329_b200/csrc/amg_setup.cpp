@@ -29,6 +29,7 @@
 #include <vector>
 
 #include "../../include/mrsolve_b200.h"
+#include "spgemm.h"
 
 namespace {
 
@@ -365,11 +366,25 @@ int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarc
         const int64_t ncoarse = P.ncols;
         if (ncoarse == 0 || (double)ncoarse > prm->stall_ratio * (double)M.nrows) break;
         Csr R = transpose(P);
-        Csr RA = matmat(R, M);
-        auto t4 = now();
-        Csr Ac = matmat(RA, P);
-        auto t5 = now();
-        sort_rows(Ac);
+        Csr Ac;
+        auto t4 = now(), t5 = t4;
+        {
+            // Galerkin product on the GPU when one is present (spgemm.cu: bitwise
+            // the host products below), else on the host threads
+            const mrs::HostCsrView vR{R.nrows, R.ncols, R.rp.data(), R.ci.data(), R.v.data()};
+            const mrs::HostCsrView vA{M.nrows, M.ncols, M.rp.data(), M.ci.data(), M.v.data()};
+            const mrs::HostCsrView vP{P.nrows, P.ncols, P.rp.data(), P.ci.data(), P.v.data()};
+            Ac.nrows = R.nrows; Ac.ncols = P.ncols;
+            if (mrs::galerkin_gpu(vR, vA, vP, Ac.rp, Ac.ci, Ac.v)) {
+                t4 = t5 = now();
+            } else {
+                Csr RA = matmat(R, M);
+                t4 = now();
+                Ac = matmat(RA, P);
+                t5 = now();
+                sort_rows(Ac);
+            }
+        }
         auto t6 = now();
         tphase[0] += secs(t0, t1); tphase[1] += secs(t1, t2); tphase[2] += secs(t2, t3);
         tphase[3] += secs(t3, t4); tphase[4] += secs(t4, t5); tphase[5] += secs(t5, t6);
@@ -377,8 +392,9 @@ int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarc
         chain.push_back(std::move(Ac));
     }
     if (timing)
-        fprintf(stderr, "[mrs_amg_setup] strength %.2fs split %.2fs interp %.2fs RA %.2fs RAP %.2fs sort %.2fs (%d threads)\n",
-                tphase[0], tphase[1], tphase[2], tphase[3], tphase[4], tphase[5], setup_threads());
+        fprintf(stderr, "[mrs_amg_setup] strength %.2fs split %.2fs interp %.2fs RA %.2fs RAP %.2fs sort %.2fs (%d threads; %lld Galerkin products on the GPU so far: those count under RA)\n",
+                tphase[0], tphase[1], tphase[2], tphase[3], tphase[4], tphase[5], setup_threads(),
+                (long long)mrs::galerkin_gpu_count());
     mrs_hierarchy* h = new mrs_hierarchy();
     h->levels.resize(chain.size());
     for (size_t l = 0; l < chain.size(); ++l) {

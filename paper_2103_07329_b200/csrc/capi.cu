@@ -16,6 +16,7 @@
 #include "dispatch.h"
 #include "sgs.cuh"
 #include "sgs_sched.h"
+#include "spgemm.h"
 
 using namespace mrs;
 
@@ -134,6 +135,7 @@ extern "C" {
 int mrs_version(void) { return 1; }
 
 int64_t mrs_stream_launches(void) { return spmm_stream_launches(); }
+int64_t mrs_galerkin_gpu_count(void) { return galerkin_gpu_count(); }
 
 // Tuning knobs.  "pdl": launch the solve-path kernels with programmatic
 // dependent launch (default 0; env MRS_PDL=1).  Plans capture their graph at
@@ -152,6 +154,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_coop")) { set_spmm_coop(value); return MRS_OK; }
     if (!strcmp(key, "dense_mma")) { set_dense_mma(value); return MRS_OK; }
     if (!strcmp(key, "loop_unroll")) { set_loop_unroll(value); return MRS_OK; }
+    if (!strcmp(key, "setup_gpu")) { set_setup_gpu(value); return MRS_OK; }
     return MRS_ERR_ARG;
 }
 
