@@ -94,6 +94,14 @@ CONFIGS["c3v32"] = dict(CONFIGS["c3"], workload=CONFIGS["c3"]["workload"].replac
     "fp64 vectors)", "fp64 Krylov vectors, fp32 V-cycle vectors below level 0)"),
     roles=dict(CONFIGS["c3"]["roles"], preconditioner={
         "method": "MultiGrid", "mg_mixed_precision": "1", "mg_vector_precision": "fp32"}))
+CONFIGS["c3v32a"] = dict(CONFIGS["c3"], workload=CONFIGS["c3"]["workload"].replace(
+    "fp64 vectors)", "fp64 Krylov vectors, fp32 V-cycle vectors on every level incl. 0)"),
+    roles=dict(CONFIGS["c3"]["roles"], preconditioner={
+        "method": "MultiGrid", "mg_mixed_precision": "1", "mg_vector_precision": "fp32_all"}))
+CONFIGS["c4v32a"] = dict(CONFIGS["c4"], workload=CONFIGS["c4"]["workload"].replace(
+    "fp64, tol", "fp64 Krylov vectors, fp32 V-cycle vectors on every level incl. 0, tol"),
+    roles=dict(CONFIGS["c4"]["roles"], preconditioner={
+        "method": "MultiGrid", "mg_vector_precision": "fp32_all"}))
 CONFIGS["c2v32"] = dict(CONFIGS["c2"], workload=CONFIGS["c2"]["workload"].replace(
     "fp64, tol", "fp64 Krylov vectors, fp32 V-cycle vectors below level 0, tol"),
     roles=dict(CONFIGS["c2"]["roles"], preconditioner={

@@ -98,7 +98,9 @@ typedef struct {
     int32_t val_bytes;
     const int32_t* slab_base; /* optional slab-relative 16-bit indices (see mrs_csr) */
     int32_t slab_shift;
-    int32_t pad_;
+    int32_t pad_;             /* flags.  bit 0: 32-bit columns may be compressed to
+                               * slab-relative 16-bit ones by the upload, on the device
+                               * (csrc/slab.cu; the rule of core.slab_compress) */
 } mrs_host_csr;
 
 /* ---- 1. kernel plugin (src/kernels/__init__.py:27-41) ------------------ */
@@ -207,7 +209,10 @@ typedef struct {
     int32_t vec32;       /* MultiGrid, single GPU: 1 = the V-cycle vectors of levels
                             1 .. (collapsed tail or coarsest) - 1 are float32 (loads
                             widened, fp64 accumulation, stores rounded); the Krylov
-                            vectors and level 0 stay float64 (an fp32 preconditioner) */
+                            vectors and level 0 stay float64.  2 = level 0 of the
+                            V-cycle too: the whole preconditioner runs on float32
+                            vectors (r is rounded on entry, z widened on exit), only
+                            the Krylov vectors stay float64 */
 } mrs_plan_desc;
 
 typedef struct mrs_plan mrs_plan;

@@ -180,6 +180,11 @@ def check(code: int, what: str = "mrsolve_b200 call"):
     raise DeviceError(msg, code)
 
 
+#: index compression of plan uploads on the device (False / MRS_SLAB_ON_DEVICE=0:
+#: core.slab_compress on the host, the round-1 path; identical result)
+SLAB_ON_DEVICE = os.environ.get("MRS_SLAB_ON_DEVICE", "1") != "0"
+
+
 def host_csr(blk, keep: list, slab=False) -> mrs_host_csr:
     """mrs_host_csr view of a CsrBlock-like object (arrays kept alive in `keep`).
     ``slab=True``: store 32-bit column indices as slab-relative 16-bit ones
@@ -193,14 +198,18 @@ def host_csr(blk, keep: list, slab=False) -> mrs_host_csr:
     if v.dtype not in (np.float32, np.float64):
         v = v.astype(np.float64)
     base_p, shift = None, 0
+    flags = 0
     if slab and ci.dtype == np.uint32:
-        from .core import slab_compress
-        sc = slab_compress(rp, ci)
-        if sc is not None:
-            ci, base, shift = sc
-            keep.append(base)
-            base_p = base.ctypes.data
+        if SLAB_ON_DEVICE:
+            flags = 1           # the upload compresses on the GPU (csrc/slab.cu, same rule)
+        else:
+            from .core import slab_compress
+            sc = slab_compress(rp, ci)
+            if sc is not None:
+                ci, base, shift = sc
+                keep.append(base)
+                base_p = base.ctypes.data
     keep.extend([rp, ci, v])
     return mrs_host_csr(int(blk.nrows), int(blk.ncols), int(rp[-1]), rp.ctypes.data,
                         ci.ctypes.data, v.ctypes.data, ci.dtype.itemsize, v.dtype.itemsize,
-                        base_p, shift, 0)
+                        base_p, shift, flags)

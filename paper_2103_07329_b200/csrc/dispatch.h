@@ -46,8 +46,18 @@ cudaError_t launch_spmm(int op, const DevCsr& A, SpArgs a, int64_t m, cudaStream
 bool spmm_stream_eligible(const DevCsr& A, int64_t m, const SpArgs& a);
 cudaError_t launch_spmm_stream(const DevCsr& A, const SpArgs& a, cudaStream_t s);
 int64_t spmm_stream_launches();
+// Device-side index compression at upload (slab.cu; same rule as core.slab_compress).
+int slab_compress_device(const int32_t* rp_dev, const uint32_t* ci32_dev, int64_t nrows, int64_t nnz,
+                         int64_t ncols, uint16_t** ci16, int32_t** base, int* shift,
+                         int64_t* nslabs);
 // Vector-family launch (OP = VecOp).
 cudaError_t launch_vec(int op, VArgs a, cudaStream_t s);
+// fp32-preconditioner interface kernels (kernels.cu): r -> float b (+ seed), float x -> z
+cudaError_t launch_cvt_to32(const double* r, float* b32, int64_t n, int64_t m, int seed_mode,
+                            const double* d, double w, float* seed_out, const int* guard,
+                            cudaStream_t s);
+cudaError_t launch_cvt_from32(const float* x32, double* z, int64_t total, const int* guard,
+                              cudaStream_t s);
 // Dense coarse solve x = Ainv b for (nc, m) blocks.
 cudaError_t launch_dense(const double* T, int64_t n, const double* b, double* x, int64_t m,
                          const int* guard, cudaStream_t s);

@@ -222,6 +222,49 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     return best;
 }
 
+// fp32 preconditioner interface (plan option vec32 = 2: level 0 of the V-cycle
+// stores its vectors in float too): the Krylov residual enters the V-cycle as a
+// float right-hand side (+ the level-0 zero-guess smoother seed), the V-cycle's
+// float result leaves as the double z.
+__global__ void __launch_bounds__(kThreads) cvt_to32_kernel(const double* __restrict__ r,
+                                                            float* __restrict__ b32, int64_t n, int m,
+                                                            int seed_mode, const double* __restrict__ d,
+                                                            double w, float* __restrict__ seed_out,
+                                                            const int* guard) {
+    pdl_enter();
+    if (guard && *guard) return;
+    const int64_t total = n * m;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const float f = __double2float_rn(r[i]);
+        b32[i] = f;
+        if (seed_mode) seed_out[i] = __double2float_rn(seed_value(seed_mode, (double)f, __ldg(d + i / m), w));
+    }
+}
+__global__ void __launch_bounds__(kThreads) cvt_from32_kernel(const float* __restrict__ x32,
+                                                              double* __restrict__ z, int64_t total,
+                                                              const int* guard) {
+    pdl_enter();
+    if (guard && *guard) return;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x)
+        z[i] = (double)x32[i];
+}
+cudaError_t launch_cvt_to32(const double* r, float* b32, int64_t n, int64_t m, int seed_mode,
+                            const double* d, double w, float* seed_out, const int* guard,
+                            cudaStream_t s) {
+    const int g = (int)std::min<int64_t>((n * m + kThreads - 1) / kThreads, (int64_t)num_sms() * 8);
+    (void)launch_ex(cvt_to32_kernel, std::max(g, 1), s, r, b32, n, (int)m, seed_mode, d, w, seed_out,
+                    guard);
+    return cudaGetLastError();
+}
+cudaError_t launch_cvt_from32(const float* x32, double* z, int64_t total, const int* guard,
+                              cudaStream_t s) {
+    const int g = (int)std::min<int64_t>((total + kThreads - 1) / kThreads, (int64_t)num_sms() * 8);
+    (void)launch_ex(cvt_from32_kernel, std::max(g, 1), s, x32, z, total, guard);
+    return cudaGetLastError();
+}
+
 template <int OP>
 static cudaError_t vec_op(const VArgs& a, cudaStream_t s) {
     int g;

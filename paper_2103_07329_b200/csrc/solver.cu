@@ -609,6 +609,43 @@ PCPlan plan_precond(mrs_plan* P, const int* guard, const double* r, double* want
             if (!producer_seeds) bd.seed_kernel(r, P->n, pc.seed);
             bd.smooth_zero_seeded(lv, r, Builder::pc_smoother(d), x, dot_epi);
             pc.out = x.cur;
+        } else if (P->L[0].f32) {
+            // fp32 preconditioner (vec32 = 2): the whole V-cycle, level 0 included,
+            // on float vectors; r -> float b (+ seed) on entry, float x -> z on exit
+            const int cycles = d.mg_cycles < 1 ? 1 : d.mg_cycles;
+            LevelDev& lv = P->L[0];
+            XB x32{lv.xa, lv.xb};
+            const Seed sd = bd.level_seed(0, x32);
+            const int64_t n = P->n, m = P->m;
+            {
+                const double* rr = r;
+                float* b32 = reinterpret_cast<float*>(lv.b);
+                float* so = reinterpret_cast<float*>(sd.out);
+                const int md = sd.mode;
+                const double* dd = sd.d;
+                const double w = sd.w;
+                const int* g = guard;
+                pc.ops.push_back([=](cudaStream_t s) {
+                    return launch_cvt_to32(rr, b32, n, m, md, dd, w, so, g, s);
+                });
+                bd.bytes += bd.V(n) + bd.V(n, true) * (md ? 2 : 1) + (md ? 8.0 * n : 0.0);
+                bd.kernels++;
+            }
+            for (int c = 0; c < cycles; ++c) bd.vcycle(0, lv.b, c == 0, c == 0, x32, -1);
+            {
+                const float* xs = reinterpret_cast<const float*>(x32.cur);
+                double* z = a;
+                const int* g = guard;
+                pc.ops.push_back([=](cudaStream_t s) { return launch_cvt_from32(xs, z, n * m, g, s); });
+                bd.bytes += bd.V(n) + bd.V(n, true);
+                bd.kernels++;
+            }
+            if (dot_epi >= 0) bd.dot(r, a, n, dot_epi);
+            pc.out = a;
+            pc.seed = Seed();
+            pc.bytes = bd.bytes;
+            pc.kernels = bd.kernels;
+            return;
         } else {
             const int cycles = d.mg_cycles < 1 ? 1 : d.mg_cycles;
             pc.seed = bd.level_seed(0, x);
@@ -1089,12 +1126,44 @@ int upload_csr(const mrs_host_csr* h, DevCsr& d, std::vector<void*>& owned) {
     d.ib = h->idx_bytes == 1 ? 2 : h->idx_bytes;
     std::vector<int32_t> rp(h->nrows + 1);
     for (int64_t i = 0; i <= h->nrows; ++i) rp[i] = (int32_t)h->row_ptr[i];
+    // pad_ bit 0: compress 32-bit columns to slab-relative 16-bit ones on the
+    // device when they fit (slab.cu)
+    const bool try_slab = (h->pad_ & 1) && h->idx_bytes == 4 && !h->slab_base && h->nnz > 0;
     d.rp = dalloc<int32_t>(h->nrows + 1, owned);
-    d.ci = dalloc<char>((size_t)h->nnz * d.ib, owned);
     d.v = dalloc<char>((size_t)h->nnz * d.vb, owned);
-    if (!d.rp || !d.ci || !d.v) return MRS_ERR_ALLOC;
+    if (!d.rp || !d.v) return MRS_ERR_ALLOC;
     MRS_CUDA_OK(cudaMemcpy(d.rp, rp.data(), rp.size() * 4, cudaMemcpyHostToDevice));
-    if (h->idx_bytes == 1) {
+    bool slabbed = false;
+    if (try_slab) {
+        uint32_t* c32 = nullptr;
+        if (cudaMalloc(&c32, (size_t)h->nnz * 4) != cudaSuccess) return MRS_ERR_ALLOC;
+        if (cudaMemcpy(c32, h->col_idx, (size_t)h->nnz * 4, cudaMemcpyHostToDevice) != cudaSuccess) {
+            cudaFree(c32);
+            return MRS_ERR_CUDA;
+        }
+        uint16_t* c16 = nullptr;
+        int32_t* base = nullptr;
+        int shift = 0;
+        int64_t ns = 0;
+        const int rc = slab_compress_device(d.rp, c32, h->nrows, h->nnz, h->ncols, &c16, &base,
+                                            &shift, &ns);
+        if (rc < 0) { cudaFree(c32); return MRS_ERR_CUDA; }
+        if (rc == 1) {
+            cudaFree(c32);
+            owned.push_back(c16); owned.push_back(base);
+            d.ci = c16; d.ib = 2; d.slab_base = base; d.slab_shift = shift;
+        } else {
+            owned.push_back(c32);
+            d.ci = c32;
+        }
+        slabbed = true;
+    } else {
+        d.ci = dalloc<char>((size_t)h->nnz * d.ib, owned);
+        if (!d.ci) return MRS_ERR_ALLOC;
+    }
+    if (slabbed) {
+        // columns are in place
+    } else if (h->idx_bytes == 1) {
         std::vector<uint16_t> w(h->nnz);
         for (int64_t k = 0; k < h->nnz; ++k) w[k] = ((const uint8_t*)h->col_idx)[k];
         MRS_CUDA_OK(cudaMemcpy(d.ci, w.data(), w.size() * 2, cudaMemcpyHostToDevice));
@@ -1383,12 +1452,18 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
             if (p->m > 32 || (p->m & (p->m - 1)) != 0) return MRS_ERR_UNSUPPORTED;
             const int end = p->dense_from >= 1 ? p->dense_from : (int)p->L.size() - 1;
             for (int l = 1; l < end; ++l) p->L[l].f32 = true;
+            if (d.vec32 == 2) {
+                // level 0 too: the "fp32 preconditioner" (Krylov vectors stay double);
+                // MultiGrid as the SOLVER iterates on the double X itself
+                if (d.method == MRS_METHOD_STATIONARY || end < 1) return MRS_ERR_UNSUPPORTED;
+                p->L[0].f32 = true;
+            }
         }
         for (size_t l = 0; l < p->L.size(); ++l) {
             LevelDev& lv = p->L[l];
             // float levels: the same element count in half the bytes
             const int64_t nl = lv.f32 ? (lv.vrows + 1) / 2 : lv.vrows;
-            if (l > 0) lv.b = dalloc<double>(nl * m, o);
+            if (l > 0 || lv.f32) lv.b = dalloc<double>(nl * m, o);
             lv.xa = dalloc<double>(nl * m, o);
             lv.xb = dalloc<double>(nl * m, o);
             lv.r = dalloc<double>(nl * m, o);
@@ -1399,7 +1474,7 @@ int mrs_plan_finalize(mrs_plan* p, void* stream) {
                 lv.dvb = dalloc<double>(nl * m, o);
                 if (!(lv.lmin > 0.0 && lv.lmin < lv.lmax)) return MRS_ERR_ARG;
             }
-            if (!lv.xa || !lv.xb || !lv.r || (l > 0 && !lv.b)) return MRS_ERR_ALLOC;
+            if (!lv.xa || !lv.xb || !lv.r || ((l > 0 || lv.f32) && !lv.b)) return MRS_ERR_ALLOC;
         }
     } else if (p->desc.precond == MRS_PC_JACOBI || p->desc.precond == MRS_PC_SGS) {
         if (!p->L[0].d) return MRS_ERR_STATE;

@@ -406,9 +406,12 @@ def _configure(config, A, hierarchy, exec_mode, eig_bounds):
             vprec = pl.get_str("mg_vector_precision")
         except Exception:            # a reference ParamTree has no such key
             vprec = "fp64"
-        if vprec not in ("fp64", "fp32"):
-            raise InvalidArgumentError(f"mg_vector_precision must be fp64 or fp32, got {vprec!r}")
-        desc.vec32 = int(vprec == "fp32")
+        if vprec not in ("fp64", "fp32", "fp32_all"):
+            raise InvalidArgumentError(
+                f"mg_vector_precision must be fp64, fp32 or fp32_all, got {vprec!r}")
+        # fp32: V-cycle vectors below level 0; fp32_all: level 0's too (the whole
+        # preconditioner on float vectors, Krylov vectors fp64)
+        desc.vec32 = {"fp64": 0, "fp32": 1, "fp32_all": 2}[vprec]
         if hierarchy is None:
             params = AmgParams(strength_threshold=pl.get_float("mg_strength_threshold"),
                                agg_num_levels=pl.get_int("mg_agg_num_levels"),

@@ -60,3 +60,31 @@ def test_gpu_galerkin_hierarchy_bitwise(case):
             assert x.values.dtype == y.values.dtype
             assert np.array_equal(x.values.view(np.uint8), y.values.view(np.uint8)), \
                 f"level {l} {name} values differ"
+
+
+@pytest.mark.parametrize("case", ["poisson_48", "s27_44", "random_sdd_wide"])
+def test_device_slab_compression_matches_host(case, monkeypatch):
+    """Index compression at upload on the device (csrc/slab.cu) vs on the host
+    (core.slab_compress): same shift / bases (the plans stream the same bytes)
+    and bitwise the same solve."""
+    from paper_2103_07329_b200 import BlockVector
+    from paper_2103_07329_b200.params import tree
+    from paper_2103_07329_b200 import solvers as S
+    A = {"poisson_48": lambda: gen_poisson3d(48, 48, 48)[0],
+         "s27_44": lambda: gen_stencil27_aniso(44, seed=4),
+         "random_sdd_wide": lambda: gen_random_sdd(n=200000, band=40000)}[case]()
+    roles = {"solver": {"method": "CG", "rel_tolerance": "1e-8", "max_iters": "60"},
+             "preconditioner": {"method": "MultiGrid"},
+             "pre_smoother": {"method": "Jacobi", "weight": "0.8"},
+             "post_smoother": {"method": "Jacobi", "weight": "0.8"}}
+    B = np.random.default_rng(5).uniform(-1, 1, (A.nrows, 4))
+    out = {}
+    for dev in (True, False):
+        monkeypatch.setattr(_lib, "SLAB_ON_DEVICE", dev)
+        cs = S.prepare(tree(roles), A)
+        X = BlockVector.zeros(A.nrows, 4)
+        st = cs.run(BlockVector.from_array(B), X)
+        out[dev] = (st.iterations, X.data.copy(), cs.plan_factory(4).iteration_bytes)
+    assert out[True][0] == out[False][0]
+    assert out[True][2] == out[False][2], "different index widths / slab counts"
+    assert np.array_equal(out[True][1], out[False][1])

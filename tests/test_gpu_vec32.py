@@ -110,3 +110,54 @@ def test_vec32_unsupported_combinations_raise():
         prepare(tree(roles("CG", JAC, "fp32")), A, team=team).run(
             BlockVector.from_array(B[:, :2].copy()), BlockVector.zeros(A.nrows, 2))
     team.close()
+
+
+# ---- fp32_all: level 0 of the V-cycle on float vectors too (plan vec32 = 2) ----
+
+@pytest.mark.parametrize("case", list(CASES))
+def test_vec32_all_matches_fp64_solve(case):
+    """The whole preconditioner on float vectors (the Krylov residual rounded on
+    entry, the result widened on exit): iterations within +-1 of the fp64 solve,
+    every column converged to 1e-8 (true fp64 residual), X within 1e-6.  (No byte
+    claim: the two conversion passes and the separate (r, z) dot cost about what
+    the float level-0 kernels save -- DESIGN.md section 5.)"""
+    mk, m, solver, sm, mixed = CASES[case]
+    A = mk()
+    B = np.random.default_rng(7).uniform(-1, 1, (A.nrows, m))
+    cs64, st64, X64 = solve(A, B, roles(solver, sm, "fp64", mixed))
+    csa, sta, Xa = solve(A, B, roles(solver, sm, "fp32_all", mixed))
+    assert abs(sta.iterations - st64.iterations) <= 1, (sta.iterations, st64.iterations)
+    assert sta.all_converged and np.all(sta.final_rel_residual <= 1e-8)
+    err = np.abs(Xa - X64).max(axis=0) / np.abs(X64).max(axis=0)
+    assert err.max() <= 1e-6, err
+
+
+@pytest.mark.parametrize("case", ["c2_shrunk", "c3_shrunk"])
+def test_vec32_all_matches_rounding_oracle(case, monkeypatch):
+    from paper_2103_07329_b200 import amg
+    from oracle.amg_setup import setup as osetup
+    monkeypatch.setattr(amg, "DENSE_TAIL_ROWS", 0)
+    mk, m, solver, sm, mixed = CASES[case]
+    A = mk()
+    B = np.random.default_rng(8).uniform(-1, 1, (A.nrows, m))
+    cs, st, X = solve(A, B, roles(solver, sm, "fp32_all", mixed))
+    Ao = O.Csr.of(A)
+    h = osetup(Ao, mixed=bool(int(mixed)))
+    spec = ("jacobi", 0.8, 1) if sm is JAC else ("chebyshev", 2)
+    mg = O.MultiGridVec32(h, spec, spec, level0=True)
+    Xo = np.zeros_like(B)
+    drv = O.cg_solve if solver == "CG" else O.bicgstab_solve
+    so = drv(Ao, B, Xo, mg, 1e-8, 100)
+    assert abs(st.iterations - so.iterations) <= 1, (st.iterations, so.iterations)
+    err = np.abs(X - Xo).max(axis=0) / np.abs(Xo).max(axis=0)
+    assert err.max() <= 1e-6, err
+
+
+def test_vec32_all_multigrid_solver_is_rejected():
+    """MultiGrid as the SOLVER iterates on the fp64 X itself: no float level 0."""
+    A = gen_poisson3d(12, 12, 12)[0]
+    B = np.random.default_rng(1).uniform(-1, 1, (A.nrows, 2))
+    r = {"solver": {"method": "MultiGrid", "rel_tolerance": "1e-8", "mg_vector_precision": "fp32_all"},
+         "pre_smoother": JAC, "post_smoother": JAC}
+    with pytest.raises(ConfigurationError):
+        solve(A, B, r)
