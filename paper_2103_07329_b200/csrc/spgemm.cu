@@ -16,7 +16,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <cub/device/device_scan.cuh>
 
@@ -370,9 +372,18 @@ bool galerkin_gpu(const HostCsrView& R, const HostCsrView& A, const HostCsrView&
         return false;
     }
     DCsr dR, dA, dP, dRA, dC;
-    bool ok = upload(R, dR) && upload(A, dA) && product(dR, dA, 0, dRA);
+    const bool timing = getenv("MRS_SETUP_TIMING") != nullptr;
+    auto now = [] { return std::chrono::steady_clock::now(); };
+    auto secs = [](auto a, auto b) { return std::chrono::duration<double>(b - a).count(); };
+    const auto t0 = now();
+    bool ok = upload(R, dR) && upload(A, dA);
+    const auto t1 = now();
+    ok = ok && product(dR, dA, 0, dRA);
+    const auto t2 = now();
     dR.release(); dA.release();
     ok = ok && upload(P, dP) && product(dRA, dP, 1, dC);
+    const auto t3 = now();
+    const int64_t nnz_ra = dRA.nnz;
     dRA.release(); dP.release();
     if (ok) {
         const int64_t n = dC.nrows, nnz = dC.nnz;
@@ -389,6 +400,11 @@ bool galerkin_gpu(const HostCsrView& R, const HostCsrView& A, const HostCsrView&
     }
     dC.release();
     if (!ok) { cudaGetLastError(); return false; }
+    if (timing && A.nrows > 100000)
+        fprintf(stderr, "[galerkin_gpu] n %lld nnz(A) %lld nnz(RA) %lld nnz(Ac) %lld: upload %.2fs  R*A %.2fs  "
+                "(RA)*P %.2fs  download %.2fs\n", (long long)A.nrows, (long long)A.rp[A.nrows],
+                (long long)nnz_ra, (long long)rp.back(), secs(t0, t1), secs(t1, t2), secs(t2, t3),
+                secs(t3, now()));
     g_count.fetch_add(1);
     return true;
 }
