@@ -414,9 +414,13 @@ def spmm_sweep(torch, K, quick: bool):
             D = K.DeviceCsr(A.row_ptr, A.col_idx, vals, A.nrows, A.ncols, slab=idx == "u16slab")
             ib = D.col_idx.element_size()
             nslab = 0 if D.slab_base is None else D.slab_base.numel()
-            for m in ms_list:
-                x = torch.rand(A.ncols, m, dtype=torch.float64, device="cuda")
-                y = torch.empty(A.nrows, m, dtype=torch.float64, device="cuda")
+            for m, vec in [(m, "f64") for m in ms_list] + [(m, "f32") for m in ms_list
+                                                           if vdt == "f32" and idx == "u16slab"]:
+                # (fp32 VECTORS -- an extension, loads widened / fp64 accumulation /
+                # one rounding at the store -- on the fully compressed format only)
+                tdt = torch.float64 if vec == "f64" else torch.float32
+                x = torch.rand(A.ncols, m, dtype=tdt, device="cuda")
+                y = torch.empty(A.nrows, m, dtype=tdt, device="cuda")
                 for _ in range(3):
                     K.csr_spmv(D, None, None, x, y, K.MODE_ASSIGN)
                 times = []
@@ -432,8 +436,9 @@ def spmm_sweep(torch, K, quick: bool):
                     times.append(e0.elapsed_time(e1) * 1e-3)
                 t = sorted(times)[len(times) // 2]
                 vb = 8 if vdt == "f64" else 4
-                byts = A.nnz * (vb + ib) + (A.nrows + 1) * 4 + 4 * nslab + 2 * A.nrows * m * 8
-                out.append({"m": m, "values": vdt, "idx": idx, "us": t * 1e6,
+                byts = (A.nnz * (vb + ib) + (A.nrows + 1) * 4 + 4 * nslab
+                        + 2 * A.nrows * m * (8 if vec == "f64" else 4))
+                out.append({"m": m, "values": vdt, "idx": idx, "vectors": vec, "us": t * 1e6,
                             "GBps": byts / t / 1e9, "frac": byts / t / 1e9 / peak,
                             "kernel": "stream (TMA-fed, csrc/stream.cu)"
                             if _lib.lib().mrs_stream_launches() > sl0 else "lane family (csrc/spmm.cuh)"})

@@ -110,6 +110,12 @@ typedef struct {
  * separately rounded mul/add: bitwise equal to the reference kernel. */
 int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m,
                  int32_t mode, const double* b, void* stream);
+/* Extension (no reference counterpart: its vectors are always float64): the same
+ * product on float32 block vectors -- loads widened, float64 accumulation in entry
+ * order, one rounding at the store.  m in {1, 2, 4, 8, 16, 32}; 16/32-bit columns;
+ * 16-byte aligned vectors. */
+int mrs_csr_spmv_f32(const mrs_csr* A, const float* x, float* y, int64_t m,
+                     int32_t mode, const float* b, void* stream);
 /* Diagnostics: launches of the single-RHS stream kernel (csrc/stream.cu) made by
  * this process so far -- lets tests and the bench see which path a product took. */
 int64_t mrs_stream_launches(void);

@@ -78,6 +78,8 @@ _lib = None
 SIGNATURES = {
     "mrs_csr_spmv": (C.c_int, [C.POINTER(mrs_csr), C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
                                C.c_void_p, C.c_void_p]),
+    "mrs_csr_spmv_f32": (C.c_int, [C.POINTER(mrs_csr), C.c_void_p, C.c_void_p, C.c_int64, C.c_int32,
+                                   C.c_void_p, C.c_void_p]),
     "mrs_axpby": (C.c_int, [C.c_int64, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                             C.c_void_p]),
     "mrs_add2_scaled": (C.c_int, [C.c_int64, C.c_int64] + [C.c_void_p] * 6),

@@ -174,9 +174,29 @@ const char* mrs_status_string(int32_t s) {
     return "unknown status";
 }
 
+static int spmv_common(const mrs_csr* A, const double* x, double* y, int64_t m, int32_t mode,
+                       const double* b, void* stream, int vp);
+
 // _ckernels.pyx:30-57
 int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_t mode,
                  const double* b, void* stream) {
+    return spmv_common(A, x, y, m, mode, b, stream, VP_DD);
+}
+
+// The same product on float32 block vectors (an extension: the reference's vectors
+// are always float64): loads widened, accumulation in float64 in CSR entry order,
+// ONE rounding at the store -- y = float(acc).  m in {1, 2, 4, 8, 16, 32}.
+int mrs_csr_spmv_f32(const mrs_csr* A, const float* x, float* y, int64_t m, int32_t mode,
+                     const float* b, void* stream) {
+    if (m < 1 || m > 32 || (m & (m - 1)) != 0) return MRS_ERR_UNSUPPORTED;
+    if (A && A->idx_bytes == 1) return MRS_ERR_UNSUPPORTED;
+    if (!aligned16(x) || !aligned16(y) || (b && !aligned16(b))) return MRS_ERR_UNSUPPORTED;
+    return spmv_common(A, reinterpret_cast<const double*>(x), reinterpret_cast<double*>(y), m, mode,
+                       reinterpret_cast<const double*>(b), stream, VP_FF);
+}
+
+static int spmv_common(const mrs_csr* A, const double* x, double* y, int64_t m, int32_t mode,
+                       const double* b, void* stream, int vp) {
     if (!A || !m_ok(m) || mode < 0 || mode > 3) return MRS_ERR_ARG;
     if (A->idx_bytes != 1 && A->idx_bytes != 2 && A->idx_bytes != 4) return MRS_ERR_ARG;
     if (A->val_bytes != 4 && A->val_bytes != 8) return MRS_ERR_ARG;
@@ -206,10 +226,10 @@ int mrs_csr_spmv(const mrs_csr* A, const double* x, double* y, int64_t m, int32_
     D.padded = (A->flags & 1) != 0;
     // unaligned views fall back to the scalar-per-column kernel
     bool vec_ok = aligned16(x) && aligned16(y) && (!b || aligned16(b));
-    if (vec_ok) D.variant = plugin_variant(D, x, m, (cudaStream_t)stream);
+    if (vec_ok && vp == VP_DD) D.variant = plugin_variant(D, x, m, (cudaStream_t)stream);
     SpArgs a;
     memset(&a, 0, sizeof(a));
-    a.x = x; a.y = y; a.b = b; a.mode = mode;
+    a.x = x; a.y = y; a.b = b; a.mode = mode; a.vp = vp;
     cudaError_t e = launch_spmm(OP_SPMV, D, a, m, (cudaStream_t)stream, !vec_ok && m > 1);
     return e == cudaSuccess ? MRS_OK : MRS_ERR_CUDA;
 }

@@ -40,11 +40,11 @@ def _stream():
     return C.c_void_p(torch.cuda.current_stream().cuda_stream)
 
 
-def _vec(t, name):
+def _vec(t, name, dtype=torch.float64):
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise InvalidArgumentError(f"{name} must be a CUDA tensor (no CPU fallback)")
-    if t.dtype != torch.float64 or t.dim() != 2 or not t.is_contiguous():
-        raise InvalidArgumentError(f"{name} must be a contiguous (n, m) float64 tensor")
+    if t.dtype != dtype or t.dim() != 2 or not t.is_contiguous():
+        raise InvalidArgumentError(f"{name} must be a contiguous (n, m) {dtype} tensor")
     return t
 
 
@@ -175,7 +175,11 @@ def _csr_view(row_ptr, col_idx, values, nrows, ncols):
 
 def csr_spmv(row_ptr, col_idx, values, x, y, mode, b=None):
     """y op= A x (_ckernels.pyx:30-57).  ``row_ptr`` may be a DeviceCsr, in which
-    case ``col_idx``/``values`` are ignored."""
+    case ``col_idx``/``values`` are ignored.
+
+    Extension: float32 block vectors (x, y and b all float32; the reference's
+    are always float64) -- loads widened, float64 accumulation in entry order,
+    one rounding at the store; m in {1, 2, 4, 8, 16, 32}."""
     if isinstance(row_ptr, DeviceCsr):
         view = row_ptr.view()
         ncols = row_ptr.ncols
@@ -184,7 +188,8 @@ def csr_spmv(row_ptr, col_idx, values, x, y, mode, b=None):
             row_ptr = row_ptr.to(torch.int32)
         ncols = x.shape[0]
         view = _csr_view(row_ptr, col_idx, values, row_ptr.numel() - 1, ncols)
-    _vec(x, "x"); _vec(y, "y")
+    vdt = x.dtype if isinstance(x, torch.Tensor) and x.dtype == torch.float32 else torch.float64
+    _vec(x, "x", vdt); _vec(y, "y", vdt)
     if mode not in (0, 1, 2, 3):
         raise ValueError(f"unknown spmv mode {mode}")
     if y.shape[0] != view.nrows or x.shape[1] != y.shape[1]:
@@ -194,12 +199,12 @@ def csr_spmv(row_ptr, col_idx, values, x, y, mode, b=None):
         raise InvalidArgumentError("spmv output must not alias the input")
     bp = None
     if mode == MODE_RSUB:
-        _vec(b, "b")
+        _vec(b, "b", vdt)
         if b.shape != y.shape:
             raise ShapeMismatchError("b and y shapes differ")
         bp = b.data_ptr()
-    _ck(_lib.lib().mrs_csr_spmv(C.byref(view), x.data_ptr(), y.data_ptr(), x.shape[1], mode, bp,
-                                _stream()), "csr_spmv")
+    fn = _lib.lib().mrs_csr_spmv if vdt == torch.float64 else _lib.lib().mrs_csr_spmv_f32
+    _ck(fn(C.byref(view), x.data_ptr(), y.data_ptr(), x.shape[1], mode, bp, _stream()), "csr_spmv")
 
 
 def _same(*ts):

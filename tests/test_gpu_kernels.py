@@ -297,3 +297,30 @@ def test_every_spmm_variant_bitwise(m, variant, rng):
                 np.testing.assert_array_equal(y, ref, err_msg=f"variant {variant} mode {mode}")
     finally:
         _lib.set_option("spmm_variant", 0)
+
+
+@pytest.mark.parametrize("m", [1, 2, 4, 8, 16, 32])
+@pytest.mark.parametrize("vdt", [np.float64, np.float32])
+def test_spmv_float32_vectors_bitwise(m, vdt, rng):
+    """csr_spmv on float32 block vectors (extension): fp64 accumulation in entry
+    order, ONE rounding at the store -- equal to the oracle kernel run on the
+    widened operands and rounded once, every mode, plain and slab indices."""
+    from mrs_testutil import random_csr
+    n = 30000
+    blk = random_csr(n, n, 11.0, rng)
+    vals = blk.values.astype(vdt)
+    x = rng.standard_normal((n, m)).astype(np.float32)
+    b = rng.standard_normal((n, m)).astype(np.float32)
+    y0 = rng.standard_normal((n, m)).astype(np.float32)
+    for slab in (False, True):
+        D = K.DeviceCsr(blk.row_ptr, blk.col_idx, vals, n, n, slab=slab)
+        for mode in range(4):
+            y = T(y0)
+            K.csr_spmv(D, None, None, T(x), y, mode, T(b) if mode == 3 else None)
+            ref = y0.astype(np.float64)
+            O.csr_spmv(blk.row_ptr, blk.col_idx, vals, x.astype(np.float64), ref, mode,
+                       b.astype(np.float64) if mode == 3 else None)
+            np.testing.assert_array_equal(y.cpu().numpy(), ref.astype(np.float32),
+                                          err_msg=f"mode {mode} slab {slab}")
+    with pytest.raises(Exception):                       # mixed vector types are rejected
+        K.csr_spmv(D, None, None, T(x), T(y0.astype(np.float64)), 0)
