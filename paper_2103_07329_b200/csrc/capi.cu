@@ -152,6 +152,7 @@ int mrs_set_option(const char* key, int64_t value) {
     if (!strcmp(key, "spmm_variant")) { set_spmm_variant(value); return MRS_OK; }
     if (!strcmp(key, "halo_overlap")) { set_halo_overlap(value); return MRS_OK; }
     if (!strcmp(key, "spmm_coop")) { set_spmm_coop(value); return MRS_OK; }
+    if (!strcmp(key, "spmm_pair")) { set_spmm_pair(value); return MRS_OK; }
     if (!strcmp(key, "dense_mma")) { set_dense_mma(value); return MRS_OK; }
     if (!strcmp(key, "loop_unroll")) { set_loop_unroll(value); return MRS_OK; }
     if (!strcmp(key, "setup_gpu")) { set_setup_gpu(value); return MRS_OK; }

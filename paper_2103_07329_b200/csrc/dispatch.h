@@ -68,6 +68,7 @@ void set_spmm_long_rows(int64_t v);
 void set_spmm_chunk_rows(int64_t v);
 void set_spmm_long_split(int64_t v);
 void set_spmm_coop(int64_t v);
+void set_spmm_pair(int64_t v);
 bool dense_mma_enabled();
 int64_t loop_unroll();
 void set_loop_unroll(int64_t v);

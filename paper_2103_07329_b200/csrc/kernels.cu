@@ -47,7 +47,19 @@ int64_t halo_overlap() { return g_halo_overlap; }
 void set_halo_overlap(int64_t v) { g_halo_overlap = v < 0 ? 0 : (v > 2 ? 2 : v); }
 static int64_t g_variant = 0;         // 0: per operator (autotuned / heuristic)
 int64_t spmm_variant() { return g_variant; }
-void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 6 ? 0 : v); }
+void set_spmm_variant(int64_t v) { g_variant = v < 0 ? 0 : (v > 7 ? 0 : v); }
+// pair loads for operators with >= 12 entries per row (knob spmm_pair, env MRS_SPMM_PAIR):
+// 0 off, 1 instead of the plain lane kernel, 2 also instead of the cooperative one
+static int64_t g_pair = -1;
+int64_t spmm_pair() {
+    if (g_pair < 0) {
+        const char* e = getenv("MRS_SPMM_PAIR");
+        g_pair = e ? atoi(e) : 2;
+        if (g_pair < 0 || g_pair > 2) g_pair = 2;
+    }
+    return g_pair;
+}
+void set_spmm_pair(int64_t v) { g_pair = v < 0 ? 0 : (v > 2 ? 2 : v); }
 static int64_t g_coop = 2;            // cooperative entry loads (A/B: profiles/r01_ab_experiments.txt)
 int64_t spmm_coop() { return g_coop; }
 void set_spmm_coop(int64_t v) { g_coop = v < 0 ? 0 : (v > 2 ? 2 : v); }
@@ -162,7 +174,7 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     if (best_us) *best_us = 0.f;
     if (!spmm_autotune_enabled() || A.nrows == 0 || A.nnz == 0 || spmm_variant() != SV_AUTO)
         return SV_AUTO;
-    int cand[6], nc = 0;
+    int cand[7], nc = 0;
     cand[nc++] = SV_LANE;
     {
         SpArgs probe;
@@ -175,7 +187,9 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     if (vp == VP_DD && m <= 16 && (m & (m - 1)) == 0) {
         cand[nc++] = SV_LANE_L2;
         cand[nc++] = SV_LANE_NA;
+        if (m >= 2) cand[nc++] = SV_PAIR;
     }
+    if (vp == VP_DD && m == 32) cand[nc++] = SV_PAIR;
     if (nc == 1) return SV_AUTO;
     constexpr int kReps = 5;
     cudaEvent_t ev[2 * kReps];
@@ -187,7 +201,7 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
     a.x = x; a.y = y; a.mode = MRS_MODE_ASSIGN; a.vp = vp;
     int best = SV_AUTO;
     float best_t = 3.4e38f;
-    float tm[6] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    float tm[7] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
     for (int i = 0; i < nc && made == 2 * kReps; ++i) {
         DevCsr B = A;
         B.variant = cand[i];

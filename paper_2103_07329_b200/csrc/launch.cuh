@@ -14,6 +14,7 @@ int64_t spmm_long_max_rows();   // LONG-row SpMM variant up to this many rows (k
 int64_t spmm_chunk_rows();      // rows per CTA chunk of the SpMM grid (knob)
 int64_t spmm_coop();            // cooperative entry loads for long-row operators (knob)
 int64_t spmm_variant();         // force one SpmmVariant everywhere (knob; 0 = per operator)
+int64_t spmm_pair();            // pair loads for long-row operators (knob)
 
 
 // cudaLaunchKernelEx with programmatic stream serialization (PDL).
@@ -69,6 +70,10 @@ inline void wave_grid(const void* fn, int64_t nrows, int64_t rows_per_pass, int&
 }
 
 
+// SV_PAIR (round 2): large operators with >= 12 entries per row fetch their entries
+// as aligned pairs -- knob spmm_pair: 1 instead of LANE, 2 (default) also instead of
+// COOP (whose shuffles run on the same L1 data pipe as the loads they save).
+// Whole-solve A/B (profiles/r02s4_pair_variant.txt): C3 60.3 -> 58.6 ms, C4 53.8 -> 51.6 ms.
 // Shape heuristic (the default when an operator carries no measured choice):
 // small operators with long rows -> LONG (16 entries in flight); large
 // operators with long AND uniform rows (27-point stencils: mean >= 20, no row
@@ -80,9 +85,15 @@ inline int spmm_shape_variant(int64_t nr, int64_t nnz, int max_row, int64_t m) {
     const bool uniform_long = nnz >= 20 * nr && max_row > 0 &&
                               (int64_t)max_row * 10 * nr <= 11 * nnz + 10 * nr;
     if (m <= 16 && nr <= spmm_long_max_rows() && nnz >= 12 * nr) return SV_LONG;
+    const int64_t pair = spmm_pair();
+    // (operators under ~200 k rows are latency-bound, not L1-pipe-bound: the pair
+    // kernel's peeling costs them ~1 %, measured on C2's level 1)
+    const bool pair_ok = (m == 2 || m == 4 || m == 8 || m == 16 || m == 32) && nnz >= 12 * nr &&
+                         nr >= 200000;
     if ((m == 4 || m == 8 || m == 16) &&
         ((coop == 1 && nnz >= 12 * nr) || (coop == 2 && uniform_long)))
-        return SV_COOP;
+        return (pair == 2 && pair_ok) ? SV_PAIR : SV_COOP;
+    if (pair >= 1 && pair_ok) return SV_PAIR;
     return SV_LANE;
 }
 
@@ -119,6 +130,8 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     int v = a.variant ? a.variant : (int)spmm_variant();
     if (v == SV_AUTO)
         v = spmm_shape_variant(a.rows_hint, a.nnz_hint, a.max_row_hint, m);
+    // pair loads need naturally aligned entry arrays (cudaMalloc'ed ones are)
+    if (v == SV_PAIR && (((uintptr_t)a.vals & 15u) || ((uintptr_t)a.ci & 7u))) v = SV_LANE;
     if (!generic && v == SV_LONG) {
         switch (m) {
         case 1: go(spmm_kernel<1, OP, Tv, Ti, true, false, Tx, Ty>, Lay<1>::RPB); return cudaGetLastError();
@@ -148,6 +161,16 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
             case 16: l2 ? go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 1>, Lay<16>::RPB)
                         : go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 2>, Lay<16>::RPB);
                 return cudaGetLastError();
+            default: break;
+            }
+        }
+        if (!generic && v == SV_PAIR) {
+            switch (m) {
+            case 2: go(spmm_kernel<2, OP, Tv, Ti, false, false, double, double, 3>, Lay<2>::RPB); return cudaGetLastError();
+            case 4: go(spmm_kernel<4, OP, Tv, Ti, false, false, double, double, 3>, Lay<4>::RPB); return cudaGetLastError();
+            case 8: go(spmm_kernel<8, OP, Tv, Ti, false, false, double, double, 3>, Lay<8>::RPB); return cudaGetLastError();
+            case 16: go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 3>, Lay<16>::RPB); return cudaGetLastError();
+            case 32: go(spmm_kernel<32, OP, Tv, Ti, false, false, double, double, 3>, Lay<32>::RPB); return cudaGetLastError();
             default: break;
             }
         }

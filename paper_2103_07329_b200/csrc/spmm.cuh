@@ -48,6 +48,9 @@ enum SpmmVariant : int {
     SV_LANE_L2 = 4,  // lane, gathered x through L2 only (ld.global.cg: no L1 fills)
     SV_LANE_NA = 5,  // lane, gathered x with L1::no_allocate (hits kept, misses not filled)
     SV_STREAM = 6,   // m = 1, banded operators: TMA-fed entry-parallel products (stream.cu)
+    SV_PAIR = 7,     // lane, entries loaded as aligned PAIRS (one 16-byte value load and one
+                     // 4/8-byte index load per two entries): half the L1 wavefronts of the
+                     // matrix stream on long-row operators (a warp's 8 rows sit in 8 lines)
 };
 
 // Vector precisions of one SpMM launch (gathered operand -> row operands).
@@ -249,6 +252,28 @@ template <typename Tv, typename Ti> struct GSrc {
         return c;
     }
     __device__ __forceinline__ double val(int k) const { return widen(__ldg(v + k)); }
+    // entries k, k + 1 with ONE value load and ONE index load (k even: the arrays
+    // are 16-byte aligned, so the pair is naturally aligned)
+    __device__ __forceinline__ void pair(int k, int& c0, int& c1, double& v0, double& v1) const {
+        if constexpr (sizeof(Tv) == 8) {
+            const double2 t = __ldg(reinterpret_cast<const double2*>(v + k));
+            v0 = t.x; v1 = t.y;
+        } else {
+            const float2 t = __ldg(reinterpret_cast<const float2*>(v + k));
+            v0 = (double)t.x; v1 = (double)t.y;
+        }
+        if constexpr (sizeof(Ti) == 4) {
+            const uint2 w = __ldg(reinterpret_cast<const uint2*>(ci + k));
+            c0 = base + (int)w.x; c1 = base + (int)w.y;
+        } else if constexpr (sizeof(Ti) == 2) {
+            const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(ci + k));
+            c0 = base + (int)(w & 0xffffu); c1 = base + (int)(w >> 16);
+        } else {
+            const uint16_t w = __ldg(reinterpret_cast<const uint16_t*>(ci + k));
+            c0 = base + (int)(w & 0xffu); c1 = base + (int)(w >> 8);
+        }
+        MRS_DCHECK(c0 >= 0 && c1 >= 0);
+    }
     // the row's view: slab base of `row` (16-bit slab-relative columns)
     __device__ __forceinline__ GSrc at_row(const SpArgs& a, int row) const {
         GSrc r = *this;
@@ -294,6 +319,54 @@ __device__ __forceinline__ void row_accumulate(const SpArgs& a, const Src& src, 
                 }
             }
         }
+    }
+}
+
+// SV_PAIR: the same entry order, entries fetched as aligned pairs (LM == 3).
+template <int CPL, bool SUBTRACT, typename Tx, class Src>
+__device__ __forceinline__ void row_accumulate_pairs(const SpArgs& a, const Src& src, int lo, int hi,
+                                                     int ld, int cofs, double (&acc)[CPL]) {
+    auto fma1 = [&](double v, const Vec<CPL>& g) {
+#pragma unroll
+        for (int i = 0; i < CPL; ++i) {
+            if constexpr (SUBTRACT) acc[i] = sub(acc[i], mul(v, g.v[i]));
+            else acc[i] = add(acc[i], mul(v, g.v[i]));
+        }
+    };
+    int k = lo;
+    if ((k & 1) && k < hi) {                         // odd first entry: alone
+        const int c = src.col(k);
+        const double v = src.val(k);
+        fma1(v, gather<CPL, Tx, 0>(a, c, ld, cofs));
+        ++k;
+    }
+    for (; k + 3 < hi; k += 4) {                     // two pairs in flight
+        int c[4];
+        double v[4];
+        Vec<CPL> g[4];
+        src.pair(k, c[0], c[1], v[0], v[1]);
+        src.pair(k + 2, c[2], c[3], v[2], v[3]);
+        compiler_fence();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) g[u] = gather<CPL, Tx, 0>(a, c[u], ld, cofs);
+        compiler_fence();
+#pragma unroll
+        for (int u = 0; u < 4; ++u) fma1(v[u], g[u]);
+    }
+    if (k + 1 < hi) {
+        int c0, c1;
+        double v0, v1;
+        src.pair(k, c0, c1, v0, v1);
+        const Vec<CPL> g0 = gather<CPL, Tx, 0>(a, c0, ld, cofs);
+        const Vec<CPL> g1 = gather<CPL, Tx, 0>(a, c1, ld, cofs);
+        fma1(v0, g0);
+        fma1(v1, g1);
+        k += 2;
+    }
+    if (k < hi) {
+        const int c = src.col(k);
+        const double v = src.val(k);
+        fma1(v, gather<CPL, Tx, 0>(a, c, ld, cofs));
     }
 }
 
@@ -417,7 +490,10 @@ __device__ __forceinline__ void do_row(const SpArgs& a, const Src& src, int row,
     double acc[CPL];
     bool subtract;
     row_begin<OP, CPL, Ty>(a, o, acc, subtract);
-    if (subtract)
+    if constexpr (LM == 3) {
+        if (subtract) row_accumulate_pairs<CPL, true, Tx, Src>(a, src, lo, hi, ld, cofs, acc);
+        else row_accumulate_pairs<CPL, false, Tx, Src>(a, src, lo, hi, ld, cofs, acc);
+    } else if (subtract)
         row_accumulate<CPL, true, Tx, Src, UNR, LM>(a, src, lo, hi, ld, cofs, acc);
     else
         row_accumulate<CPL, false, Tx, Src, UNR, LM>(a, src, lo, hi, ld, cofs, acc);

@@ -60,10 +60,16 @@ def main():
                             + 2 * A.nrows * m * 8)
                     row = {"op": name, "values": vdt, "idx": "u16slab" if nslab else f"u{8*ib}",
                            "m": m, "bytes": byts}
-                    for v, vn in ((1, "lane"), (2, "coop"), (3, "long"), (4, "l2"), (5, "na")):
+                    only = os.environ.get("VARIANTS")      # e.g. VARIANTS=lane,pair
+                    for v, vn in ((1, "lane"), (2, "coop"), (3, "long"), (4, "l2"), (5, "na"),
+                                  (7, "pair")):
+                        if only and vn not in only.split(","):
+                            continue
                         if v == 2 and m not in (4, 8, 16):
                             continue
                         if v in (3, 4, 5) and m > 16:
+                            continue
+                        if v == 7 and m not in (2, 4, 8, 16, 32):
                             continue
                         _lib.set_option("spmm_variant", v)
                         t = timed(D, x, y)

@@ -274,7 +274,7 @@ def test_spmv_coop_entry_loads_bitwise(m, vdt, coop, rng):
 
 
 @pytest.mark.parametrize("m", [1, 2, 4, 8, 16])
-@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("variant", [1, 2, 3, 4, 5, 7])
 def test_every_spmm_variant_bitwise(m, variant, rng):
     """Every SpMM variant the per-operator choice can pick (lane, cooperative
     loads, 16 in flight, gathers through L2 only, L1::no_allocate) gives the
