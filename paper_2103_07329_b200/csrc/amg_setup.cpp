@@ -174,6 +174,9 @@ void sort_rows(Csr& A) {
         std::vector<std::pair<int64_t, double>> row;
         for (int64_t i = r0; i < r1; ++i) {
             int64_t lo = A.rp[i], hi = A.rp[i + 1];
+            bool sorted = true;
+            for (int64_t k = lo + 1; k < hi && sorted; ++k) sorted = A.ci[k - 1] <= A.ci[k];
+            if (sorted) continue;
             row.clear();
             for (int64_t k = lo; k < hi; ++k) row.emplace_back(A.ci[k], A.v[k]);
             std::sort(row.begin(), row.end(),
@@ -312,23 +315,26 @@ Csr from_host(const mrs_host_csr* h) {
     A.nrows = h->nrows; A.ncols = h->ncols;
     A.rp.assign(h->row_ptr, h->row_ptr + h->nrows + 1);
     A.ci.resize(h->nnz); A.v.resize(h->nnz);
-    for (int64_t k = 0; k < h->nnz; ++k) {
-        A.ci[k] = h->idx_bytes == 4 ? ((const uint32_t*)h->col_idx)[k]
-                : h->idx_bytes == 2 ? ((const uint16_t*)h->col_idx)[k]
-                                    : ((const uint8_t*)h->col_idx)[k];
-        A.v[k] = h->val_bytes == 8 ? ((const double*)h->values)[k]
-                                   : (double)((const float*)h->values)[k];
-    }
+    for_row_parts(h->nnz, setup_threads(), [&](int64_t k0, int64_t k1, int) {
+        for (int64_t k = k0; k < k1; ++k) {
+            A.ci[k] = h->idx_bytes == 4 ? ((const uint32_t*)h->col_idx)[k]
+                    : h->idx_bytes == 2 ? ((const uint16_t*)h->col_idx)[k]
+                                        : ((const uint8_t*)h->col_idx)[k];
+            A.v[k] = h->val_bytes == 8 ? ((const double*)h->values)[k]
+                                       : (double)((const float*)h->values)[k];
+        }
+    });
     return A;
 }
 
 void export_csr(const Csr& A, bool reduced, std::vector<float>& vf, std::vector<uint32_t>& ci) {
     ci.resize(A.nnz());
-    for (int64_t k = 0; k < A.nnz(); ++k) ci[k] = (uint32_t)A.ci[k];
-    if (reduced) {
-        vf.resize(A.nnz());
-        for (int64_t k = 0; k < A.nnz(); ++k) vf[k] = (float)A.v[k];
-    }
+    if (reduced) vf.resize(A.nnz());
+    for_row_parts(A.nnz(), setup_threads(), [&](int64_t k0, int64_t k1, int) {
+        for (int64_t k = k0; k < k1; ++k) ci[k] = (uint32_t)A.ci[k];
+        if (reduced)
+            for (int64_t k = k0; k < k1; ++k) vf[k] = (float)A.v[k];
+    });
 }
 
 }  // namespace
@@ -343,7 +349,7 @@ int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarc
     std::vector<Csr> chain;
     chain.push_back(from_host(Ah));
     sort_rows(chain.back());
-    std::vector<Csr> Ps;
+    std::vector<Csr> Ps, Rs;
     const bool timing = getenv("MRS_SETUP_TIMING") != nullptr;
     double tphase[6] = {0, 0, 0, 0, 0, 0};
     auto now = [] { return std::chrono::steady_clock::now(); };
@@ -389,6 +395,7 @@ int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarc
         tphase[0] += secs(t0, t1); tphase[1] += secs(t1, t2); tphase[2] += secs(t2, t3);
         tphase[3] += secs(t3, t4); tphase[4] += secs(t4, t5); tphase[5] += secs(t5, t6);
         Ps.push_back(std::move(P));
+        Rs.push_back(std::move(R));
         chain.push_back(std::move(Ac));
     }
     if (timing)
@@ -405,7 +412,7 @@ int mrs_amg_setup(const mrs_host_csr* Ah, const mrs_amg_params* prm, mrs_hierarc
         if (l < Ps.size()) {
             lv.hasP = true;
             lv.P = std::move(Ps[l]);
-            lv.R = transpose(lv.P);
+            lv.R = std::move(Rs[l]);
             export_csr(lv.P, lv.reduced, lv.Pf, lv.Pci);
             export_csr(lv.R, lv.reduced, lv.Rf, lv.Rci);
         }

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cub/device/device_scan.cuh>
+#include <thread>
 
 namespace mrs {
 
@@ -260,6 +261,18 @@ __global__ void __launch_bounds__(kT2Threads) spgemm_cta_kernel(PArgs a) {
     }
 }
 
+// fn(lo, hi) over contiguous ranges of [0, n) on host threads
+template <class Fn> void host_parallel(int64_t n, Fn fn) {
+    const int parts = (int)std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    if (parts <= 1 || n < (1 << 16)) { fn((int64_t)0, n); return; }
+    std::vector<std::thread> th;
+    for (int p = 0; p < parts; ++p) {
+        const int64_t lo = n * p / parts, hi = n * (p + 1) / parts;
+        th.emplace_back([=, &fn] { fn(lo, hi); });
+    }
+    for (auto& t : th) t.join();
+}
+
 int sm_count() {
     int dev = 0, sms = 0;
     cudaGetDevice(&dev);
@@ -270,15 +283,18 @@ int sm_count() {
 bool upload(const HostCsrView& H, DCsr& D) {
     D.nrows = H.nrows; D.ncols = H.ncols; D.nnz = H.rp[H.nrows];
     if (H.ncols >= INT32_MAX || H.nrows >= INT32_MAX) return false;
-    Buf tmp;
     if (cudaMalloc(&D.rp, (H.nrows + 1) * 8) != cudaSuccess) return false;
     if (cudaMalloc(&D.ci, std::max<int64_t>(D.nnz, 1) * 4) != cudaSuccess) return false;
     if (cudaMalloc(&D.v, std::max<int64_t>(D.nnz, 1) * 8) != cudaSuccess) return false;
-    if (!tmp.alloc((size_t)D.nnz * 8)) return false;
     if (cudaMemcpy(D.rp, H.rp, (H.nrows + 1) * 8, cudaMemcpyHostToDevice) != cudaSuccess) return false;
     if (D.nnz) {
-        if (cudaMemcpy(tmp.p, H.ci, D.nnz * 8, cudaMemcpyHostToDevice) != cudaSuccess) return false;
-        narrow_kernel<<<1024, 256>>>(tmp.as<int64_t>(), D.ci, D.nnz);
+        // columns narrowed to 32 bits on the host threads: half the PCIe bytes
+        std::vector<int32_t> c32((size_t)D.nnz);
+        const int64_t* src = H.ci;
+        host_parallel(D.nnz, [&](int64_t lo, int64_t hi) {
+            for (int64_t k = lo; k < hi; ++k) c32[k] = (int32_t)src[k];
+        });
+        if (cudaMemcpy(D.ci, c32.data(), D.nnz * 4, cudaMemcpyHostToDevice) != cudaSuccess) return false;
         if (cudaMemcpy(D.v, H.v, D.nnz * 8, cudaMemcpyHostToDevice) != cudaSuccess) return false;
     }
     return cudaDeviceSynchronize() == cudaSuccess;
@@ -388,15 +404,15 @@ bool galerkin_gpu(const HostCsrView& R, const HostCsrView& A, const HostCsrView&
     if (ok) {
         const int64_t n = dC.nrows, nnz = dC.nnz;
         rp.resize(n + 1); ci.resize(nnz); v.resize(nnz);
-        Buf wide;
-        ok = wide.alloc((size_t)std::max<int64_t>(nnz, 1) * 8);
-        if (ok) {
-            widen_kernel<<<1024, 256>>>(dC.ci, wide.as<int64_t>(), nnz);
-            ok = cudaMemcpy(rp.data(), dC.rp, (n + 1) * 8, cudaMemcpyDeviceToHost) == cudaSuccess &&
-                 (nnz == 0 ||
-                  (cudaMemcpy(ci.data(), wide.p, nnz * 8, cudaMemcpyDeviceToHost) == cudaSuccess &&
-                   cudaMemcpy(v.data(), dC.v, nnz * 8, cudaMemcpyDeviceToHost) == cudaSuccess));
-        }
+        std::vector<int32_t> c32((size_t)nnz);
+        ok = cudaMemcpy(rp.data(), dC.rp, (n + 1) * 8, cudaMemcpyDeviceToHost) == cudaSuccess &&
+             (nnz == 0 ||
+              (cudaMemcpy(c32.data(), dC.ci, nnz * 4, cudaMemcpyDeviceToHost) == cudaSuccess &&
+               cudaMemcpy(v.data(), dC.v, nnz * 8, cudaMemcpyDeviceToHost) == cudaSuccess));
+        if (ok)
+            host_parallel(nnz, [&](int64_t lo, int64_t hi) {
+                for (int64_t k = lo; k < hi; ++k) ci[k] = c32[k];
+            });
     }
     dC.release();
     if (!ok) { cudaGetLastError(); return false; }
