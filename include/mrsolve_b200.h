@@ -361,6 +361,9 @@ int  mrs_version(void);
  *   "plan_autotune" 0/1  solver plans: the same measurement for every level
  *                   operator at finalize (default 0: the shape heuristic)
  * (Measured-and-rejected variants are listed in profiles/r01_ab_experiments.txt.) */
+/* (round 2 keys: "spmm_pair" 0/1/2 pair loads on long-row operators, default 2;
+ *  "spmm_variant" 0..7 force one SpMM variant (6 = m=1 stream kernel, 7 = pair loads);
+ *  "setup_gpu" 0/1 Galerkin products of mrs_amg_setup on the GPU, default 1) */
 int  mrs_set_option(const char* key, int64_t value);
 
 #ifdef __cplusplus

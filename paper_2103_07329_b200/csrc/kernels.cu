@@ -189,7 +189,6 @@ int spmm_tune(const DevCsr& A, const double* x, double* y, int64_t m, cudaStream
         cand[nc++] = SV_LANE_NA;
         if (m >= 2) cand[nc++] = SV_PAIR;
     }
-    if (vp == VP_DD && m == 32) cand[nc++] = SV_PAIR;
     if (nc == 1) return SV_AUTO;
     constexpr int kReps = 5;
     cudaEvent_t ev[2 * kReps];

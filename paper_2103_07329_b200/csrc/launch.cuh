@@ -88,7 +88,7 @@ inline int spmm_shape_variant(int64_t nr, int64_t nnz, int max_row, int64_t m) {
     const int64_t pair = spmm_pair();
     // (operators under ~200 k rows are latency-bound, not L1-pipe-bound: the pair
     // kernel's peeling costs them ~1 %, measured on C2's level 1)
-    const bool pair_ok = (m == 2 || m == 4 || m == 8 || m == 16 || m == 32) && nnz >= 12 * nr &&
+    const bool pair_ok = (m == 2 || m == 4 || m == 8 || m == 16) && nnz >= 12 * nr &&
                          nr >= 200000;
     if ((m == 4 || m == 8 || m == 16) &&
         ((coop == 1 && nnz >= 12 * nr) || (coop == 2 && uniform_long)))
@@ -131,7 +131,7 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
     if (v == SV_AUTO)
         v = spmm_shape_variant(a.rows_hint, a.nnz_hint, a.max_row_hint, m);
     // pair loads need naturally aligned entry arrays (cudaMalloc'ed ones are)
-    if (v == SV_PAIR && (((uintptr_t)a.vals & 15u) || ((uintptr_t)a.ci & 7u))) v = SV_LANE;
+    if (v == SV_PAIR && (((uintptr_t)a.vals & 15u) || ((uintptr_t)a.ci & 15u))) v = SV_LANE;
     if (!generic && v == SV_LONG) {
         switch (m) {
         case 1: go(spmm_kernel<1, OP, Tv, Ti, true, false, Tx, Ty>, Lay<1>::RPB); return cudaGetLastError();
@@ -170,7 +170,6 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
             case 4: go(spmm_kernel<4, OP, Tv, Ti, false, false, double, double, 3>, Lay<4>::RPB); return cudaGetLastError();
             case 8: go(spmm_kernel<8, OP, Tv, Ti, false, false, double, double, 3>, Lay<8>::RPB); return cudaGetLastError();
             case 16: go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 3>, Lay<16>::RPB); return cudaGetLastError();
-            case 32: go(spmm_kernel<32, OP, Tv, Ti, false, false, double, double, 3>, Lay<32>::RPB); return cudaGetLastError();
             default: break;
             }
         }

@@ -288,7 +288,11 @@ def gs_sweep(row_ptr, col_idx, values, diag_pos, b, c, x, forward):
     v = b - c, v -= a_ik x_k for k != diag_pos[i] in entry order, x_i = v / a_ii,
     rows ascending (``forward``) or descending -- bitwise the sequential
     sweep, run level by level on one thread-block cluster (csrc/sgs.cuh).
-    ``row_ptr`` may be a DeviceCsr (``col_idx``/``values`` then ignored)."""
+    ``row_ptr`` may be a DeviceCsr (``col_idx``/``values`` then ignored).
+
+    Off the hot path: this plugin entry is SYNCHRONOUS and rebuilds the level
+    schedule on the host from the device structure on every call (solver plans
+    build theirs once at upload and replay it inside the solve graph)."""
     if isinstance(row_ptr, DeviceCsr):
         view = row_ptr.view()
     else:

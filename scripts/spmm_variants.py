@@ -69,7 +69,7 @@ def main():
                             continue
                         if v in (3, 4, 5) and m > 16:
                             continue
-                        if v == 7 and m not in (2, 4, 8, 16, 32):
+                        if v == 7 and m not in (2, 4, 8, 16):
                             continue
                         _lib.set_option("spmm_variant", v)
                         t = timed(D, x, y)
