@@ -256,41 +256,53 @@ bool interp(const Csr& A, const Csr& S, const std::vector<int8_t>& st, Csr& P,
         if (st[i] == C) cmap[i] = nc++;
     P = Csr();
     P.nrows = n; P.ncols = nc;
-    P.rp.assign(n + 1, 0);
     bad.clear();
-    std::vector<double> diag, off, sel;
-    std::vector<int64_t> selc;
-    std::vector<char> strong_mark(n, 0);
-    for (int64_t i = 0; i < n; ++i) {
-        if (st[i] == C) {
-            P.ci.push_back(cmap[i]); P.v.push_back(1.0);
-            P.rp[i + 1] = P.nnz();
-            continue;
+    // rows are independent: row-parallel on the host threads, each row computed
+    // exactly as in the sequential loop (same pairwise sums, same entry order)
+    const int parts = std::max<int>(1, std::min<int64_t>(setup_threads(),
+                                                         (int64_t)(2e9 / (double)(n + 1))));
+    RowParts rows(parts);
+    std::vector<std::vector<int64_t>> badp(parts);
+    for_row_parts(n, parts, [&](int64_t r0, int64_t r1, int part) {
+        std::vector<double> diag, off, sel;
+        std::vector<int64_t> selc;
+        std::vector<char> strong_mark(n, 0);
+        auto& len = rows.len[part];
+        auto& oc = rows.ci[part];
+        auto& ov = rows.v[part];
+        for (int64_t i = r0; i < r1; ++i) {
+            if (st[i] == C) {
+                oc.push_back(cmap[i]); ov.push_back(1.0);
+                len.push_back(1);
+                continue;
+            }
+            for (int64_t k = S.rp[i]; k < S.rp[i + 1]; ++k) strong_mark[S.ci[k]] = 1;
+            diag.clear(); off.clear(); sel.clear(); selc.clear();
+            for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
+                const int64_t c = A.ci[k];
+                if (c == i) diag.push_back(A.v[k]);
+                else off.push_back(A.v[k]);
+                if (strong_mark[c] && st[c] == C) { sel.push_back(A.v[k]); selc.push_back(c); }
+            }
+            for (int64_t k = S.rp[i]; k < S.rp[i + 1]; ++k) strong_mark[S.ci[k]] = 0;
+            if (sel.empty()) {
+                badp[part].push_back(i);
+                len.push_back(0);
+                continue;
+            }
+            const double a_ii = pairwise_sum(diag.data(), (int64_t)diag.size());
+            const double off_sum = pairwise_sum(off.data(), (int64_t)off.size());
+            const double strong_sum = pairwise_sum(sel.data(), (int64_t)sel.size());
+            const double ratio = off_sum / strong_sum;
+            for (size_t q = 0; q < sel.size(); ++q) {
+                oc.push_back(cmap[selc[q]]);
+                ov.push_back((-(sel[q] / a_ii)) * ratio);
+            }
+            len.push_back((int64_t)sel.size());
         }
-        for (int64_t k = S.rp[i]; k < S.rp[i + 1]; ++k) strong_mark[S.ci[k]] = 1;
-        diag.clear(); off.clear(); sel.clear(); selc.clear();
-        for (int64_t k = A.rp[i]; k < A.rp[i + 1]; ++k) {
-            const int64_t c = A.ci[k];
-            if (c == i) diag.push_back(A.v[k]);
-            else off.push_back(A.v[k]);
-            if (strong_mark[c] && st[c] == C) { sel.push_back(A.v[k]); selc.push_back(c); }
-        }
-        for (int64_t k = S.rp[i]; k < S.rp[i + 1]; ++k) strong_mark[S.ci[k]] = 0;
-        if (sel.empty()) {
-            bad.push_back(i);
-            P.rp[i + 1] = P.nnz();
-            continue;
-        }
-        const double a_ii = pairwise_sum(diag.data(), (int64_t)diag.size());
-        const double off_sum = pairwise_sum(off.data(), (int64_t)off.size());
-        const double strong_sum = pairwise_sum(sel.data(), (int64_t)sel.size());
-        const double ratio = off_sum / strong_sum;
-        for (size_t q = 0; q < sel.size(); ++q) {
-            P.ci.push_back(cmap[selc[q]]);
-            P.v.push_back((-(sel[q] / a_ii)) * ratio);
-        }
-        P.rp[i + 1] = P.nnz();
-    }
+    });
+    rows.into(P);
+    for (auto& bp : badp) bad.insert(bad.end(), bp.begin(), bp.end());
     return bad.empty();
 }
 
