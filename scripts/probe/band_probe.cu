@@ -1249,6 +1249,151 @@ __global__ void __launch_bounds__(TT * NT + 32, 1) k_stream3(S2Args a) {
     }
 }
 
+
+// ------------------------------------------------------------------ direct (m = 1, 2)
+// The stream producer (entry ring per team + sliding x window) with thread-per-row
+// consumers that accumulate straight from the staged entries (no product buffer):
+// NT teams of TT threads; team q owns sub-blocks q, q + NT, ... and a private ring of ST
+// slots that holds one whole sub-block.
+template <int M, int TT, int NT, int LSE, int ST>
+__global__ void __launch_bounds__(TT * NT + 32, 1) k_direct(S2Args a) {
+    constexpr int T = TT * NT, SE = 1 << LSE, NS = ST * NT, STB = SE * 12;
+    extern __shared__ __align__(128) unsigned char sm[];
+    const int WCAP = a.wcap;
+    double* xs = reinterpret_cast<double*>(sm);                              // WCAP x M
+    unsigned char* ring = reinterpret_cast<unsigned char*>(xs + (size_t)WCAP * M);
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + NS * STB);
+    uint64_t* empty = full + NS;
+    int* slot_rb = reinterpret_cast<int*>(empty + NS);
+    int* iss = slot_rb + NS;
+    int* rel = iss + NT;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) { mb_init(full + s, 1); mb_init(empty + s, TT / 32); }
+        for (int q = 0; q < NT; ++q) { iss[q] = 0; rel[q] = 0; }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const int R0 = min(a.n, (int)blockIdx.x * a.rows_per_cta);
+    const int R1 = min(a.n, R0 + a.rows_per_cta);
+    if (R0 >= R1) return;
+    const int nsb = (R1 - R0 + TT - 1) / TT;
+    if (threadIdx.x >= T) {
+        // ---------------- producer warp
+        const int lane = threadIdx.x - T;
+        int whi = max(0, R0 - a.band) & ~1;
+        auto release_one = [&](int q) {
+            const int r = rel[q];
+            mb_wait(empty + q * ST + r % ST, (r / ST) & 1);
+            rel[q] = r + 1;
+        };
+        for (int sb0 = 0; sb0 < nsb; sb0 += 32) {
+            const int rbj = min(R1, R0 + (sb0 + lane) * TT);
+            const int ebj = __ldg(a.rp + rbj);
+            int eej = __shfl_down_sync(~0u, ebj, 1);
+            if (lane == 31) eej = __ldg(a.rp + min(R1, rbj + TT));
+            const int cntj = min(32, nsb - sb0);
+            for (int j = 0; j < cntj; ++j) {
+                const int eb = __shfl_sync(~0u, ebj, j), ee = __shfl_sync(~0u, eej, j);
+                if (lane != 0) continue;
+                const int q = (sb0 + j) % NT;
+                const int rb = R0 + (sb0 + j) * TT, re = min(R1, rb + TT);
+                bool first = true;
+                for (int cs = eb & ~7; cs < ee; cs += SE, first = false) {
+                    while (rel[q] < iss[q] - ST + 1) release_one(q);
+                    const int slot = q * ST + iss[q] % ST;
+                    const int len = min(SE, (ee - cs + 7) & ~7);
+                    uint32_t tx = (uint32_t)len * 12;
+                    int wnew = whi;
+                    if (first) {
+                        wnew = min(a.n, (re + a.band + 1) & ~1);
+                        if (wnew > whi) {
+                            for (int t = 0; t < NT; ++t)
+                                while (rel[t] < iss[t] && wnew - WCAP > slot_rb[t * ST + rel[t] % ST] - a.band)
+                                    release_one(t);
+                            tx += (uint32_t)(wnew - whi) * M * 8;
+                        } else wnew = whi;
+                    }
+                    slot_rb[slot] = rb;
+                    mb_expect(full + slot, tx);
+                    unsigned char* st = ring + slot * STB;
+                    bulk_g2s(st, a.ci + cs, (uint32_t)len * 4, full + slot);
+                    bulk_g2s(st + SE * 4, a.v + cs, (uint32_t)len * 8, full + slot);
+                    for (int c = whi; c < wnew;) {
+                        const int sl = c % WCAP;
+                        const int cnt = min(min(wnew - c, WCAP - sl), 32768 / (M * 8));
+                        bulk_g2s(xs + (size_t)sl * M, a.x + (size_t)c * M, (uint32_t)cnt * M * 8, full + slot);
+                        c += cnt;
+                    }
+                    whi = wnew;
+                    iss[q] += 1;
+                }
+            }
+        }
+        return;
+    }
+    // ---------------- consumers: one thread per row
+    const int team = threadIdx.x / TT, tt = threadIdx.x % TT;
+    int it = 0;
+    for (int sb = team; sb < nsb; sb += NT) {
+        const int rb = R0 + sb * TT, re = min(R1, rb + TT);
+        const int row = rb + tt;
+        const int eb = __ldg(a.rp + rb), ee = __ldg(a.rp + re);
+        int lo = 0, hi = 0;
+        if (row < re) { lo = __ldg(a.rp + row); hi = __ldg(a.rp + row + 1); }
+        const int a0 = eb & ~7;
+        const int nst = ee > a0 ? (ee - a0 + SE - 1) >> LSE : 0;
+        const int wbase = max(0, rb - a.band) & ~1;
+        const int wofs = wbase % WCAP - wbase;
+        for (int j = 0; j < nst; ++j) mb_wait(full + team * ST + (it + j) % ST, ((it + j) / ST) & 1);
+        double acc[M];
+#pragma unroll
+        for (int i = 0; i < M; ++i) acc[i] = 0.0;
+        int e = lo;
+        while (e < hi) {
+            const int j = (e - a0) >> LSE;
+            const int send = min(hi, a0 + ((j + 1) << LSE));           // entries of this stage
+            const unsigned char* st = ring + (size_t)(team * ST + (it + j) % ST) * STB;
+            const uint32_t* sc = reinterpret_cast<const uint32_t*>(st) - (a0 + (j << LSE));
+            const double* sv = reinterpret_cast<const double*>(st + SE * 4) - (a0 + (j << LSE));
+            constexpr int U = 4;
+            for (; e < send; e += U) {
+                int sl[U]; double v[U]; double px[U][M];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = min(e + u, send - 1);
+                    sl[u] = wofs + (int)sc[k];
+                    v[u] = sv[k];
+                }
+                fence();
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (sl[u] >= WCAP) sl[u] -= WCAP;
+                    if constexpr (M == 1) px[u][0] = xs[sl[u]];
+                    else {
+                        const double2 t = *reinterpret_cast<const double2*>(xs + 2 * sl[u]);
+                        px[u][0] = t.x; px[u][1] = t.y;
+                    }
+                }
+                fence();
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (e + u < send)
+#pragma unroll
+                        for (int i = 0; i < M; ++i) acc[i] = add(acc[i], mul(v[u], px[u][i]));
+            }
+            e = send;
+        }
+        if (row < re) {
+            if constexpr (M == 1) a.y[row] = acc[0];
+            else *reinterpret_cast<double2*>(a.y + 2 * (size_t)row) = make_double2(acc[0], acc[1]);
+        }
+        bar_team(1 + team, TT);
+        if (threadIdx.x % 32 == 0)
+            for (int j = 0; j < nst; ++j) mb_arrive(empty + team * ST + (it + j) % ST);
+        it += nst;
+    }
+}
+
 // ------------------------------------------------------------------ tile (m >= 4)
 // Band-tile format: rows in blocks of R, each block's column window cut into tiles
 // of W columns; tile = packed [u16 ptr[R+8] | u16 col[ne] (tile-relative) | f64 val[ne]],
@@ -1570,6 +1715,41 @@ template <int M> static void bench(const Csr& A, int band) {
             check(buf, y, (size_t)A.n * M, us, bytes);
         };
 
+
+        auto direct = [&](auto kern, int TT, int NT, int LSE, int ST, const char* name) {
+            if (!want(name)) return;
+            const int SE = 1 << LSE;
+            S2Args t = {};
+            t.rp = a.rp; t.ci = a.ci; t.v = a.v; t.x = a.x; t.y = y; t.n = A.n; t.band = band;
+            t.wcap = (2 * band + (NT + 1) * TT + 256 + 1) & ~1;
+            const int grid = S;
+            t.rows_per_cta = (((A.n + grid - 1) / grid + TT - 1) / TT) * TT;
+            int mxs = 0;
+            for (int r = 0; r < A.n; r += TT) {
+                const int eb = A.rp[r], ee = A.rp[std::min(A.n, r + TT)];
+                if (ee > (eb & ~7)) mxs = std::max(mxs, (ee - (eb & ~7) + SE - 1) / SE);
+            }
+            if (mxs > ST) { printf("  %s: a sub-block needs %d stages > %d\n", name, mxs, ST); return; }
+            const size_t smem = (size_t)t.wcap * M * 8 + (size_t)ST * NT * SE * 12 + ST * NT * 20 + NT * 8 + 16;
+            if (smem > 227 * 1024) { printf("  %s: smem %zu too large\n", name, smem); return; }
+            CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            float us = time_us([&] { kern<<<grid, TT * NT + 32, smem>>>(t); });
+            char buf[128];
+            snprintf(buf, sizeof buf, "%s TT%d NT%d SE%d ST%d (%zuK)", name, TT, NT, SE, ST, smem >> 10);
+            check(buf, y, (size_t)A.n * M, us, bytes);
+        };
+        if constexpr (M == 1) {
+            direct(k_direct<M, 256, 2, 10, 6>, 256, 2, 10, 6, "direct-a");
+            direct(k_direct<M, 128, 4, 9, 6>, 128, 4, 9, 6, "direct-b");
+            direct(k_direct<M, 128, 3, 9, 6>, 128, 3, 9, 6, "direct-c");
+            direct(k_direct<M, 256, 1, 10, 8>, 256, 1, 10, 8, "direct-d");
+            direct(k_direct<M, 192, 3, 9, 8>, 192, 3, 9, 8, "direct-e");
+        } else {
+            direct(k_direct<M, 128, 2, 9, 6>, 128, 2, 9, 6, "direct-a");
+            direct(k_direct<M, 64, 4, 8, 6>, 64, 4, 8, 6, "direct-b");
+            direct(k_direct<M, 96, 3, 8, 8>, 96, 3, 8, 8, "direct-c");
+            direct(k_direct<M, 128, 1, 9, 12>, 128, 1, 9, 12, "direct-d");
+        }
         auto stream3 = [&](auto kern, int TT, int NT, int SE, int Sg, int PCAP, int wcap, const char* name) {
             if (!want(name)) return;
             S2Args t = {};
