@@ -247,11 +247,20 @@ __global__ void __launch_bounds__(kSumT + kProdT + 32, 1) stream_spmv_kernel(StA
         constexpr int U2 = 4;
         const int klo = lo - a0, khi = hi - a0;
         MRS_DCHECK(klo >= 0 && khi <= PCAP);
-        for (int k = klo; k < khi; k += U2) {
-            double t[U2];
-#pragma unroll
-            for (int u = 0; u < U2; ++u) t[u] = P2[min(k + u, khi - 1)];
+        int k = klo;
+        if ((k & 1) && k < khi) {                    // odd first product: alone
+            const double t = P2[k];
+            acc = subtract ? sub(acc, t) : add(acc, t);
+            ++k;
+        }
+        // products as aligned pairs (16-byte shared loads: half the requests of the
+        // row-strided, bank-conflicting scalar reads), four per round
+        for (; k < khi; k += U2) {
+            const int k2 = min(k + 2, ((khi - 1) & ~1));      // second pair (clamped, aligned)
+            const double2 p0 = *reinterpret_cast<const double2*>(P2 + k);
+            const double2 p1 = *reinterpret_cast<const double2*>(P2 + k2);
             compiler_fence();
+            const double t[U2] = {p0.x, p0.y, p1.x, p1.y};
             if (subtract) {
 #pragma unroll
                 for (int u = 0; u < U2; ++u)
