@@ -142,6 +142,15 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
         default: break;
         }
     }
+    if (!generic && v == SV_PAIR) {          // any vector precision
+        switch (m) {
+        case 2: go(spmm_kernel<2, OP, Tv, Ti, false, false, Tx, Ty, 3>, Lay<2>::RPB); return cudaGetLastError();
+        case 4: go(spmm_kernel<4, OP, Tv, Ti, false, false, Tx, Ty, 3>, Lay<4>::RPB); return cudaGetLastError();
+        case 8: go(spmm_kernel<8, OP, Tv, Ti, false, false, Tx, Ty, 3>, Lay<8>::RPB); return cudaGetLastError();
+        case 16: go(spmm_kernel<16, OP, Tv, Ti, false, false, Tx, Ty, 3>, Lay<16>::RPB); return cudaGetLastError();
+        default: break;
+        }
+    }
     if constexpr (kF64) {
         if (!generic && (v == SV_LANE_L2 || v == SV_LANE_NA)) {
             const bool l2 = v == SV_LANE_L2;
@@ -161,15 +170,6 @@ inline cudaError_t spmm_m(SpArgs a, int64_t m, cudaStream_t s, bool generic) {
             case 16: l2 ? go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 1>, Lay<16>::RPB)
                         : go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 2>, Lay<16>::RPB);
                 return cudaGetLastError();
-            default: break;
-            }
-        }
-        if (!generic && v == SV_PAIR) {
-            switch (m) {
-            case 2: go(spmm_kernel<2, OP, Tv, Ti, false, false, double, double, 3>, Lay<2>::RPB); return cudaGetLastError();
-            case 4: go(spmm_kernel<4, OP, Tv, Ti, false, false, double, double, 3>, Lay<4>::RPB); return cudaGetLastError();
-            case 8: go(spmm_kernel<8, OP, Tv, Ti, false, false, double, double, 3>, Lay<8>::RPB); return cudaGetLastError();
-            case 16: go(spmm_kernel<16, OP, Tv, Ti, false, false, double, double, 3>, Lay<16>::RPB); return cudaGetLastError();
             default: break;
             }
         }
