@@ -295,13 +295,10 @@ cudaError_t stream_launch(const StArgs& a, cudaStream_t s) {
     constexpr int S = stream_stages<Ti, Tv>();
     auto kern = stream_spmv_kernel<Tv, Ti, S>;
     const size_t smem = stream_smem(a.band, (int)(sizeof(Ti) + sizeof(Tv)), S);
-    static bool attr_set = false;       // per instantiation
-    if (!attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             227 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_set = true;
-    }
+    // (per launch: the attribute is per device, and a process may drive several)
+    cudaError_t ea = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          227 * 1024);
+    if (ea != cudaSuccess) return ea;
     const int nblk = (a.n + kSumT - 1) / kSumT;
     const int grid = std::max(1, std::min(num_sms(), nblk));
     StArgs b = a;
